@@ -1,0 +1,210 @@
+/*
+ * evr.h -- C ABI of the B200-native per-packet event reconstruction
+ *          (arXiv 1607.06283), the drop-in for the evrecon hot path.
+ *
+ * The reference (/root/reference/pkg/src/evrecon) is a pure-Python/numpy
+ * package with no FFI; its "operator API" is the Python module surface.
+ * Each entry point below names the reference function it replaces
+ * (file:line).  The Python host package paper_1607_06283_b200 binds this
+ * header with ctypes and re-exports the reference names; INTEGRATION.md
+ * shows the binding a maintainer of the reference would add.
+ *
+ * Conventions
+ *  - Plain C: pointers + sizes, no C++ or torch types.  Every call returns
+ *    EVR_OK (0) or a negative evr_status; evr_last_error(ctx) describes the
+ *    last failure on that context.  Nothing throws across the ABI.
+ *  - Host arrays are row-major (H, W) float64 / int64, dual fields p are
+ *    (H, W, 3) float64 interleaved -- exactly the reference's numpy layouts.
+ *    Host pointers are borrowed for the duration of the call only.
+ *  - One evr_ctx per (event stream, device).  Calls on a context are
+ *    serialised on its own CUDA stream; use one host thread per context.
+ *  - EVR_PREC_F64 reproduces the reference bit for bit (every stage, every
+ *    packet).  EVR_PREC_F32 runs the surface and the solver in binary32
+ *    (ingest stays binary64/int64 and bit-exact); it is held to 1e-4
+ *    max-abs on log u against the reference.
+ */
+#ifndef EVR_H
+#define EVR_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define EVR_ABI_VERSION 1
+
+typedef enum {
+    EVR_OK = 0,
+    EVR_ERR_INVALID = -1,     /* bad argument (maps to ValueError) */
+    EVR_ERR_CUDA = -2,        /* CUDA runtime failure */
+    EVR_ERR_OOM = -3,         /* device allocation failed */
+    EVR_ERR_RANGE = -4,       /* event coordinate outside the sensor */
+    EVR_ERR_UNSUPPORTED = -5  /* shape/mode not supported by this call */
+} evr_status;
+
+typedef enum { EVR_PREC_F64 = 0, EVR_PREC_F32 = 1 } evr_precision;
+
+/* Solver-engine selection for the per-packet path. */
+typedef enum {
+    EVR_ENGINE_AUTO = 0,      /* resident when it fits, else streaming */
+    EVR_ENGINE_STREAMING = 1, /* one launch per half-step, fields in HBM/L2 */
+    EVR_ENGINE_RESIDENT = 2   /* persistent on-chip kernel (row bands) */
+} evr_engine;
+
+/* One camera event: events.py:35-43 Event(x, y, polarity, timestamp).
+ * 16 bytes, little endian; numpy dtype
+ * [('t','<i8'),('x','<i4'),('y','<i2'),('polarity','<i2')]. */
+typedef struct {
+    int64_t t;
+    int32_t x;
+    int16_t y;
+    int16_t polarity;
+} evr_event;
+
+/* SolverConfig (solve.py:41-78), ManifoldConfig (pipeline.py:71-84) and
+ * Thresholds (pipeline.py:51-68; c_pos/c_neg are host math.exp values). */
+typedef struct {
+    double lam, u_min, u_max, tau, sigma, convergence_tol;
+    int32_t max_iterations;
+    int32_t manifold_enabled;
+    double t_scale;
+    double denoise_weight;
+    int32_t denoise_iterations;
+    int32_t engine; /* evr_engine */
+    double c_pos, c_neg;
+} evr_config;
+
+/* SolveResult.iterations / .rel_change (solve.py:81-85). */
+typedef struct {
+    int32_t iterations;
+    int32_t _pad;
+    double rel_change;
+} evr_solve_info;
+
+typedef struct evr_ctx evr_ctx;
+
+/* ---- lifetime ---------------------------------------------------------- */
+const char *evr_version(void);
+int evr_device_count(int *count);
+/* A context for an H x W sensor on `device` (H, W >= 1; the stencil entry
+ * points need H, W >= 2 like the reference's div_xy, surface.py:107-121). */
+int evr_create(evr_ctx **out, int device, int height, int width, int precision);
+void evr_destroy(evr_ctx *ctx);
+const char *evr_last_error(const evr_ctx *ctx);
+int evr_set_config(evr_ctx *ctx, const evr_config *cfg);
+/* engine actually used by the per-packet path (after AUTO resolution) */
+int evr_active_engine(evr_ctx *ctx, int *engine);
+
+/* ---- stream state: ReconstructionState (pipeline.py:87-111) ------------- */
+/* init_state (pipeline.py:102-111): u = f = (u_min+u_max)/2, raw = 0, p = 0 */
+int evr_init_state(evr_ctx *ctx);
+/* NULL pointers leave that field untouched. */
+int evr_set_state(evr_ctx *ctx, const double *u, const double *f,
+                  const int64_t *raw, const double *p);
+int evr_get_state(evr_ctx *ctx, double *u, double *f, int64_t *raw, double *p);
+
+/* ---- hot path ------------------------------------------------------------ */
+/* apply_event (pipeline.py:114-121) for n events in stream order, with
+ * update_timestamp_map (surface.py:124-127).  Bit-exact, duplicates
+ * included.  Host events. */
+int evr_ingest(evr_ctx *ctx, const evr_event *events, int64_t n);
+/* process_packet (pipeline.py:142-171) for a non-empty packet: ingest,
+ * normalize/denoise/metric (_packet_metric, pipeline.py:124-139), the
+ * warm-started primal_dual_solve and the f <- u re-anchor.  `window` is the
+ * surface window the host derived from packet_starts (pipeline.py:128-132;
+ * ignored when the manifold is disabled).  Synchronous; host events. */
+int evr_process_packet(evr_ctx *ctx, const evr_event *events, int64_t n,
+                       double window, evr_solve_info *info);
+/* Same, asynchronous: enqueue on the context stream and return.  Host
+ * events are staged through pinned memory before the call returns. */
+int evr_process_packet_async(evr_ctx *ctx, const evr_event *events, int64_t n,
+                             double window);
+/* Same, events already resident in device memory (`dev_events`). */
+int evr_process_packet_device(evr_ctx *ctx, const evr_event *dev_events,
+                              int64_t n, double window);
+/* process_packet in two halves, for callers that look at the surface
+ * between them (debug_sink, pipeline.py:162-163) or need the host-driven
+ * solve (convergence_tol > 0 early stop, per-iteration energy trace rows
+ * of solve.py:255-256).  begin = ingest + surface; solve = primal-dual +
+ * re-anchor.  energy_trace / rel_trace have max_iterations slots (NULL ok);
+ * info->iterations says how many were filled. */
+int evr_packet_begin(evr_ctx *ctx, const evr_event *events, int64_t n,
+                     double window);
+int evr_packet_solve(evr_ctx *ctx, evr_solve_info *info, double *energy_trace,
+                     double *rel_trace);
+/* Wait for queued packets; info (may be NULL) gets the last packet's result. */
+int evr_synchronize(evr_ctx *ctx, evr_solve_info *info);
+/* Current frame u (the value process_packet returns), float64 (H, W). */
+int evr_get_frame(evr_ctx *ctx, double *u_out);
+/* Last packet's denoised surface t and metric determinant G (the
+ * debug_sink view, pipeline.py:162-163).  Either pointer may be NULL. */
+int evr_get_surface(evr_ctx *ctx, double *t_out, double *G_out);
+/* Last packet's metric field (compute_metric / flat_metric outputs). */
+int evr_get_metric(evr_ctx *ctx, double *tx, double *ty, double *G, double *sqrtG);
+/* Frame quantised to 8-bit gray on device (pgm.py:14-22 to_gray,
+ * floor(255*(u-lo)/(hi-lo)+0.5) clipped to [0,255]). */
+int evr_get_frame_u8(evr_ctx *ctx, double lo, double hi, uint8_t *out);
+/* Device pointer of the event staging buffer with room for `n` events
+ * (grows on demand); for zero-copy producers. */
+int evr_event_buffer(evr_ctx *ctx, int64_t n, evr_event **dev_ptr);
+/* CUDA stream handle (cudaStream_t) the context runs on. */
+void *evr_stream(evr_ctx *ctx);
+/* Count of kernel launches this context issued (graph nodes included). */
+int64_t evr_launch_count(const evr_ctx *ctx);
+
+/* ---- operator-level API on host arrays of the context's shape ----------- */
+/* grad_x / grad_y (surface.py:93-104) */
+int evr_op_grad(evr_ctx *ctx, const double *u, double *gx, double *gy);
+/* div_xy (surface.py:107-121) */
+int evr_op_div(evr_ctx *ctx, const double *qx, const double *qy, double *out);
+/* normalize_timestamps (surface.py:130-143); raw as float64 like the
+ * reference's np.asarray(raw_map, dtype=np.float64) */
+int evr_op_normalize(evr_ctx *ctx, const double *raw, double now,
+                     double t_scale, double window, double *t_out);
+/* denoise_timestamps (surface.py:146-196) */
+int evr_op_denoise(evr_ctx *ctx, const double *t_in, double weight,
+                   int iterations, double t_scale, double *t_out);
+/* compute_metric (surface.py:199-205) */
+int evr_op_metric(evr_ctx *ctx, const double *t, double *tx, double *ty,
+                  double *G, double *sqrtG);
+/* MetricField.coeffs (surface.py:81-90): out = 5 planes a11,a12,a22,a31,a32 */
+int evr_op_coeffs(evr_ctx *ctx, const double *tx, const double *ty,
+                  const double *G, double *out5);
+/* surface_gradient (surface.py:214-236): out (H, W, 3) */
+int evr_op_surface_gradient(evr_ctx *ctx, const double *u, const double *tx,
+                            const double *ty, const double *G, double *out);
+/* surface_gradient_adjoint (surface.py:239-252): p (H, W, 3) -> out (H, W) */
+int evr_op_surface_gradient_adjoint(evr_ctx *ctx, const double *p,
+                                    const double *tx, const double *ty,
+                                    const double *G, double *out);
+/* prox_data (solve.py:88-100), elementwise */
+int evr_op_prox_data(evr_ctx *ctx, const double *u_bar, const double *f,
+                     const double *sqrtG, double tau, double lam, double u_min,
+                     double u_max, double *out);
+/* prox_dual (solve.py:103-108): p (H, W, 3) */
+int evr_op_prox_dual(evr_ctx *ctx, const double *p, const double *sqrtG,
+                     double *out);
+/* energy (solve.py:111-118) */
+int evr_op_energy(evr_ctx *ctx, const double *u, const double *f,
+                  const double *tx, const double *ty, const double *G,
+                  const double *sqrtG, double lam, double *out);
+/* primal_dual_solve (solve.py:207-261) on a given metric.  u_init / p_init
+ * may be NULL (defaults u = f, p = 0).  energy_trace / rel_trace (length
+ * cfg->max_iterations, may be NULL) receive the trace rows. */
+int evr_op_pd_solve(evr_ctx *ctx, const evr_config *cfg, const double *f,
+                    const double *tx, const double *ty, const double *G,
+                    const double *sqrtG, const double *u_init,
+                    const double *p_init, double *u_out, double *p_out,
+                    evr_solve_info *info, double *energy_trace,
+                    double *rel_trace);
+/* rof_manifold_solve (solve.py:264-293) */
+int evr_op_rof_solve(evr_ctx *ctx, const double *f, const double *tx,
+                     const double *ty, const double *G, const double *sqrtG,
+                     double lam, int iterations, double *u_out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* EVR_H */

@@ -1,0 +1,39 @@
+"""Reroute an imported reference evrecon through the B200 path.
+
+evrecon.pipeline binds primal_dual_solve and the surface functions at
+import (pipeline.py:22-29), and run_stream looks up init_state /
+process_packet in the pipeline module's globals (pipeline.py:228-229,
+:240).  Patching those two names there reroutes run_stream, `evrecon
+reconstruct` (cli.py:147-152) and `evrecon bench` (cli.py:273-274) onto
+the device state machine; patching evrecon.solve.primal_dual_solve alone
+would have no effect.
+"""
+
+from __future__ import annotations
+
+import sys
+
+_SAVED = {}
+
+
+def install(evrecon_pipeline=None):
+    """Patch evrecon.pipeline.{init_state, process_packet} (and the module's
+    primal_dual_solve binding) with this package's versions.  The reference
+    config dataclasses are duck-type compatible (same fields)."""
+    from . import pipeline as ours
+    from . import solve as ours_solve
+
+    mod = evrecon_pipeline or sys.modules.get("evrecon.pipeline")
+    if mod is None:
+        import evrecon.pipeline as mod  # noqa: F811
+    for name, repl in (("init_state", ours.init_state), ("process_packet", ours.process_packet),
+                       ("primal_dual_solve", ours_solve.primal_dual_solve)):
+        _SAVED.setdefault((id(mod), name), (mod, getattr(mod, name)))
+        setattr(mod, name, repl)
+    return mod
+
+
+def uninstall():
+    for (_, name), (mod, orig) in list(_SAVED.items()):
+        setattr(mod, name, orig)
+    _SAVED.clear()

@@ -1,0 +1,1068 @@
+// evr_capi.cu -- the C ABI (include/evr.h): per-stream device context,
+// captured CUDA graphs of the per-packet sequence, and the operator API.
+//
+// Engines
+//   streaming: one launch per half-step over HBM/L2-resident SoA planes
+//              (evr_kernels.cuh); the whole packet is one CUDA graph.
+//   resident : one persistent kernel per packet, state on chip in row bands
+//              (evr_resident.cuh); used when the sensor fits (AUTO).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/evr.h"
+#include "evr_kernels.cuh"
+#include "evr_resident.cuh"
+
+using namespace evr;
+
+namespace {
+
+constexpr int kNT = 256;          // 1-D block size
+constexpr int kIngestCH = 1024;   // ingest chunk / CTA size
+constexpr int kRedBlocks = 296;   // reduction partial blocks (2 x 148 SMs)
+
+enum Field {
+  F_U, F_UN, F_V, F_P1, F_P2, F_P3,
+  F_T, F_TU, F_TUB, F_TPX, F_TPY,
+  F_TX, F_TY, F_G, F_SG, F_A11, F_A12, F_A22, F_A31, F_A32, F_BETA, F_FB,
+  F_COUNT
+};
+
+}  // namespace
+
+struct evr_ctx {
+  int device = 0;
+  int H = 0, W = 0;
+  int64_t N = 0;
+  int prec = EVR_PREC_F64;
+  evr_config cfg{};
+  bool cfg_set = false;
+  cudaStream_t stream = nullptr;
+  // device memory
+  char* slab = nullptr;
+  size_t field_stride = 0;  // bytes between planes
+  double* f = nullptr;
+  int64_t* raw = nullptr;
+  double* aos_a = nullptr;  // (H, W, 3) staging
+  double* aos_b = nullptr;
+  double* part = nullptr;   // reduction partials
+  double* d_scalar = nullptr;
+  int* d_err = nullptr;
+  evr_solve_info* d_info = nullptr;
+  // packet staging: [PacketHdr | events...] on device and 2 pinned host slots
+  char* d_stage = nullptr;
+  char* h_stage[2] = {nullptr, nullptr};
+  cudaEvent_t stage_done[2] = {nullptr, nullptr};
+  int stage_slot = 0;
+  int64_t ev_cap = 0;
+  evr_solve_info* h_info = nullptr;
+  int64_t seq = 0;
+  // graphs: 0 = surface, 1 = solve, 2 = whole packet
+  cudaGraphExec_t graph[3] = {nullptr, nullptr, nullptr};
+  int64_t graph_launches[3] = {0, 0, 0};
+  int64_t launches = 0;
+  int engine = EVR_ENGINE_STREAMING;  // resolved
+  ResidentPlan rplan{};
+  unsigned* d_flags = nullptr;        // resident engine sync words
+  char* d_xchg = nullptr;             // resident engine halo exchange rows
+  size_t xchg_bytes = 0;
+  std::string err;
+
+  template <class T> T* fld(int k) const { return reinterpret_cast<T*>(slab + field_stride * k); }
+  PacketHdr* hdr() const { return reinterpret_cast<PacketHdr*>(d_stage); }
+};
+
+namespace {
+
+int fail(evr_ctx* c, int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  if (c) c->err = buf;
+  return code;
+}
+
+#define CK(call)                                                                      \
+  do {                                                                                \
+    cudaError_t e_ = (call);                                                          \
+    if (e_ != cudaSuccess)                                                            \
+      return fail(ctx, e_ == cudaErrorMemoryAllocation ? EVR_ERR_OOM : EVR_ERR_CUDA,  \
+                  "%s failed: %s", #call, cudaGetErrorString(e_));                    \
+  } while (0)
+
+#define CHECK_CTX()                                                   \
+  do {                                                                \
+    if (!ctx) return EVR_ERR_INVALID;                                 \
+    cudaError_t e_ = cudaSetDevice(ctx->device);                      \
+    if (e_ != cudaSuccess)                                            \
+      return fail(ctx, EVR_ERR_CUDA, "cudaSetDevice: %s", cudaGetErrorString(e_)); \
+  } while (0)
+
+inline dim3 grid2d(const evr_ctx* c) { return dim3((c->W + 31) / 32, (c->H + 7) / 8); }
+inline dim3 block2d() { return dim3(32, 8); }
+inline unsigned grid1d(int64_t n) { return (unsigned)((n + kNT - 1) / kNT); }
+inline int red_blocks(int64_t n) {
+  return (int)std::max<int64_t>(1, std::min<int64_t>(kRedBlocks, (n + kNT - 1) / kNT));
+}
+
+int launch_err(evr_ctx* ctx, const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(ctx, EVR_ERR_CUDA, "%s launch: %s", what, cudaGetErrorString(e));
+  return EVR_OK;
+}
+
+template <class T> CoefPlanes<T> coefs(const evr_ctx* c) {
+  return CoefPlanes<T>{c->fld<T>(F_A11), c->fld<T>(F_A12), c->fld<T>(F_A22), c->fld<T>(F_A31),
+                       c->fld<T>(F_A32)};
+}
+
+// ---- per-packet sequence (streaming engine) -------------------------------
+
+// ingest -> normalize -> TV-L1 -> metric (+ solver constants)
+template <class T> int enqueue_surface(evr_ctx* ctx) {
+  const evr_config& g = ctx->cfg;
+  cudaStream_t s = ctx->stream;
+  const int H = ctx->H, W = ctx->W;
+  const int64_t N = ctx->N;
+  k_ingest<kIngestCH><<<1, kIngestCH, 0, s>>>(ctx->hdr(), ctx->f, ctx->raw, H, W, g.c_pos,
+                                               g.c_neg, g.u_min, g.u_max, ctx->d_err);
+  int n = 1;
+  if (g.manifold_enabled) {
+    T *t = ctx->fld<T>(F_T), *tu = ctx->fld<T>(F_TU), *tub = ctx->fld<T>(F_TUB);
+    T *px = ctx->fld<T>(F_TPX), *py = ctx->fld<T>(F_TPY);
+    k_normalize_tvinit<T><<<grid1d(N), kNT, 0, s>>>(ctx->raw, ctx->hdr(), g.t_scale, t, tu, tub,
+                                                    px, py, N);
+    const double step = 1.0 / std::sqrt(8.0);  // surface.py:158
+    const T sigma = (T)step, tau = (T)step, shrink = (T)(step * g.denoise_weight);
+    for (int it = 0; it < g.denoise_iterations; ++it) {
+      k_tv_dual<T><<<grid2d(ctx), block2d(), 0, s>>>(tub, px, py, H, W, sigma);
+      k_tv_primal<T><<<grid2d(ctx), block2d(), 0, s>>>(px, py, tu, tub, t, H, W, tau, shrink);
+    }
+    k_tv_finish<T><<<grid1d(N), kNT, 0, s>>>(tu, t, (T)g.t_scale, N);
+    n += 2 + 2 * g.denoise_iterations;
+  }
+  k_metric_setup<T><<<grid2d(ctx), block2d(), 0, s>>>(
+      ctx->fld<T>(F_T), ctx->f, ctx->fld<T>(F_TX), ctx->fld<T>(F_TY), ctx->fld<T>(F_G),
+      ctx->fld<T>(F_SG), coefs<T>(ctx), ctx->fld<T>(F_BETA), ctx->fld<T>(F_FB), H, W,
+      (T)(g.tau * g.lam), g.manifold_enabled ? 0 : 1);
+  n += 1;
+  int rc = launch_err(ctx, "surface");
+  return rc ? rc : n;
+}
+
+// one KL primal-dual iteration: u (in `cur`) -> u+ (in `nxt`), p updated
+template <class T> void pd_iteration(evr_ctx* ctx, T* cur, T* nxt) {
+  const evr_config& g = ctx->cfg;
+  cudaStream_t s = ctx->stream;
+  T* v = ctx->fld<T>(F_V);
+  k_pd_primal<T><<<grid2d(ctx), block2d(), 0, s>>>(
+      ctx->fld<T>(F_P1), ctx->fld<T>(F_P2), ctx->fld<T>(F_P3), coefs<T>(ctx), cur,
+      ctx->fld<T>(F_BETA), ctx->fld<T>(F_FB), nxt, v, ctx->H, ctx->W, (T)g.tau, (T)g.u_min,
+      (T)g.u_max);
+  k_pd_dual<T><<<grid2d(ctx), block2d(), 0, s>>>(v, ctx->fld<T>(F_P1), ctx->fld<T>(F_P2),
+                                                 ctx->fld<T>(F_P3), coefs<T>(ctx),
+                                                 ctx->fld<T>(F_SG), ctx->H, ctx->W,
+                                                 (T)g.sigma);
+}
+
+template <class T> void relchange(evr_ctx* ctx, const T* un, const T* u, int iterations) {
+  const int nb = red_blocks(ctx->N);
+  k_relchange_partial<T, kNT><<<nb, kNT, 0, ctx->stream>>>(un, u, ctx->N, ctx->part);
+  k_relchange_final<kNT><<<1, kNT, 0, ctx->stream>>>(ctx->part, nb, ctx->d_info, iterations);
+}
+
+// fixed-iteration solve (convergence_tol == 0) + epilogue, graph-capturable
+template <class T> int enqueue_solve(evr_ctx* ctx) {
+  const int iters = ctx->cfg.max_iterations;
+  T* bufs[2] = {ctx->fld<T>(F_U), ctx->fld<T>(F_UN)};
+  int n = 0;
+  for (int it = 0; it < iters; ++it) {
+    T* cur = bufs[it & 1];
+    T* nxt = bufs[(it + 1) & 1];
+    if (it == iters - 1) {
+      // rel_change needs u_old and u+ both alive: run the primal, reduce, dual
+      const evr_config& g = ctx->cfg;
+      T* v = ctx->fld<T>(F_V);
+      k_pd_primal<T><<<grid2d(ctx), block2d(), 0, ctx->stream>>>(
+          ctx->fld<T>(F_P1), ctx->fld<T>(F_P2), ctx->fld<T>(F_P3), coefs<T>(ctx), cur,
+          ctx->fld<T>(F_BETA), ctx->fld<T>(F_FB), nxt, v, ctx->H, ctx->W, (T)g.tau,
+          (T)g.u_min, (T)g.u_max);
+      relchange<T>(ctx, nxt, cur, iters);
+      k_pd_dual<T><<<grid2d(ctx), block2d(), 0, ctx->stream>>>(
+          v, ctx->fld<T>(F_P1), ctx->fld<T>(F_P2), ctx->fld<T>(F_P3), coefs<T>(ctx),
+          ctx->fld<T>(F_SG), ctx->H, ctx->W, (T)g.sigma);
+      n += 4;
+    } else {
+      pd_iteration<T>(ctx, cur, nxt);
+      n += 2;
+    }
+  }
+  T* last = bufs[iters & 1];
+  k_epilogue<T><<<grid1d(ctx->N), kNT, 0, ctx->stream>>>(last, ctx->fld<T>(F_U), ctx->f, ctx->N);
+  n += 1;
+  int rc = launch_err(ctx, "solve");
+  return rc ? rc : n;
+}
+
+template <class T> int enqueue_packet(evr_ctx* ctx, int which) {
+  int n = 0, r;
+  if (which == 0 || which == 2) {
+    if ((r = enqueue_surface<T>(ctx)) < 0) return r;
+    n += r;
+  }
+  if (which == 1 || which == 2) {
+    if ((r = enqueue_solve<T>(ctx)) < 0) return r;
+    n += r;
+  }
+  return n;
+}
+
+int enqueue_packet_any(evr_ctx* ctx, int which) {
+  if (ctx->engine == EVR_ENGINE_RESIDENT) {
+    int r = ctx->prec == EVR_PREC_F64 ? resident_enqueue<double>(ctx, which)
+                                      : resident_enqueue<float>(ctx, which);
+    return r;
+  }
+  return ctx->prec == EVR_PREC_F64 ? enqueue_packet<double>(ctx, which)
+                                   : enqueue_packet<float>(ctx, which);
+}
+
+void drop_graphs(evr_ctx* ctx) {
+  for (auto& g : ctx->graph)
+    if (g) {
+      cudaGraphExecDestroy(g);
+      g = nullptr;
+    }
+}
+
+// Launch packet stage `which` (0 surface, 1 solve, 2 both) through a CUDA
+// graph captured on first use.
+int launch_stage(evr_ctx* ctx, int which) {
+  if (!ctx->graph[which]) {
+    cudaGraph_t graph;
+    CK(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+    int n = enqueue_packet_any(ctx, which);
+    cudaError_t e = cudaStreamEndCapture(ctx->stream, &graph);
+    if (n < 0) {
+      if (e == cudaSuccess) cudaGraphDestroy(graph);
+      return n;
+    }
+    CK(e);
+    e = cudaGraphInstantiate(&ctx->graph[which], graph, 0);
+    cudaGraphDestroy(graph);
+    CK(e);
+    ctx->graph_launches[which] = n;
+  }
+  CK(cudaGraphLaunch(ctx->graph[which], ctx->stream));
+  ctx->launches += ctx->graph_launches[which];
+  return EVR_OK;
+}
+
+int ensure_stage(evr_ctx* ctx, int64_t n) {
+  if (n <= ctx->ev_cap) return EVR_OK;
+  int64_t cap = std::max<int64_t>(n, std::max<int64_t>(4096, ctx->ev_cap * 2));
+  CK(cudaStreamSynchronize(ctx->stream));
+  for (int i = 0; i < 2; ++i)
+    if (ctx->h_stage[i]) cudaFreeHost(ctx->h_stage[i]);
+  if (ctx->d_stage) cudaFree(ctx->d_stage);
+  ctx->h_stage[0] = ctx->h_stage[1] = nullptr;
+  ctx->d_stage = nullptr;
+  const size_t bytes = sizeof(PacketHdr) + (size_t)cap * sizeof(evr_event);
+  CK(cudaMalloc(&ctx->d_stage, bytes));
+  CK(cudaMallocHost(&ctx->h_stage[0], bytes));
+  CK(cudaMallocHost(&ctx->h_stage[1], bytes));
+  ctx->ev_cap = cap;
+  drop_graphs(ctx);  // graphs bake the staging address
+  return EVR_OK;
+}
+
+int validate_events(evr_ctx* ctx, const evr_event* ev, int64_t n) {
+  for (int64_t k = 0; k < n; ++k)
+    if (ev[k].x < 0 || ev[k].x >= ctx->W || ev[k].y < 0 || ev[k].y >= ctx->H)
+      return fail(ctx, EVR_ERR_RANGE, "event %lld at (%d, %d) outside the %dx%d sensor",
+                  (long long)k, (int)ev[k].x, (int)ev[k].y, ctx->W, ctx->H);
+  return EVR_OK;
+}
+
+// Stage host events + header into pinned memory and copy them to the device.
+int stage_host_packet(evr_ctx* ctx, const evr_event* ev, int64_t n, double window) {
+  int rc;
+  if ((rc = validate_events(ctx, ev, n))) return rc;
+  if ((rc = ensure_stage(ctx, n))) return rc;
+  const int slot = ctx->stage_slot;
+  ctx->stage_slot ^= 1;
+  CK(cudaEventSynchronize(ctx->stage_done[slot]));  // previous copy from this slot
+  char* h = ctx->h_stage[slot];
+  PacketHdr hdr{n, ev[n - 1].t, window, ++ctx->seq};
+  std::memcpy(h, &hdr, sizeof hdr);
+  std::memcpy(h + sizeof hdr, ev, (size_t)n * sizeof(evr_event));
+  CK(cudaMemcpyAsync(ctx->d_stage, h, sizeof hdr + (size_t)n * sizeof(evr_event),
+                     cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaEventRecord(ctx->stage_done[slot], ctx->stream));
+  return EVR_OK;
+}
+
+// Device-resident events: copy into the staging slot (unless the producer
+// wrote there directly through evr_event_buffer) and fill the header.
+__global__ void k_stage_device(PacketHdr* hdr, evr_event* dst, const evr_event* __restrict__ src,
+                               int64_t n, double window, int64_t seq) {
+  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k < n && dst != src) dst[k] = src[k];
+  if (k == 0) {
+    hdr->n = n;
+    hdr->now = src[n - 1].t;
+    hdr->window = window;
+    hdr->seq = seq;
+  }
+}
+
+int stage_device_packet(evr_ctx* ctx, const evr_event* dev, int64_t n, double window) {
+  int rc;
+  if ((rc = ensure_stage(ctx, n))) return rc;
+  evr_event* dst = reinterpret_cast<evr_event*>(ctx->d_stage + sizeof(PacketHdr));
+  k_stage_device<<<grid1d(n), kNT, 0, ctx->stream>>>(ctx->hdr(), dst, dev, n, window, ++ctx->seq);
+  ctx->launches += 1;
+  return launch_err(ctx, "stage");
+}
+
+bool solve_needs_host_loop(const evr_ctx* ctx) { return ctx->cfg.convergence_tol > 0; }
+
+// Host-driven solve for convergence_tol > 0 and/or traces (solve.py:233-258):
+// rel_change every iteration, early stop, optional energy rows.
+template <class T>
+int solve_host_loop(evr_ctx* ctx, const evr_config& g, evr_solve_info* info, double* etrace,
+                    double* rtrace, bool write_state) {
+  const bool track = g.convergence_tol > 0 || etrace || rtrace;
+  T* bufs[2] = {ctx->fld<T>(F_U), ctx->fld<T>(F_UN)};
+  int iterations = 0, cur_i = 0;
+  double rel = INFINITY;
+  for (int it = 0; it < g.max_iterations; ++it) {
+    T* cur = bufs[cur_i];
+    T* nxt = bufs[cur_i ^ 1];
+    T* v = ctx->fld<T>(F_V);
+    k_pd_primal<T><<<grid2d(ctx), block2d(), 0, ctx->stream>>>(
+        ctx->fld<T>(F_P1), ctx->fld<T>(F_P2), ctx->fld<T>(F_P3), coefs<T>(ctx), cur,
+        ctx->fld<T>(F_BETA), ctx->fld<T>(F_FB), nxt, v, ctx->H, ctx->W, (T)g.tau, (T)g.u_min,
+        (T)g.u_max);
+    iterations = it + 1;
+    ctx->launches += 1;
+    if (track || it == g.max_iterations - 1) {
+      relchange<T>(ctx, nxt, cur, iterations);
+      ctx->launches += 2;
+    }
+    k_pd_dual<T><<<grid2d(ctx), block2d(), 0, ctx->stream>>>(
+        v, ctx->fld<T>(F_P1), ctx->fld<T>(F_P2), ctx->fld<T>(F_P3), coefs<T>(ctx),
+        ctx->fld<T>(F_SG), ctx->H, ctx->W, (T)g.sigma);
+    ctx->launches += 1;
+    cur_i ^= 1;
+    if (etrace) {
+      const int nb = red_blocks(ctx->N);
+      k_energy_partial<T, kNT><<<nb, kNT, 0, ctx->stream>>>(nxt, ctx->f, coefs<T>(ctx),
+                                                           ctx->fld<T>(F_G), ctx->fld<T>(F_SG),
+                                                           ctx->H, ctx->W, ctx->part);
+      k_energy_final<kNT><<<1, kNT, 0, ctx->stream>>>(ctx->part, nb, g.lam, ctx->d_scalar);
+      ctx->launches += 2;
+      CK(cudaMemcpyAsync(&etrace[it], ctx->d_scalar, sizeof(double), cudaMemcpyDeviceToHost,
+                         ctx->stream));
+    }
+    if (track) {
+      CK(cudaMemcpyAsync(ctx->h_info, ctx->d_info, sizeof(evr_solve_info),
+                         cudaMemcpyDeviceToHost, ctx->stream));
+      CK(cudaStreamSynchronize(ctx->stream));
+      rel = ctx->h_info->rel_change;
+      if (rtrace) rtrace[it] = rel;
+      if (g.convergence_tol > 0 && rel < g.convergence_tol) break;
+    }
+  }
+  T* last = bufs[cur_i];
+  if (write_state) {
+    k_epilogue<T><<<grid1d(ctx->N), kNT, 0, ctx->stream>>>(last, ctx->fld<T>(F_U), ctx->f,
+                                                          ctx->N);
+    ctx->launches += 1;
+  } else if (last != bufs[0]) {
+    CK(cudaMemcpyAsync(bufs[0], last, sizeof(T) * ctx->N, cudaMemcpyDeviceToDevice,
+                       ctx->stream));
+  }
+  int rc = launch_err(ctx, "solve loop");
+  if (rc) return rc;
+  CK(cudaMemcpyAsync(ctx->h_info, ctx->d_info, sizeof(evr_solve_info), cudaMemcpyDeviceToHost,
+                     ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  if (info) {
+    info->iterations = iterations;
+    info->rel_change = track ? rel : ctx->h_info->rel_change;
+  }
+  return EVR_OK;
+}
+
+int check_err_flag(evr_ctx* ctx) {
+  int h = 0;
+  CK(cudaMemcpy(&h, ctx->d_err, sizeof(int), cudaMemcpyDeviceToHost));
+  if (h) {
+    CK(cudaMemset(ctx->d_err, 0, sizeof(int)));
+    return fail(ctx, EVR_ERR_RANGE, "a device-side event lay outside the %dx%d sensor", ctx->W,
+                ctx->H);
+  }
+  return EVR_OK;
+}
+
+int require_config(evr_ctx* ctx) {
+  if (!ctx->cfg_set) return fail(ctx, EVR_ERR_INVALID, "evr_set_config has not been called");
+  return EVR_OK;
+}
+
+int require_f64(evr_ctx* ctx) {
+  if (ctx->prec != EVR_PREC_F64)
+    return fail(ctx, EVR_ERR_UNSUPPORTED, "operator API needs an EVR_PREC_F64 context");
+  return EVR_OK;
+}
+
+int require_stencil(evr_ctx* ctx) {
+  if (ctx->H < 2 || ctx->W < 2)
+    return fail(ctx, EVR_ERR_UNSUPPORTED, "stencil operators need H, W >= 2 (got %dx%d)",
+                ctx->H, ctx->W);
+  return EVR_OK;
+}
+
+template <class T> int set_state_t(evr_ctx* ctx, const double* u, const double* f,
+                                   const int64_t* raw, const double* p) {
+  const int64_t N = ctx->N;
+  cudaStream_t s = ctx->stream;
+  if (u) {
+    CK(cudaMemcpyAsync(ctx->aos_a, u, sizeof(double) * N, cudaMemcpyHostToDevice, s));
+    k_convert<double, T><<<grid1d(N), kNT, 0, s>>>(ctx->aos_a, ctx->fld<T>(F_U), N);
+  }
+  if (f) CK(cudaMemcpyAsync(ctx->f, f, sizeof(double) * N, cudaMemcpyHostToDevice, s));
+  if (raw) CK(cudaMemcpyAsync(ctx->raw, raw, sizeof(int64_t) * N, cudaMemcpyHostToDevice, s));
+  if (p) {
+    CK(cudaMemcpyAsync(ctx->aos_b, p, sizeof(double) * 3 * N, cudaMemcpyHostToDevice, s));
+    k_aos_to_planes<T><<<grid1d(N), kNT, 0, s>>>(ctx->aos_b, ctx->fld<T>(F_P1), ctx->fld<T>(F_P2),
+                                                 ctx->fld<T>(F_P3), N);
+  }
+  int rc = launch_err(ctx, "set_state");
+  if (rc) return rc;
+  CK(cudaStreamSynchronize(s));
+  return EVR_OK;
+}
+
+template <class T> int get_state_t(evr_ctx* ctx, double* u, double* f, int64_t* raw, double* p) {
+  const int64_t N = ctx->N;
+  cudaStream_t s = ctx->stream;
+  if (u) {
+    k_convert<T, double><<<grid1d(N), kNT, 0, s>>>(ctx->fld<T>(F_U), ctx->aos_a, N);
+    CK(cudaMemcpyAsync(u, ctx->aos_a, sizeof(double) * N, cudaMemcpyDeviceToHost, s));
+  }
+  if (f) CK(cudaMemcpyAsync(f, ctx->f, sizeof(double) * N, cudaMemcpyDeviceToHost, s));
+  if (raw) CK(cudaMemcpyAsync(raw, ctx->raw, sizeof(int64_t) * N, cudaMemcpyDeviceToHost, s));
+  if (p) {
+    k_planes_to_aos<T><<<grid1d(N), kNT, 0, s>>>(ctx->fld<T>(F_P1), ctx->fld<T>(F_P2),
+                                                 ctx->fld<T>(F_P3), ctx->aos_b, N);
+    CK(cudaMemcpyAsync(p, ctx->aos_b, sizeof(double) * 3 * N, cudaMemcpyDeviceToHost, s));
+  }
+  int rc = launch_err(ctx, "get_state");
+  if (rc) return rc;
+  CK(cudaStreamSynchronize(s));
+  return EVR_OK;
+}
+
+template <class T> int get_plane_t(evr_ctx* ctx, int field, double* out) {
+  k_convert<T, double><<<grid1d(ctx->N), kNT, 0, ctx->stream>>>(ctx->fld<T>(field), ctx->aos_a,
+                                                                ctx->N);
+  CK(cudaMemcpyAsync(out, ctx->aos_a, sizeof(double) * ctx->N, cudaMemcpyDeviceToHost,
+                     ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  return launch_err(ctx, "get_plane");
+}
+
+int h2d(evr_ctx* ctx, void* dst, const void* src, size_t bytes) {
+  CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, ctx->stream));
+  return EVR_OK;
+}
+
+int d2h_sync(evr_ctx* ctx, void* dst, const void* src, size_t bytes) {
+  CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  return EVR_OK;
+}
+
+}  // namespace
+
+// =========================================================================
+extern "C" {
+
+const char* evr_version(void) { return "evr-b200 0.1.0 (sm_100a)"; }
+
+int evr_device_count(int* count) {
+  if (!count) return EVR_ERR_INVALID;
+  cudaError_t e = cudaGetDeviceCount(count);
+  if (e != cudaSuccess) {
+    *count = 0;
+    return EVR_ERR_CUDA;
+  }
+  return EVR_OK;
+}
+
+const char* evr_last_error(const evr_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+int evr_create(evr_ctx** out, int device, int height, int width, int precision) {
+  if (!out) return EVR_ERR_INVALID;
+  *out = nullptr;
+  if (height < 1 || width < 1) return EVR_ERR_INVALID;
+  if (precision != EVR_PREC_F64 && precision != EVR_PREC_F32) return EVR_ERR_INVALID;
+  evr_ctx* ctx = new evr_ctx();
+  ctx->device = device;
+  ctx->H = height;
+  ctx->W = width;
+  ctx->N = (int64_t)height * width;
+  ctx->prec = precision;
+  auto bail = [&](int rc) {
+    std::string msg = ctx->err;
+    evr_destroy(ctx);
+    (void)msg;
+    return rc;
+  };
+  cudaError_t e = cudaSetDevice(device);
+  if (e != cudaSuccess) return bail(EVR_ERR_CUDA);
+  const size_t esz = precision == EVR_PREC_F64 ? 8 : 4;
+  ctx->field_stride = ((size_t)ctx->N * esz + 255) / 256 * 256;
+  const int64_t N = ctx->N;
+  int rc = [&]() -> int {
+    CK(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+    CK(cudaMalloc(&ctx->slab, ctx->field_stride * F_COUNT));
+    CK(cudaMemsetAsync(ctx->slab, 0, ctx->field_stride * F_COUNT, ctx->stream));
+    CK(cudaMalloc(&ctx->f, sizeof(double) * N));
+    CK(cudaMalloc(&ctx->raw, sizeof(int64_t) * N));
+    CK(cudaMalloc(&ctx->aos_a, sizeof(double) * 3 * N));
+    CK(cudaMalloc(&ctx->aos_b, sizeof(double) * 3 * N));
+    CK(cudaMalloc(&ctx->part, sizeof(double) * 2 * kRedBlocks));
+    CK(cudaMalloc(&ctx->d_scalar, sizeof(double) * 4));
+    CK(cudaMalloc(&ctx->d_err, sizeof(int)));
+    CK(cudaMemsetAsync(ctx->d_err, 0, sizeof(int), ctx->stream));
+    CK(cudaMalloc(&ctx->d_info, sizeof(evr_solve_info)));
+    CK(cudaMemsetAsync(ctx->d_info, 0, sizeof(evr_solve_info), ctx->stream));
+    CK(cudaMallocHost(&ctx->h_info, sizeof(evr_solve_info)));
+    for (int i = 0; i < 2; ++i) {
+      CK(cudaEventCreateWithFlags(&ctx->stage_done[i], cudaEventDisableTiming));
+      CK(cudaEventRecord(ctx->stage_done[i], ctx->stream));
+    }
+    CK(cudaStreamSynchronize(ctx->stream));
+    return EVR_OK;
+  }();
+  if (rc) return bail(rc);
+  *out = ctx;
+  return EVR_OK;
+}
+
+void evr_destroy(evr_ctx* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+  drop_graphs(ctx);
+  cudaFree(ctx->slab);
+  cudaFree(ctx->f);
+  cudaFree(ctx->raw);
+  cudaFree(ctx->aos_a);
+  cudaFree(ctx->aos_b);
+  cudaFree(ctx->part);
+  cudaFree(ctx->d_scalar);
+  cudaFree(ctx->d_err);
+  cudaFree(ctx->d_info);
+  cudaFree(ctx->d_stage);
+  cudaFree(ctx->d_flags);
+  cudaFree(ctx->d_xchg);
+  for (int i = 0; i < 2; ++i) {
+    if (ctx->h_stage[i]) cudaFreeHost(ctx->h_stage[i]);
+    if (ctx->stage_done[i]) cudaEventDestroy(ctx->stage_done[i]);
+  }
+  if (ctx->h_info) cudaFreeHost(ctx->h_info);
+  if (ctx->stream) cudaStreamDestroy(ctx->stream);
+  delete ctx;
+}
+
+int evr_set_config(evr_ctx* ctx, const evr_config* cfg) {
+  CHECK_CTX();
+  if (!cfg) return fail(ctx, EVR_ERR_INVALID, "null config");
+  if (cfg->max_iterations < 1) return fail(ctx, EVR_ERR_INVALID, "max_iterations must be >= 1");
+  if (cfg->manifold_enabled && cfg->denoise_iterations < 1)
+    return fail(ctx, EVR_ERR_INVALID, "denoise iterations must be >= 1");
+  if (!(0 < cfg->u_min && cfg->u_min < cfg->u_max))
+    return fail(ctx, EVR_ERR_INVALID, "need 0 < u_min < u_max");
+  ctx->cfg = *cfg;
+  ctx->cfg_set = true;
+  drop_graphs(ctx);
+  ctx->engine = EVR_ENGINE_STREAMING;
+  if (cfg->engine != EVR_ENGINE_STREAMING && ctx->H >= 2 && ctx->W >= 2) {
+    ResidentPlan plan;
+    const bool ok = ctx->prec == EVR_PREC_F64 ? resident_plan<double>(ctx, plan)
+                                              : resident_plan<float>(ctx, plan);
+    if (ok) {
+      ctx->engine = EVR_ENGINE_RESIDENT;
+      ctx->rplan = plan;
+      int rc = ctx->prec == EVR_PREC_F64 ? resident_alloc<double>(ctx) : resident_alloc<float>(ctx);
+      if (rc) return rc;
+    } else if (cfg->engine == EVR_ENGINE_RESIDENT) {
+      return fail(ctx, EVR_ERR_UNSUPPORTED, "resident engine does not fit a %dx%d sensor", ctx->W,
+                  ctx->H);
+    }
+  }
+  return EVR_OK;
+}
+
+int evr_active_engine(evr_ctx* ctx, int* engine) {
+  if (!ctx || !engine) return EVR_ERR_INVALID;
+  *engine = ctx->engine;
+  return EVR_OK;
+}
+
+int evr_init_state(evr_ctx* ctx) {
+  CHECK_CTX();
+  int rc;
+  if ((rc = require_config(ctx))) return rc;
+  const double mid = 0.5 * (ctx->cfg.u_min + ctx->cfg.u_max);  // pipeline.py:105
+  const int64_t N = ctx->N;
+  cudaStream_t s = ctx->stream;
+  k_fill<double><<<grid1d(N), kNT, 0, s>>>(ctx->f, mid, N);
+  if (ctx->prec == EVR_PREC_F64) {
+    k_fill<double><<<grid1d(N), kNT, 0, s>>>(ctx->fld<double>(F_U), mid, N);
+  } else {
+    k_fill<float><<<grid1d(N), kNT, 0, s>>>(ctx->fld<float>(F_U), (float)mid, N);
+  }
+  CK(cudaMemsetAsync(ctx->raw, 0, sizeof(int64_t) * N, s));
+  for (int k : {F_P1, F_P2, F_P3}) CK(cudaMemsetAsync(ctx->slab + ctx->field_stride * k, 0, ctx->field_stride, s));
+  if ((rc = launch_err(ctx, "init_state"))) return rc;
+  CK(cudaStreamSynchronize(s));
+  return EVR_OK;
+}
+
+int evr_set_state(evr_ctx* ctx, const double* u, const double* f, const int64_t* raw,
+                  const double* p) {
+  CHECK_CTX();
+  return ctx->prec == EVR_PREC_F64 ? set_state_t<double>(ctx, u, f, raw, p)
+                                   : set_state_t<float>(ctx, u, f, raw, p);
+}
+
+int evr_get_state(evr_ctx* ctx, double* u, double* f, int64_t* raw, double* p) {
+  CHECK_CTX();
+  return ctx->prec == EVR_PREC_F64 ? get_state_t<double>(ctx, u, f, raw, p)
+                                   : get_state_t<float>(ctx, u, f, raw, p);
+}
+
+int evr_ingest(evr_ctx* ctx, const evr_event* events, int64_t n) {
+  CHECK_CTX();
+  int rc;
+  if ((rc = require_config(ctx))) return rc;
+  if (n <= 0) return EVR_OK;
+  if (!events) return fail(ctx, EVR_ERR_INVALID, "null events");
+  if ((rc = stage_host_packet(ctx, events, n, 1.0))) return rc;
+  k_ingest<kIngestCH><<<1, kIngestCH, 0, ctx->stream>>>(ctx->hdr(), ctx->f, ctx->raw, ctx->H,
+                                                        ctx->W, ctx->cfg.c_pos, ctx->cfg.c_neg,
+                                                        ctx->cfg.u_min, ctx->cfg.u_max, ctx->d_err);
+  ctx->launches += 1;
+  if ((rc = launch_err(ctx, "ingest"))) return rc;
+  CK(cudaStreamSynchronize(ctx->stream));
+  return check_err_flag(ctx);
+}
+
+// Split packet API used when the host needs the surface between the two
+// halves (debug_sink) or a host-driven solve (convergence_tol, trace).
+int evr_packet_begin(evr_ctx* ctx, const evr_event* events, int64_t n, double window) {
+  CHECK_CTX();
+  int rc;
+  if ((rc = require_config(ctx))) return rc;
+  if (n <= 0 || !events) return fail(ctx, EVR_ERR_INVALID, "empty packet");
+  if ((rc = stage_host_packet(ctx, events, n, window))) return rc;
+  if (ctx->engine == EVR_ENGINE_RESIDENT) {
+    // the resident kernel fuses the whole packet; run the streaming
+    // surface stage here so the host can look at it between the halves
+    int r = ctx->prec == EVR_PREC_F64 ? enqueue_surface<double>(ctx) : enqueue_surface<float>(ctx);
+    if (r < 0) return r;
+    ctx->launches += r;
+    return EVR_OK;
+  }
+  return launch_stage(ctx, 0);
+}
+
+int evr_packet_solve(evr_ctx* ctx, evr_solve_info* info, double* energy_trace,
+                     double* rel_trace) {
+  CHECK_CTX();
+  int rc;
+  if ((rc = require_config(ctx))) return rc;
+  if (solve_needs_host_loop(ctx) || energy_trace || rel_trace || ctx->engine == EVR_ENGINE_RESIDENT) {
+    rc = ctx->prec == EVR_PREC_F64
+             ? solve_host_loop<double>(ctx, ctx->cfg, info, energy_trace, rel_trace, true)
+             : solve_host_loop<float>(ctx, ctx->cfg, info, energy_trace, rel_trace, true);
+    if (rc) return rc;
+    return check_err_flag(ctx);
+  }
+  if ((rc = launch_stage(ctx, 1))) return rc;
+  return evr_synchronize(ctx, info);
+}
+
+int evr_process_packet(evr_ctx* ctx, const evr_event* events, int64_t n, double window,
+                       evr_solve_info* info) {
+  CHECK_CTX();
+  int rc;
+  if ((rc = require_config(ctx))) return rc;
+  if (solve_needs_host_loop(ctx)) {
+    if ((rc = evr_packet_begin(ctx, events, n, window))) return rc;
+    return evr_packet_solve(ctx, info, nullptr, nullptr);
+  }
+  if ((rc = evr_process_packet_async(ctx, events, n, window))) return rc;
+  return evr_synchronize(ctx, info);
+}
+
+int evr_process_packet_async(evr_ctx* ctx, const evr_event* events, int64_t n, double window) {
+  CHECK_CTX();
+  int rc;
+  if ((rc = require_config(ctx))) return rc;
+  if (n <= 0 || !events) return fail(ctx, EVR_ERR_INVALID, "empty packet");
+  if (solve_needs_host_loop(ctx))
+    return fail(ctx, EVR_ERR_UNSUPPORTED, "convergence_tol > 0 needs evr_process_packet");
+  if ((rc = stage_host_packet(ctx, events, n, window))) return rc;
+  return launch_stage(ctx, 2);
+}
+
+int evr_process_packet_device(evr_ctx* ctx, const evr_event* dev_events, int64_t n,
+                              double window) {
+  CHECK_CTX();
+  int rc;
+  if ((rc = require_config(ctx))) return rc;
+  if (n <= 0 || !dev_events) return fail(ctx, EVR_ERR_INVALID, "empty packet");
+  if (solve_needs_host_loop(ctx))
+    return fail(ctx, EVR_ERR_UNSUPPORTED, "convergence_tol > 0 needs evr_process_packet");
+  if ((rc = stage_device_packet(ctx, dev_events, n, window))) return rc;
+  return launch_stage(ctx, 2);
+}
+
+int evr_synchronize(evr_ctx* ctx, evr_solve_info* info) {
+  CHECK_CTX();
+  if (info) {
+    CK(cudaMemcpyAsync(ctx->h_info, ctx->d_info, sizeof(evr_solve_info), cudaMemcpyDeviceToHost,
+                       ctx->stream));
+  }
+  CK(cudaStreamSynchronize(ctx->stream));
+  if (info) *info = *ctx->h_info;
+  return check_err_flag(ctx);
+}
+
+int evr_get_frame(evr_ctx* ctx, double* u_out) {
+  CHECK_CTX();
+  if (!u_out) return fail(ctx, EVR_ERR_INVALID, "null output");
+  return ctx->prec == EVR_PREC_F64 ? get_plane_t<double>(ctx, F_U, u_out)
+                                   : get_plane_t<float>(ctx, F_U, u_out);
+}
+
+int evr_get_surface(evr_ctx* ctx, double* t_out, double* G_out) {
+  CHECK_CTX();
+  int rc = EVR_OK;
+  if (t_out)
+    rc = ctx->prec == EVR_PREC_F64 ? get_plane_t<double>(ctx, F_T, t_out)
+                                   : get_plane_t<float>(ctx, F_T, t_out);
+  if (!rc && G_out)
+    rc = ctx->prec == EVR_PREC_F64 ? get_plane_t<double>(ctx, F_G, G_out)
+                                   : get_plane_t<float>(ctx, F_G, G_out);
+  return rc;
+}
+
+int evr_get_metric(evr_ctx* ctx, double* tx, double* ty, double* G, double* sqrtG) {
+  CHECK_CTX();
+  double* outs[4] = {tx, ty, G, sqrtG};
+  const int fl[4] = {F_TX, F_TY, F_G, F_SG};
+  for (int m = 0; m < 4; ++m) {
+    if (!outs[m]) continue;
+    int rc = ctx->prec == EVR_PREC_F64 ? get_plane_t<double>(ctx, fl[m], outs[m])
+                                       : get_plane_t<float>(ctx, fl[m], outs[m]);
+    if (rc) return rc;
+  }
+  return EVR_OK;
+}
+
+int evr_get_frame_u8(evr_ctx* ctx, double lo, double hi, uint8_t* out) {
+  CHECK_CTX();
+  if (!out || !(hi > lo)) return fail(ctx, EVR_ERR_INVALID, "bad gray range");
+  uint8_t* d = reinterpret_cast<uint8_t*>(ctx->aos_a);
+  if (ctx->prec == EVR_PREC_F64)
+    k_to_gray<double><<<grid1d(ctx->N), kNT, 0, ctx->stream>>>(ctx->fld<double>(F_U), lo, hi, d, ctx->N);
+  else
+    k_to_gray<float><<<grid1d(ctx->N), kNT, 0, ctx->stream>>>(ctx->fld<float>(F_U), lo, hi, d, ctx->N);
+  ctx->launches += 1;
+  int rc = launch_err(ctx, "to_gray");
+  if (rc) return rc;
+  return d2h_sync(ctx, out, d, (size_t)ctx->N);
+}
+
+int evr_event_buffer(evr_ctx* ctx, int64_t n, evr_event** dev_ptr) {
+  CHECK_CTX();
+  if (!dev_ptr || n < 1) return fail(ctx, EVR_ERR_INVALID, "bad event buffer request");
+  int rc = ensure_stage(ctx, n);
+  if (rc) return rc;
+  *dev_ptr = reinterpret_cast<evr_event*>(ctx->d_stage + sizeof(PacketHdr));
+  return EVR_OK;
+}
+
+void* evr_stream(evr_ctx* ctx) { return ctx ? (void*)ctx->stream : nullptr; }
+
+int64_t evr_launch_count(const evr_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+// ---- operator API (float64 contexts) ---------------------------------------
+#define OP_PROLOGUE(stencil)                     \
+  CHECK_CTX();                                   \
+  {                                              \
+    int rc_ = require_f64(ctx);                  \
+    if (!rc_ && (stencil)) rc_ = require_stencil(ctx); \
+    if (rc_) return rc_;                         \
+  }                                              \
+  const int64_t N = ctx->N;                      \
+  const size_t B = sizeof(double) * N;           \
+  cudaStream_t s = ctx->stream;                  \
+  (void)B; (void)s;
+
+int evr_op_grad(evr_ctx* ctx, const double* u, double* gx, double* gy) {
+  OP_PROLOGUE(false);
+  double *du = ctx->fld<double>(F_T), *dx = ctx->fld<double>(F_TX), *dy = ctx->fld<double>(F_TY);
+  int rc;
+  if ((rc = h2d(ctx, du, u, B))) return rc;
+  k_op_grad<<<grid2d(ctx), block2d(), 0, s>>>(du, dx, dy, ctx->H, ctx->W);
+  ctx->launches += 1;
+  if ((rc = launch_err(ctx, "grad"))) return rc;
+  CK(cudaMemcpyAsync(gx, dx, B, cudaMemcpyDeviceToHost, s));
+  return d2h_sync(ctx, gy, dy, B);
+}
+
+int evr_op_div(evr_ctx* ctx, const double* qx, const double* qy, double* out) {
+  OP_PROLOGUE(true);
+  double *a = ctx->fld<double>(F_TX), *b = ctx->fld<double>(F_TY), *o = ctx->fld<double>(F_T);
+  int rc;
+  if ((rc = h2d(ctx, a, qx, B)) || (rc = h2d(ctx, b, qy, B))) return rc;
+  k_op_div<<<grid2d(ctx), block2d(), 0, s>>>(a, b, o, ctx->H, ctx->W, 0);
+  ctx->launches += 1;
+  if ((rc = launch_err(ctx, "div"))) return rc;
+  return d2h_sync(ctx, out, o, B);
+}
+
+int evr_op_normalize(evr_ctx* ctx, const double* raw, double now, double t_scale, double window,
+                     double* t_out) {
+  OP_PROLOGUE(false);
+  if (!(window > 0)) return fail(ctx, EVR_ERR_INVALID, "t_window must be positive, got %g", window);
+  double *r = ctx->fld<double>(F_TX), *t = ctx->fld<double>(F_T);
+  int rc;
+  if ((rc = h2d(ctx, r, raw, B))) return rc;
+  k_op_normalize<<<grid1d(N), kNT, 0, s>>>(r, now, t_scale, window, t, N);
+  ctx->launches += 1;
+  if ((rc = launch_err(ctx, "normalize"))) return rc;
+  return d2h_sync(ctx, t_out, t, B);
+}
+
+int evr_op_denoise(evr_ctx* ctx, const double* t_in, double weight, int iterations, double t_scale,
+                   double* t_out) {
+  OP_PROLOGUE(true);
+  if (!(weight > 0)) return fail(ctx, EVR_ERR_INVALID, "denoise weight must be positive, got %g", weight);
+  if (iterations < 1) return fail(ctx, EVR_ERR_INVALID, "iterations must be >= 1, got %d", iterations);
+  double *t = ctx->fld<double>(F_T), *tu = ctx->fld<double>(F_TU), *tub = ctx->fld<double>(F_TUB);
+  double *px = ctx->fld<double>(F_TPX), *py = ctx->fld<double>(F_TPY);
+  int rc;
+  if ((rc = h2d(ctx, t, t_in, B))) return rc;
+  CK(cudaMemcpyAsync(tu, t, B, cudaMemcpyDeviceToDevice, s));
+  CK(cudaMemcpyAsync(tub, t, B, cudaMemcpyDeviceToDevice, s));
+  CK(cudaMemsetAsync(px, 0, B, s));
+  CK(cudaMemsetAsync(py, 0, B, s));
+  const double step = 1.0 / std::sqrt(8.0);
+  for (int it = 0; it < iterations; ++it) {
+    k_tv_dual<double><<<grid2d(ctx), block2d(), 0, s>>>(tub, px, py, ctx->H, ctx->W, step);
+    k_tv_primal<double><<<grid2d(ctx), block2d(), 0, s>>>(px, py, tu, tub, t, ctx->H, ctx->W, step,
+                                                          step * weight);
+  }
+  k_tv_finish<double><<<grid1d(N), kNT, 0, s>>>(tu, tub, t_scale, N);
+  ctx->launches += 2 * iterations + 1;
+  if ((rc = launch_err(ctx, "denoise"))) return rc;
+  return d2h_sync(ctx, t_out, tub, B);
+}
+
+int evr_op_metric(evr_ctx* ctx, const double* t, double* tx, double* ty, double* G, double* sqrtG) {
+  OP_PROLOGUE(false);
+  double* dt = ctx->fld<double>(F_T);
+  int rc;
+  if ((rc = h2d(ctx, dt, t, B))) return rc;
+  k_op_metric<<<grid2d(ctx), block2d(), 0, s>>>(dt, ctx->fld<double>(F_TX), ctx->fld<double>(F_TY),
+                                                ctx->fld<double>(F_G), ctx->fld<double>(F_SG),
+                                                ctx->H, ctx->W);
+  ctx->launches += 1;
+  if ((rc = launch_err(ctx, "metric"))) return rc;
+  CK(cudaMemcpyAsync(tx, ctx->fld<double>(F_TX), B, cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(ty, ctx->fld<double>(F_TY), B, cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(G, ctx->fld<double>(F_G), B, cudaMemcpyDeviceToHost, s));
+  return d2h_sync(ctx, sqrtG, ctx->fld<double>(F_SG), B);
+}
+
+// upload a caller MetricField and build the coefficient planes
+static int upload_metric(evr_ctx* ctx, const double* tx, const double* ty, const double* G,
+                         const double* sqrtG) {
+  const size_t B = sizeof(double) * ctx->N;
+  int rc;
+  if ((rc = h2d(ctx, ctx->fld<double>(F_TX), tx, B)) || (rc = h2d(ctx, ctx->fld<double>(F_TY), ty, B)) ||
+      (rc = h2d(ctx, ctx->fld<double>(F_G), G, B)))
+    return rc;
+  if (sqrtG && (rc = h2d(ctx, ctx->fld<double>(F_SG), sqrtG, B))) return rc;
+  k_op_coeffs<<<grid1d(ctx->N), kNT, 0, ctx->stream>>>(ctx->fld<double>(F_TX), ctx->fld<double>(F_TY),
+                                                       ctx->fld<double>(F_G), coefs<double>(ctx), ctx->N);
+  ctx->launches += 1;
+  return launch_err(ctx, "coeffs");
+}
+
+int evr_op_coeffs(evr_ctx* ctx, const double* tx, const double* ty, const double* G, double* out5) {
+  OP_PROLOGUE(false);
+  int rc;
+  if ((rc = upload_metric(ctx, tx, ty, G, nullptr))) return rc;
+  const int fl[5] = {F_A11, F_A12, F_A22, F_A31, F_A32};
+  for (int m = 0; m < 5; ++m)
+    CK(cudaMemcpyAsync(out5 + m * N, ctx->fld<double>(fl[m]), B, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  return EVR_OK;
+}
+
+int evr_op_surface_gradient(evr_ctx* ctx, const double* u, const double* tx, const double* ty,
+                            const double* G, double* out) {
+  OP_PROLOGUE(false);
+  int rc;
+  if ((rc = upload_metric(ctx, tx, ty, G, nullptr))) return rc;
+  double* du = ctx->fld<double>(F_T);
+  if ((rc = h2d(ctx, du, u, B))) return rc;
+  k_op_surface_gradient<<<grid2d(ctx), block2d(), 0, s>>>(du, coefs<double>(ctx), ctx->aos_a, ctx->H,
+                                                          ctx->W);
+  ctx->launches += 1;
+  if ((rc = launch_err(ctx, "surface_gradient"))) return rc;
+  return d2h_sync(ctx, out, ctx->aos_a, 3 * B);
+}
+
+int evr_op_surface_gradient_adjoint(evr_ctx* ctx, const double* p, const double* tx, const double* ty,
+                                    const double* G, double* out) {
+  OP_PROLOGUE(true);
+  int rc;
+  if ((rc = upload_metric(ctx, tx, ty, G, nullptr))) return rc;
+  if ((rc = h2d(ctx, ctx->aos_a, p, 3 * B))) return rc;
+  double *qx = ctx->fld<double>(F_TU), *qy = ctx->fld<double>(F_TUB), *o = ctx->fld<double>(F_T);
+  k_op_q<<<grid1d(N), kNT, 0, s>>>(ctx->aos_a, coefs<double>(ctx), qx, qy, N);
+  k_op_div<<<grid2d(ctx), block2d(), 0, s>>>(qx, qy, o, ctx->H, ctx->W, 1);
+  ctx->launches += 2;
+  if ((rc = launch_err(ctx, "surface_gradient_adjoint"))) return rc;
+  return d2h_sync(ctx, out, o, B);
+}
+
+int evr_op_prox_data(evr_ctx* ctx, const double* u_bar, const double* f, const double* sqrtG,
+                     double tau, double lam, double u_min, double u_max, double* out) {
+  OP_PROLOGUE(false);
+  double *a = ctx->fld<double>(F_T), *b = ctx->fld<double>(F_TU), *c = ctx->fld<double>(F_SG),
+         *o = ctx->fld<double>(F_TUB);
+  int rc;
+  if ((rc = h2d(ctx, a, u_bar, B)) || (rc = h2d(ctx, b, f, B)) || (rc = h2d(ctx, c, sqrtG, B)))
+    return rc;
+  k_op_prox_data<<<grid1d(N), kNT, 0, s>>>(a, b, c, tau * lam, u_min, u_max, o, N);
+  ctx->launches += 1;
+  if ((rc = launch_err(ctx, "prox_data"))) return rc;
+  return d2h_sync(ctx, out, o, B);
+}
+
+int evr_op_prox_dual(evr_ctx* ctx, const double* p, const double* sqrtG, double* out) {
+  OP_PROLOGUE(false);
+  int rc;
+  if ((rc = h2d(ctx, ctx->aos_a, p, 3 * B)) || (rc = h2d(ctx, ctx->fld<double>(F_SG), sqrtG, B)))
+    return rc;
+  k_op_prox_dual<<<grid1d(N), kNT, 0, s>>>(ctx->aos_a, ctx->fld<double>(F_SG), ctx->aos_b, N);
+  ctx->launches += 1;
+  if ((rc = launch_err(ctx, "prox_dual"))) return rc;
+  return d2h_sync(ctx, out, ctx->aos_b, 3 * B);
+}
+
+int evr_op_energy(evr_ctx* ctx, const double* u, const double* f, const double* tx, const double* ty,
+                  const double* G, const double* sqrtG, double lam, double* out) {
+  OP_PROLOGUE(false);
+  int rc;
+  if ((rc = upload_metric(ctx, tx, ty, G, sqrtG))) return rc;
+  if ((rc = h2d(ctx, ctx->fld<double>(F_T), u, B)) || (rc = h2d(ctx, ctx->aos_a, f, B))) return rc;
+  const int nb = red_blocks(N);
+  k_energy_partial<double, kNT><<<nb, kNT, 0, s>>>(ctx->fld<double>(F_T), ctx->aos_a, coefs<double>(ctx),
+                                                   ctx->fld<double>(F_G), ctx->fld<double>(F_SG),
+                                                   ctx->H, ctx->W, ctx->part);
+  k_energy_final<kNT><<<1, kNT, 0, s>>>(ctx->part, nb, lam, ctx->d_scalar);
+  ctx->launches += 2;
+  if ((rc = launch_err(ctx, "energy"))) return rc;
+  return d2h_sync(ctx, out, ctx->d_scalar, sizeof(double));
+}
+
+int evr_op_pd_solve(evr_ctx* ctx, const evr_config* cfg, const double* f, const double* tx,
+                    const double* ty, const double* G, const double* sqrtG, const double* u_init,
+                    const double* p_init, double* u_out, double* p_out, evr_solve_info* info,
+                    double* energy_trace, double* rel_trace) {
+  OP_PROLOGUE(true);
+  if (!cfg || cfg->max_iterations < 1) return fail(ctx, EVR_ERR_INVALID, "bad solver config");
+  int rc;
+  if ((rc = upload_metric(ctx, tx, ty, G, sqrtG))) return rc;
+  // the op API works on scratch copies: stash the stream state's f aside
+  double* fdev = ctx->aos_b;  // first N doubles of the (H,W,3) scratch
+  if ((rc = h2d(ctx, fdev, f, B))) return rc;
+  if ((rc = h2d(ctx, ctx->fld<double>(F_U), u_init ? u_init : f, B))) return rc;
+  if (p_init) {
+    if ((rc = h2d(ctx, ctx->aos_a, p_init, 3 * B))) return rc;
+    k_aos_to_planes<double><<<grid1d(N), kNT, 0, s>>>(ctx->aos_a, ctx->fld<double>(F_P1),
+                                                      ctx->fld<double>(F_P2), ctx->fld<double>(F_P3), N);
+  } else {
+    for (int k : {F_P1, F_P2, F_P3}) CK(cudaMemsetAsync(ctx->fld<double>(k), 0, B, s));
+  }
+  k_solver_setup<double><<<grid1d(N), kNT, 0, s>>>(
+      ctx->fld<double>(F_TX), ctx->fld<double>(F_TY), ctx->fld<double>(F_G), ctx->fld<double>(F_SG),
+      fdev, coefs<double>(ctx), ctx->fld<double>(F_BETA), ctx->fld<double>(F_FB), N,
+      cfg->tau * cfg->lam, 0);
+  ctx->launches += 2;
+  if ((rc = launch_err(ctx, "pd setup"))) return rc;
+  double* saved_f = ctx->f;
+  ctx->f = fdev;  // energy trace reads f
+  rc = solve_host_loop<double>(ctx, *cfg, info, energy_trace, rel_trace, false);
+  ctx->f = saved_f;
+  if (rc) return rc;
+  k_planes_to_aos<double><<<grid1d(N), kNT, 0, s>>>(ctx->fld<double>(F_P1), ctx->fld<double>(F_P2),
+                                                    ctx->fld<double>(F_P3), ctx->aos_a, N);
+  ctx->launches += 1;
+  CK(cudaMemcpyAsync(u_out, ctx->fld<double>(F_U), B, cudaMemcpyDeviceToHost, s));
+  return d2h_sync(ctx, p_out, ctx->aos_a, 3 * B);
+}
+
+int evr_op_rof_solve(evr_ctx* ctx, const double* f, const double* tx, const double* ty, const double* G,
+                     const double* sqrtG, double lam, int iterations, double* u_out) {
+  OP_PROLOGUE(true);
+  if (!(lam > 0)) return fail(ctx, EVR_ERR_INVALID, "lam must be positive, got %g", lam);
+  int rc;
+  if ((rc = upload_metric(ctx, tx, ty, G, sqrtG))) return rc;
+  double* fdev = ctx->aos_b;
+  if ((rc = h2d(ctx, fdev, f, B))) return rc;
+  CK(cudaMemcpyAsync(ctx->fld<double>(F_U), fdev, B, cudaMemcpyDeviceToDevice, s));
+  for (int k : {F_P1, F_P2, F_P3}) CK(cudaMemsetAsync(ctx->fld<double>(k), 0, B, s));
+  const double step = 1.0 / std::sqrt(8.0 + 4.0 * std::sqrt(2.0));  // solve.py:38, :277
+  k_solver_setup<double><<<grid1d(N), kNT, 0, s>>>(
+      ctx->fld<double>(F_TX), ctx->fld<double>(F_TY), ctx->fld<double>(F_G), ctx->fld<double>(F_SG),
+      fdev, coefs<double>(ctx), ctx->fld<double>(F_BETA), ctx->fld<double>(F_FB), N, step * lam, 1);
+  double* bufs[2] = {ctx->fld<double>(F_U), ctx->fld<double>(F_UN)};
+  for (int it = 0; it < iterations; ++it) {
+    double* cur = bufs[it & 1];
+    double* nxt = bufs[(it + 1) & 1];
+    double* v = ctx->fld<double>(F_V);
+    k_rof_primal<double><<<grid2d(ctx), block2d(), 0, s>>>(
+        ctx->fld<double>(F_P1), ctx->fld<double>(F_P2), ctx->fld<double>(F_P3), coefs<double>(ctx),
+        cur, ctx->fld<double>(F_BETA), ctx->fld<double>(F_FB), nxt, v, ctx->H, ctx->W, step);
+    k_pd_dual<double><<<grid2d(ctx), block2d(), 0, s>>>(v, ctx->fld<double>(F_P1), ctx->fld<double>(F_P2),
+                                                        ctx->fld<double>(F_P3), coefs<double>(ctx),
+                                                        ctx->fld<double>(F_SG), ctx->H, ctx->W, step);
+  }
+  ctx->launches += 1 + 2 * (int64_t)iterations;
+  if ((rc = launch_err(ctx, "rof"))) return rc;
+  return d2h_sync(ctx, u_out, bufs[iterations & 1], B);
+}
+
+}  // extern "C"

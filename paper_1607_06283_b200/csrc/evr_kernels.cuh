@@ -1,0 +1,514 @@
+// evr_kernels.cuh -- streaming-engine kernels (one launch per half-step,
+// fields in HBM / L2) and the operator-level kernels of the C ABI.
+//
+// Layout in device memory: every per-pixel field is its own row-major (H, W)
+// plane (SoA), 256-byte aligned, so a warp's 32 consecutive columns are one
+// coalesced 128 / 256-byte transaction.  The dual field p lives as three
+// planes p1, p2, p3 (the reference's _Loop keeps the same split,
+// solve.py:133-135); the interleaved (H, W, 3) host layout is converted at
+// the ABI boundary only.
+#pragma once
+
+#include <cstdint>
+
+#include "evr_math.cuh"
+#include "../../include/evr.h"
+
+namespace evr {
+
+// Per-packet scalars the host writes before each packet, so one captured
+// CUDA graph serves every packet.
+struct PacketHdr {
+  int64_t n;        // events in the packet
+  int64_t now;      // events[-1].timestamp (pipeline.py:160)
+  double window;    // surface window (pipeline.py:128-132)
+  int64_t seq;      // packet sequence number
+};
+
+template <class T> struct CoefPlanes {
+  T *a11, *a12, *a22, *a31, *a32;
+  __device__ __forceinline__ Coef<T> at(int64_t k) const {
+    return Coef<T>{a11[k], a12[k], a22[k], a31[k], a32[k]};
+  }
+};
+
+#define EVR_2D_INDEX                                   \
+  const int j = blockIdx.x * blockDim.x + threadIdx.x; \
+  const int i = blockIdx.y * blockDim.y + threadIdx.y; \
+  if (i >= H || j >= W) return;                        \
+  const int64_t k = (int64_t)i * W + j;
+
+// ---------------------------------------------------------------- ingest --
+// apply_event (pipeline.py:114-121) for every event of the packet, in
+// stream order, bit-exact including duplicates: one CTA walks the packet in
+// chunks of CH events; inside a chunk the first event of each pixel is the
+// pixel's leader and applies that pixel's events of the chunk in order
+// (multiply, clamp after every step), so the compounding order and the
+// last-wins timestamp (surface.py:124-127) match the sequential reference.
+// Chunks are separated by a CTA barrier, which orders them.
+template <int CH>
+__global__ void __launch_bounds__(CH)
+k_ingest(const PacketHdr* __restrict__ hdr, double* __restrict__ f, int64_t* __restrict__ raw, int H, int W,
+         double c_pos, double c_neg, double u_min, double u_max, int* err) {
+  __shared__ int spix[CH];
+  // the packet's events follow the header in the staging buffer
+  const evr_event* __restrict__ ev = reinterpret_cast<const evr_event*>(hdr + 1);
+  const int64_t n = hdr->n;
+  const int tid = threadIdx.x;
+  for (int64_t base = 0; base < n; base += CH) {
+    const int m = (int)((n - base) < CH ? (n - base) : CH);
+    int pix = -1 - tid;  // never matches a real pixel or another lane
+    if (tid < m) {
+      const evr_event e = ev[base + tid];
+      if (e.x >= 0 && e.x < W && e.y >= 0 && e.y < H)
+        pix = e.y * W + e.x;
+      else
+        atomicOr(err, 1);
+    }
+    spix[tid] = pix;
+    __syncthreads();
+    if (tid < m && pix >= 0) {
+      bool leader = true;
+      for (int j = tid - 1; j >= 0; --j)
+        if (spix[j] == pix) { leader = false; break; }
+      if (leader) {
+        double v = f[pix];
+        int last = tid;
+        for (int j = tid; j < m; ++j) {
+          if (spix[j] != pix) continue;
+          const double c = ev[base + j].polarity > 0 ? c_pos : c_neg;
+          v = v * c;
+          if (u_min > v) v = u_min;  // Python max(value, u_min)
+          if (u_max < v) v = u_max;  // Python min(.., u_max)
+          last = j;
+        }
+        f[pix] = v;
+        raw[pix] = ev[base + last].t;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// ------------------------------------------------------------- surface --
+// normalize_timestamps (surface.py:130-143) fused with the TV-L1 cold start
+// (surface.py:161-165: u = u_bar = t, px = py = 0).
+template <class T>
+__global__ void k_normalize_tvinit(const int64_t* __restrict__ raw,
+                                   const PacketHdr* __restrict__ hdr, double t_scale,
+                                   T* t, T* tu, T* tub, T* tpx, T* tpy, int64_t N) {
+  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= N) return;
+  const T v = (T)normalize_at((double)raw[k], (double)hdr->now, t_scale, hdr->window);
+  t[k] = v;
+  tu[k] = v;
+  tub[k] = v;
+  tpx[k] = T(0);
+  tpy[k] = T(0);
+}
+
+// TV-L1 dual half-step (surface.py:168-183)
+template <class T>
+__global__ void k_tv_dual(const T* __restrict__ ub, T* __restrict__ px, T* __restrict__ py,
+                          int H, int W, T sigma) {
+  EVR_2D_INDEX
+  const T dx = j < W - 1 ? ub[k + 1] - ub[k] : T(0);
+  const T dy = i < H - 1 ? ub[k + W] - ub[k] : T(0);
+  T a = px[k], b = py[k];
+  tv_dual_step(dx, dy, sigma, a, b);
+  px[k] = a;
+  py[k] = b;
+}
+
+// TV-L1 primal half-step (surface.py:185-193)
+template <class T>
+__global__ void k_tv_primal(const T* __restrict__ px, const T* __restrict__ py, T* u, T* ub,
+                            const T* __restrict__ f0, int H, int W, T tau, T shrink) {
+  EVR_2D_INDEX
+  const T d = div_at(px[k], j > 0 ? px[k - 1] : T(0), py[k], i > 0 ? py[k - W] : T(0), i, j,
+                     H, W);
+  T ubar;
+  const T un = tv_primal_step(d, u[k], f0[k], tau, shrink, ubar);
+  u[k] = un;
+  ub[k] = ubar;
+}
+
+// np.clip(u, 0, t_scale) after the TV-L1 loop (surface.py:195)
+template <class T>
+__global__ void k_tv_finish(const T* __restrict__ u, T* __restrict__ t, T t_scale, int64_t N) {
+  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= N) return;
+  t[k] = vclip(u[k], T(0), t_scale);
+}
+
+// compute_metric (surface.py:199-205) + MetricField.coeffs (surface.py:81-90)
+// + the solver constants beta = (tau*lam)*sqrtG, fb = (4*beta)*f
+// (solve.py:227-228).  `flat` gives flat_metric (surface.py:208-211).
+template <class T>
+__global__ void k_metric_setup(const T* __restrict__ t, const double* __restrict__ f, T* tx,
+                               T* ty, T* G, T* sg, CoefPlanes<T> c, T* beta, T* fb, int H,
+                               int W, T tl, int flat) {
+  EVR_2D_INDEX
+  T gx = T(0), gy = T(0);
+  if (!flat) {
+    gx = j < W - 1 ? t[k + 1] - t[k] : T(0);
+    gy = i < H - 1 ? t[k + W] - t[k] : T(0);
+  }
+  const T g = metric_G(gx, gy);
+  const T s = sqrt(g);
+  const Coef<T> a = coeffs_of(gx, gy, g);
+  tx[k] = gx;
+  ty[k] = gy;
+  G[k] = g;
+  sg[k] = s;
+  c.a11[k] = a.a11;
+  c.a12[k] = a.a12;
+  c.a22[k] = a.a22;
+  c.a31[k] = a.a31;
+  c.a32[k] = a.a32;
+  const T b = tl * s;
+  beta[k] = b;
+  fb[k] = T(4) * b * (T)f[k];
+}
+
+// Solver set-up from a caller-supplied MetricField (operator API):
+// coefficients from (tx, ty, G) and beta/fb from sqrtG as given.
+template <class T>
+__global__ void k_solver_setup(const T* __restrict__ tx, const T* __restrict__ ty,
+                               const T* __restrict__ G, const T* __restrict__ sg,
+                               const double* __restrict__ f, CoefPlanes<T> c, T* beta, T* fb,
+                               int64_t N, T tl, int rof) {
+  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= N) return;
+  const Coef<T> a = coeffs_of(tx[k], ty[k], G[k]);
+  c.a11[k] = a.a11;
+  c.a12[k] = a.a12;
+  c.a22[k] = a.a22;
+  c.a31[k] = a.a31;
+  c.a32[k] = a.a32;
+  const T b = tl * sg[k];
+  if (rof) {  // solve.py:278-280: w, wf = w*f, inv = 1/(1+w)
+    beta[k] = T(1) / (T(1) + b);
+    fb[k] = b * (T)f[k];
+  } else {
+    beta[k] = b;
+    fb[k] = T(4) * b * (T)f[k];
+  }
+}
+
+// ------------------------------------------------------------ solver --
+// q = A^T p at pixel k
+template <class T>
+__device__ __forceinline__ void q_at(const CoefPlanes<T>& c, const T* p1, const T* p2,
+                                     const T* p3, int64_t k, T& qx, T& qy) {
+  q_of(c.at(k), p1[k], p2[k], p3[k], qx, qy);
+}
+
+// descent point div(A^T p) at (i, j) (solve.py:144-167, without *tau + u)
+template <class T>
+__device__ __forceinline__ T div_q(const CoefPlanes<T>& c, const T* p1, const T* p2,
+                                   const T* p3, int i, int j, int H, int W, int64_t k) {
+  T qx, qy, qxl = T(0), qyu = T(0), dummy;
+  q_at(c, p1, p2, p3, k, qx, qy);
+  if (j > 0) q_at(c, p1, p2, p3, k - 1, qxl, dummy);
+  if (i > 0) q_at(c, p1, p2, p3, k - W, dummy, qyu);
+  return div_at(qx, qxl, qy, qyu, i, j, H, W);
+}
+
+// KL primal half-step + over-relaxation (solve.py:234-252)
+template <class T>
+__global__ void k_pd_primal(const T* __restrict__ p1, const T* __restrict__ p2,
+                            const T* __restrict__ p3, CoefPlanes<T> c,
+                            const T* __restrict__ u, const T* __restrict__ beta,
+                            const T* __restrict__ fb, T* __restrict__ un, T* __restrict__ v,
+                            int H, int W, T tau, T umin, T umax) {
+  EVR_2D_INDEX
+  const T d = div_q(c, p1, p2, p3, i, j, H, W, k);
+  const T uk = u[k];
+  const T nu = kl_primal(d, uk, beta[k], fb[k], tau, umin, umax);
+  un[k] = nu;
+  v[k] = nu * T(2) - uk;
+}
+
+// ROF primal half-step + over-relaxation (solve.py:283-291); beta holds
+// inv = 1/(1+w) and fb holds wf = w*f for this variant.
+template <class T>
+__global__ void k_rof_primal(const T* __restrict__ p1, const T* __restrict__ p2,
+                             const T* __restrict__ p3, CoefPlanes<T> c,
+                             const T* __restrict__ u, const T* __restrict__ inv,
+                             const T* __restrict__ wf, T* __restrict__ un, T* __restrict__ v,
+                             int H, int W, T tau) {
+  EVR_2D_INDEX
+  const T d = div_q(c, p1, p2, p3, i, j, H, W, k);
+  const T uk = u[k];
+  const T nu = rof_primal(d, uk, wf[k], inv[k], tau);
+  un[k] = nu;
+  v[k] = nu * T(2) - uk;
+}
+
+// dual ascent + ball projection (solve.py:170-201)
+template <class T>
+__global__ void k_pd_dual(const T* __restrict__ v, T* __restrict__ p1, T* __restrict__ p2,
+                          T* __restrict__ p3, CoefPlanes<T> c, const T* __restrict__ sg, int H,
+                          int W, T sigma) {
+  EVR_2D_INDEX
+  const T gx = j < W - 1 ? v[k + 1] - v[k] : T(0);
+  const T gy = i < H - 1 ? v[k + W] - v[k] : T(0);
+  T a = p1[k], b = p2[k], d = p3[k];
+  dual_step(c.at(k), sigma, gx, gy, sg[k], a, b, d);
+  p1[k] = a;
+  p2[k] = b;
+  p3[k] = d;
+}
+
+// --------------------------------------------------------- reductions --
+// Deterministic two-pass reductions (fixed tree): pass 1 writes one partial
+// per block, pass 2 (one block) folds the partials in index order.
+template <int NT>
+__device__ __forceinline__ double block_sum(double x, double* sh) {
+  for (int o = 16; o > 0; o >>= 1) x += __shfl_down_sync(0xffffffffu, x, o);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  __syncthreads();
+  if (lane == 0) sh[wid] = x;
+  __syncthreads();
+  x = threadIdx.x < NT / 32 ? sh[threadIdx.x] : 0.0;
+  if (wid == 0)
+    for (int o = 16; o > 0; o >>= 1) x += __shfl_down_sync(0xffffffffu, x, o);
+  return x;
+}
+
+// rel_change partials: sum (un-u)^2 and sum u^2 (solve.py:246-249)
+template <class T, int NT>
+__global__ void __launch_bounds__(NT)
+k_relchange_partial(const T* __restrict__ un, const T* __restrict__ u, int64_t N,
+                    double* __restrict__ part) {
+  __shared__ double sh[NT / 32];
+  double d = 0.0, o = 0.0;
+  for (int64_t k = (int64_t)blockIdx.x * NT + threadIdx.x; k < N; k += (int64_t)gridDim.x * NT) {
+    const double a = (double)un[k], b = (double)u[k];
+    d += (a - b) * (a - b);
+    o += b * b;
+  }
+  d = block_sum<NT>(d, sh);
+  o = block_sum<NT>(o, sh);
+  if (threadIdx.x == 0) {
+    part[2 * blockIdx.x] = d;
+    part[2 * blockIdx.x + 1] = o;
+  }
+}
+
+template <int NT>
+__global__ void __launch_bounds__(NT)
+k_relchange_final(const double* __restrict__ part, int nb, evr_solve_info* info,
+                  int iterations) {
+  __shared__ double sh[NT / 32];
+  double d = 0.0, o = 0.0;
+  for (int b = threadIdx.x; b < nb; b += NT) {
+    d += part[2 * b];
+    o += part[2 * b + 1];
+  }
+  d = block_sum<NT>(d, sh);
+  o = block_sum<NT>(o, sh);
+  if (threadIdx.x == 0) {
+    const double den = sqrt(o);
+    info->rel_change = sqrt(d) / (den > 1e-30 ? den : 1e-30);
+    info->iterations = iterations;
+  }
+}
+
+// energy (solve.py:111-118) partials: tv = sqrt(G * |S u|^2), data term
+template <class T, int NT>
+__global__ void __launch_bounds__(NT)
+k_energy_partial(const T* __restrict__ u, const double* __restrict__ f, CoefPlanes<T> c,
+                 const T* __restrict__ G, const T* __restrict__ sg, int H, int W,
+                 double* __restrict__ part) {
+  __shared__ double sh[NT / 32];
+  double tv = 0.0, data = 0.0;
+  const int64_t N = (int64_t)H * W;
+  for (int64_t k = (int64_t)blockIdx.x * NT + threadIdx.x; k < N; k += (int64_t)gridDim.x * NT) {
+    const int i = (int)(k / W), j = (int)(k - (int64_t)i * W);
+    const T ux = j < W - 1 ? u[k + 1] - u[k] : T(0);
+    const T uy = i < H - 1 ? u[k + W] - u[k] : T(0);
+    const Coef<T> a = c.at(k);
+    const T s0 = a.a11 * ux + a.a12 * uy;
+    const T s1 = a.a12 * ux + a.a22 * uy;
+    const T s2 = a.a31 * ux + a.a32 * uy;
+    const T s = s0 * s0 + s1 * s1 + s2 * s2;
+    tv += (double)sqrt(G[k] * s);
+    const double uk = (double)u[k];
+    data += (uk - f[k] * log(uk)) * (double)sg[k];
+  }
+  tv = block_sum<NT>(tv, sh);
+  data = block_sum<NT>(data, sh);
+  if (threadIdx.x == 0) {
+    part[2 * blockIdx.x] = tv;
+    part[2 * blockIdx.x + 1] = data;
+  }
+}
+
+template <int NT>
+__global__ void __launch_bounds__(NT)
+k_energy_final(const double* __restrict__ part, int nb, double lam, double* out) {
+  __shared__ double sh[NT / 32];
+  double tv = 0.0, data = 0.0;
+  for (int b = threadIdx.x; b < nb; b += NT) {
+    tv += part[2 * b];
+    data += part[2 * b + 1];
+  }
+  tv = block_sum<NT>(tv, sh);
+  data = block_sum<NT>(data, sh);
+  if (threadIdx.x == 0) *out = tv + lam * data;
+}
+
+// ---------------------------------------------------------- epilogue --
+// process_packet re-anchor (pipeline.py:167-170): u <- u+, f <- copy(u+)
+template <class T>
+__global__ void k_epilogue(const T* __restrict__ un, T* __restrict__ u, double* __restrict__ f,
+                           int64_t N) {
+  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= N) return;
+  const T v = un[k];
+  if (un != u) u[k] = v;
+  f[k] = (double)v;
+}
+
+// ------------------------------------------------------ conversions --
+template <class S, class D>
+__global__ void k_convert(const S* __restrict__ s, D* __restrict__ d, int64_t N) {
+  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k < N) d[k] = (D)s[k];
+}
+
+template <class T>
+__global__ void k_fill(T* __restrict__ d, T v, int64_t N) {
+  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k < N) d[k] = v;
+}
+
+// (H, W, 3) interleaved double <-> three planes
+template <class T>
+__global__ void k_aos_to_planes(const double* __restrict__ aos, T* p1, T* p2, T* p3, int64_t N) {
+  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= N) return;
+  p1[k] = (T)aos[3 * k];
+  p2[k] = (T)aos[3 * k + 1];
+  p3[k] = (T)aos[3 * k + 2];
+}
+
+template <class T>
+__global__ void k_planes_to_aos(const T* __restrict__ p1, const T* __restrict__ p2,
+                                const T* __restrict__ p3, double* aos, int64_t N) {
+  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= N) return;
+  aos[3 * k] = (double)p1[k];
+  aos[3 * k + 1] = (double)p2[k];
+  aos[3 * k + 2] = (double)p3[k];
+}
+
+// to_gray (pgm.py:14-22): floor(255*(u-lo)/(hi-lo) + 0.5), clipped, uint8
+template <class T>
+__global__ void k_to_gray(const T* __restrict__ u, double lo, double hi, uint8_t* out, int64_t N) {
+  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= N) return;
+  double s = ((double)u[k] - lo) / (hi - lo);
+  s = floor(s * 255.0 + 0.5);
+  out[k] = (uint8_t)vclip(s, 0.0, 255.0);
+}
+
+// ------------------------------------------------- operator kernels --
+// grad_x / grad_y (surface.py:93-104)
+__global__ void k_op_grad(const double* __restrict__ u, double* gx, double* gy, int H, int W) {
+  EVR_2D_INDEX
+  gx[k] = j < W - 1 ? u[k + 1] - u[k] : 0.0;
+  gy[k] = i < H - 1 ? u[k + W] - u[k] : 0.0;
+}
+
+// div_xy (surface.py:107-121); negate for surface_gradient_adjoint
+__global__ void k_op_div(const double* __restrict__ qx, const double* __restrict__ qy,
+                         double* out, int H, int W, int negate) {
+  EVR_2D_INDEX
+  const double d = div_at(qx[k], j > 0 ? qx[k - 1] : 0.0, qy[k], i > 0 ? qy[k - W] : 0.0, i, j,
+                          H, W);
+  out[k] = negate ? -d : d;
+}
+
+// q = A^T p from interleaved p (surface.py:249-251)
+__global__ void k_op_q(const double* __restrict__ p, CoefPlanes<double> c, double* qx,
+                       double* qy, int64_t N) {
+  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= N) return;
+  q_of(c.at(k), p[3 * k], p[3 * k + 1], p[3 * k + 2], qx[k], qy[k]);
+}
+
+// surface_gradient (surface.py:214-236) -> interleaved (H, W, 3)
+__global__ void k_op_surface_gradient(const double* __restrict__ u, CoefPlanes<double> c,
+                                      double* out, int H, int W) {
+  EVR_2D_INDEX
+  const double ux = j < W - 1 ? u[k + 1] - u[k] : 0.0;
+  const double uy = i < H - 1 ? u[k + W] - u[k] : 0.0;
+  const Coef<double> a = c.at(k);
+  out[3 * k] = a.a11 * ux + a.a12 * uy;
+  out[3 * k + 1] = a.a12 * ux + a.a22 * uy;
+  out[3 * k + 2] = a.a31 * ux + a.a32 * uy;
+}
+
+// prox_data (solve.py:88-100)
+__global__ void k_op_prox_data(const double* __restrict__ ub, const double* __restrict__ f,
+                               const double* __restrict__ sg, double tl, double umin,
+                               double umax, double* out, int64_t N) {
+  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= N) return;
+  const double beta = tl * sg[k];
+  const double s = ub[k] - beta;
+  const double root = 0.5 * (s + sqrt(s * s + 4.0 * beta * f[k]));
+  out[k] = vclip(root, umin, umax);
+}
+
+// prox_dual (solve.py:103-108)
+__global__ void k_op_prox_dual(const double* __restrict__ p, const double* __restrict__ sg,
+                               double* out, int64_t N) {
+  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= N) return;
+  const double a = p[3 * k], b = p[3 * k + 1], c = p[3 * k + 2];
+  const double nrm = sqrt(a * a + b * b + c * c);
+  const double s = vmax(1.0, nrm / sg[k]);
+  out[3 * k] = a / s;
+  out[3 * k + 1] = b / s;
+  out[3 * k + 2] = c / s;
+}
+
+// coefficient planes from caller-supplied (tx, ty, G)
+__global__ void k_op_coeffs(const double* __restrict__ tx, const double* __restrict__ ty,
+                            const double* __restrict__ G, CoefPlanes<double> c, int64_t N) {
+  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= N) return;
+  const Coef<double> a = coeffs_of(tx[k], ty[k], G[k]);
+  c.a11[k] = a.a11;
+  c.a12[k] = a.a12;
+  c.a22[k] = a.a22;
+  c.a31[k] = a.a31;
+  c.a32[k] = a.a32;
+}
+
+// compute_metric fields only (surface.py:199-205)
+__global__ void k_op_metric(const double* __restrict__ t, double* tx, double* ty, double* G,
+                            double* sg, int H, int W) {
+  EVR_2D_INDEX
+  const double gx = j < W - 1 ? t[k + 1] - t[k] : 0.0;
+  const double gy = i < H - 1 ? t[k + W] - t[k] : 0.0;
+  const double g = metric_G(gx, gy);
+  tx[k] = gx;
+  ty[k] = gy;
+  G[k] = g;
+  sg[k] = sqrt(g);
+}
+
+// normalize_timestamps on a float64 raw map (surface.py:141-142)
+__global__ void k_op_normalize(const double* __restrict__ raw, double now, double t_scale,
+                               double window, double* t, int64_t N) {
+  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= N) return;
+  t[k] = normalize_at(raw[k], now, t_scale, window);
+}
+
+}  // namespace evr

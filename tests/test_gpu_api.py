@@ -1,0 +1,220 @@
+"""The reference's own behavioural tests, restated against the drop-in API
+(reference: pkg/tests/test_pipeline.py, test_solve.py, test_surface.py).
+Each test names the reference test it mirrors."""
+
+import io
+import math
+import sys
+
+import numpy as np
+import pytest
+
+import paper_1607_06283_b200 as evr
+from paper_1607_06283_b200 import (Event, ManifoldConfig, PacketPolicy, SensorGeometry,
+                                   SolverConfig, Thresholds)
+
+pytestmark = pytest.mark.gpu
+
+GEOM = SensorGeometry(width=16, height=16)
+
+
+def make_events(n, geom=GEOM, seed=0, t_step=10):
+    rng = np.random.default_rng(seed)
+    return [Event(x=int(rng.integers(0, geom.width)), y=int(rng.integers(0, geom.height)),
+                  polarity=int(rng.choice([-1, 1])), timestamp=k * t_step) for k in range(n)]
+
+
+# --- test_pipeline.py ---------------------------------------------------------
+
+
+def test_init_state_midpoint():  # test_pipeline.py:40-46
+    state = evr.init_state(GEOM, SolverConfig(u_min=1.0, u_max=2.0))
+    np.testing.assert_array_equal(state.u, 1.5)
+    np.testing.assert_array_equal(state.f, state.u)
+    np.testing.assert_array_equal(state.p, 0.0)
+    np.testing.assert_array_equal(state.raw_timestamps, 0)
+    assert state.frame_index == 0
+
+
+def test_apply_event_quanta_clamp_locality():  # test_pipeline.py:52-79
+    cfg = SolverConfig()
+    state = evr.init_state(GEOM, cfg)
+    evr.apply_event(state, Event(x=3, y=5, polarity=1, timestamp=7), Thresholds(), cfg)
+    assert state.f[5, 3] == 1.5 * math.exp(0.15)
+    assert state.raw_timestamps[5, 3] == 7
+    evr.apply_event(state, Event(x=1, y=1, polarity=-1, timestamp=3), Thresholds(), cfg)
+    assert state.f[1, 1] == 1.5 * math.exp(-0.15)
+    state.f[2, 2] = cfg.u_max  # caller edit of the host view is honoured
+    evr.apply_event(state, Event(x=2, y=2, polarity=1, timestamp=1), Thresholds(), cfg)
+    assert state.f[2, 2] == cfg.u_max
+    before = state.f.copy()
+    evr.apply_event(state, Event(x=4, y=6, polarity=1, timestamp=1), Thresholds(), cfg)
+    np.testing.assert_array_equal(np.argwhere(state.f != before), [[6, 4]])
+
+
+def test_empty_packet_is_identity():  # test_pipeline.py:85-94
+    state = evr.init_state(GEOM, SolverConfig())
+    u_before = state.u.copy()
+    state, frame, result = evr.process_packet(state, [], ManifoldConfig(), SolverConfig(),
+                                              Thresholds())
+    np.testing.assert_array_equal(frame, u_before)
+    assert result is None and state.frame_index == 0
+
+
+def test_packet_reanchors_measurement_to_solution():  # test_pipeline.py:97-106
+    state = evr.init_state(GEOM, SolverConfig())
+    state, frame, result = evr.process_packet(state, make_events(40), ManifoldConfig(),
+                                              SolverConfig(), Thresholds())
+    np.testing.assert_array_equal(state.f, state.u)
+    np.testing.assert_array_equal(frame, state.u)
+    assert frame is state.u
+    assert state.frame_index == 1 and result.iterations == SolverConfig().max_iterations
+
+
+def test_packet_monotone_raw_timestamps():  # test_pipeline.py:109-118
+    state = evr.init_state(GEOM, SolverConfig())
+    events = make_events(60, seed=1)
+    snaps = []
+    for chunk in (events[:20], events[20:40], events[40:]):
+        snaps.append(state.raw_timestamps.copy())
+        evr.process_packet(state, chunk, ManifoldConfig(), SolverConfig(), Thresholds())
+    snaps.append(state.raw_timestamps.copy())
+    for a, b in zip(snaps, snaps[1:]):
+        assert np.all(b >= a)
+
+
+def test_frame_counts_skip_and_short_final():  # test_pipeline.py:124-159
+    frames = []
+    _, stats = evr.run_stream(make_events(1500), GEOM, PacketPolicy(500), ManifoldConfig(),
+                              SolverConfig(), Thresholds(), sink=lambda i, fr: frames.append(i))
+    assert frames == [0, 1, 2] and stats.packets == 3 and stats.events_consumed == 1500
+    frames = []
+    evr.run_stream(make_events(1500), GEOM, PacketPolicy(500, frames_to_skip=2),
+                   ManifoldConfig(), SolverConfig(), Thresholds(),
+                   sink=lambda i, fr: frames.append(i))
+    assert len(frames) == 1
+    frames = []
+    _, stats = evr.run_stream(make_events(650), GEOM, PacketPolicy(500), ManifoldConfig(),
+                              SolverConfig(), Thresholds(), sink=lambda i, fr: frames.append(fr))
+    assert stats.packets == 2 and len(frames) == 2
+
+
+def test_split_run_bit_identical():  # test_pipeline.py:162-183
+    geom = SensorGeometry(width=24, height=24)
+    events = make_events(2000, geom=geom, seed=3, t_step=2)
+    args = (geom, PacketPolicy(500), ManifoldConfig(), SolverConfig(), Thresholds())
+    whole, first, second = [], [], []
+    evr.run_stream(events, *args, sink=lambda i, fr: whole.append(fr.copy()))
+    state, _ = evr.run_stream(events[:500], *args, sink=lambda i, fr: first.append(fr.copy()))
+    evr.run_stream(events[500:], *args, sink=lambda i, fr: second.append(fr.copy()), state=state)
+    assert len(whole) == len(first + second)
+    for a, b in zip(whole, first + second):
+        np.testing.assert_array_equal(a, b)
+
+
+def test_fidelity_dominant_limit_reproduces_integration():  # test_pipeline.py:186-204
+    geom = SensorGeometry(width=12, height=12)
+    events = make_events(900, geom=geom, seed=5)
+    cfg = SolverConfig(lam=1e6)
+    frames = []
+    evr.run_stream(events, geom, PacketPolicy(300), ManifoldConfig(enabled=False), cfg,
+                   Thresholds(), sink=lambda i, fr: frames.append(fr.copy()))
+    f = np.full((12, 12), 1.5)
+    for ev in events:
+        c = math.exp(0.15) if ev.polarity > 0 else math.exp(-0.15)
+        f[ev.y, ev.x] = min(max(f[ev.y, ev.x] * c, cfg.u_min), cfg.u_max)
+    assert np.abs(frames[-1] - f).max() <= 1e-3
+
+
+def test_stats_line_and_energy_trace(capsys):  # test_pipeline.py:207-214, test_cli.py:80-89
+    trace = io.StringIO()
+    evr.run_stream(make_events(600), GEOM, PacketPolicy(200), ManifoldConfig(), SolverConfig(),
+                   Thresholds(), stats_every=2, log=sys.stderr, trace=trace)
+    err = capsys.readouterr().err
+    assert "packet 2:" in err and "iterations" in err
+    rows = trace.getvalue().strip().splitlines()
+    assert rows[0] == "packet,iteration,energy,rel_change" and len(rows) == 1 + 3 * 50
+
+
+# --- test_solve.py ------------------------------------------------------------
+
+
+def test_config_validation():  # test_solve.py:32-46
+    with pytest.raises(ValueError, match="step sizes"):
+        SolverConfig(tau=1.0, sigma=1.0)
+    with pytest.raises(ValueError):
+        SolverConfig(u_min=0.0, u_max=1.0)
+
+
+def test_prox_data_cases():  # test_solve.py:52-72
+    m = evr.flat_metric((1, 3))
+    out = evr.prox_data(np.array([[0.2, 1.4, 3.0]]), np.array([[1.5, 1.5, 1.5]]), m, 0.3,
+                        SolverConfig(lam=0.0))
+    np.testing.assert_allclose(out, [[1.0, 1.4, 2.0]])
+    f = np.array([[1.2, 1.5], [1.8, 1.01]])
+    np.testing.assert_allclose(evr.prox_data(f.copy(), f, evr.flat_metric((2, 2)), 0.7,
+                                             SolverConfig(lam=2.0)), f, atol=1e-14)
+    with pytest.raises(ValueError, match="positive"):
+        evr.prox_data(np.ones((1, 1)), np.zeros((1, 1)), evr.flat_metric((1, 1)), 0.1,
+                      SolverConfig())
+
+
+def test_solve_fixed_point_box_and_errors():  # test_solve.py:190-247
+    res = evr.primal_dual_solve(np.full((8, 8), 1.3), evr.flat_metric((8, 8)),
+                                SolverConfig(lam=0.7))
+    np.testing.assert_allclose(res.u, 1.3, atol=1e-12)
+    with pytest.raises(ValueError, match="box"):
+        evr.primal_dual_solve(np.full((4, 4), 5.0), evr.flat_metric((4, 4)), SolverConfig())
+    with pytest.raises(ValueError):
+        evr.primal_dual_solve(np.full((4, 4), 1.5), evr.flat_metric((5, 5)), SolverConfig())
+
+
+def test_solve_single_iteration_matches_op_composition():  # test_solve.py:261-273
+    rng = np.random.default_rng(32)
+    cfg = SolverConfig(lam=0.9, max_iterations=1)
+    f = np.clip(1.5 + 0.4 * rng.normal(0, 1, (11, 7)), 1, 2)
+    m = evr.compute_metric(rng.normal(0, 1.3, (11, 7)))
+    u0 = np.clip(1.5 + 0.4 * rng.normal(0, 1, (11, 7)), 1, 2)
+    p0 = rng.normal(0, 0.5, (11, 7, 3))
+    res = evr.primal_dual_solve(f, m, cfg, u_init=u0, p_init=p0)
+    u1 = evr.prox_data(u0 - cfg.tau * evr.surface_gradient_adjoint(p0, m), f, m, cfg.tau, cfg)
+    p1 = evr.prox_dual(p0 + cfg.sigma * evr.surface_gradient(2 * u1 - u0, m), m)
+    np.testing.assert_allclose(res.u, u1, atol=1e-14)
+    np.testing.assert_allclose(res.p, p1, atol=1e-14)
+
+
+# --- test_surface.py ----------------------------------------------------------
+
+
+def test_adjointness():  # test_surface.py:217-236
+    rng = np.random.default_rng(7)
+    for shape in [(9, 13), (2, 2), (31, 17)]:
+        m = evr.compute_metric(rng.normal(0, 2, shape))
+        u = rng.normal(0, 1, shape)
+        p = rng.normal(0, 1, shape + (3,))
+        lhs = np.sum(evr.surface_gradient(u, m) * p)
+        rhs = np.sum(u * evr.surface_gradient_adjoint(p, m))
+        assert abs(lhs - rhs) <= 1e-10 * max(1.0, abs(lhs))
+
+
+def test_denoise_validation_and_range():  # test_surface.py:78-115
+    with pytest.raises(ValueError):
+        evr.denoise_timestamps(evr.TimeSurface(np.zeros((4, 4)), 3.0), 0.0)
+    t = np.random.default_rng(1).uniform(0, 3, (10, 12))
+    out = evr.denoise_timestamps(evr.TimeSurface(t, 3.0), 0.5, 30)
+    assert out.t.min() >= 0 and out.t.max() <= 3.0
+
+
+def test_install_reroutes_reference_stream():
+    """install() patches an evrecon.pipeline module's seam."""
+    import types
+
+    fake = types.ModuleType("evrecon.pipeline")
+    fake.init_state = fake.process_packet = fake.primal_dual_solve = None
+    evr.install(fake)
+    try:
+        assert fake.process_packet is evr.process_packet
+        assert fake.init_state is evr.init_state
+    finally:
+        evr.uninstall()
+    assert fake.process_packet is None

@@ -1,0 +1,265 @@
+"""Parity of the CUDA path with the reference (golden fixtures) and with the
+C oracle (seeded inputs at full sensor sizes).  float64: bit-exact
+(np.array_equal) for f, raw, t, metric, u, p at every packet; float32:
+log-intensity within 1e-4 max-abs (the north_star tolerance).
+"""
+
+import math
+import os
+
+import numpy as np
+import pytest
+
+import paper_1607_06283_b200 as evr
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+LOG_TOL = 1e-4  # north_star: max-abs on log intensity (float32 engine)
+
+
+def load(name):
+    return dict(np.load(os.path.join(GOLD, name)))
+
+
+def packets_of(d):
+    ev = evr.make_event_array(d["ev_x"], d["ev_y"], d["ev_pol"], d["ev_t"])
+    epp = int(d["epp"])
+    return [ev[s:s + epp] for s in range(0, len(ev), epp)]
+
+
+STREAMS = {
+    "stream_u_32x24.npz": (evr.ManifoldConfig(), evr.SolverConfig(), evr.Thresholds()),
+    "stream_s_dvs128.npz": (evr.ManifoldConfig(), evr.SolverConfig(), evr.Thresholds()),
+    "stream_flat_9x2.npz": (evr.ManifoldConfig(enabled=False),
+                            evr.SolverConfig(max_iterations=20), evr.Thresholds()),
+    "stream_window_2x7.npz": (evr.ManifoldConfig(t_window=50.0, t_scale=2.0,
+                                                 denoise_weight=0.5, denoise_iterations=7),
+                              evr.SolverConfig(lam=1.3, max_iterations=9),
+                              evr.Thresholds(0.2, 0.1)),
+}
+
+ENGINES = ["streaming", "resident"]
+
+
+def device_state(d, cfg, precision=0, engine=None):
+    H, W = int(d["height"]), int(d["width"])
+    st = evr.init_state(evr.SensorGeometry(width=W, height=H), cfg, precision=precision,
+                        engine=engine)
+    if "init_u" in d:
+        st.u, st.f = d["init_u"].copy(), d["init_f"].copy()
+        st.raw_timestamps, st.p = d["init_raw"].copy(), d["init_p"].copy()
+        st.packet_starts.extend(int(v) for v in d["init_starts"])
+        st.frame_index = int(d["init_frame_index"])
+    return st
+
+
+def engine_id(name):
+    return {"streaming": 1, "resident": 2}[name]
+
+
+@pytest.mark.parametrize("engine", ENGINES)
+@pytest.mark.parametrize("name", sorted(STREAMS))
+def test_golden_stream_bit_exact(name, engine):
+    """Chained packets through the device state machine equal the
+    reference's own per-packet outputs bit for bit."""
+    d = load(name)
+    mc, sc, th = STREAMS[name]
+    st = device_state(d, sc, engine=engine_id(engine))
+    seen = []
+    for k, pk in enumerate(packets_of(d)):
+        _, frame, res = evr.process_packet(
+            st, pk, mc, sc, th, debug_sink=(lambda i, s, m: seen.append((s, m))) if k == 0 else None)
+        assert res.iterations == int(d["iterations"][k])
+        assert np.array_equal(frame, d["u"][k]), f"u packet {k}"
+        if "p" in d:
+            assert np.array_equal(st.p, d["p"][k]), f"p packet {k}"
+        assert np.array_equal(st.raw_timestamps, d["raw_ing"][k])
+        assert np.array_equal(st.f, frame)
+        assert res.rel_change == pytest.approx(float(d["rel_change"][k]), rel=1e-9)
+    if "p_last" in d:
+        assert np.array_equal(st.p, d["p_last"])
+    # the debug view of packet 0 is the reference's surface and metric
+    s, m = seen[0]
+    if "t_den" in d and mc.enabled:
+        assert np.array_equal(s.t, d["t_den"][0])
+        assert np.array_equal(m.G, d["G"][0]) and np.array_equal(m.tx, d["tx"][0])
+
+
+@pytest.mark.parametrize("name", ["stream_u_32x24.npz", "stream_s_dvs128.npz"])
+def test_teacher_forced_ingest_bit_exact(name):
+    """apply_event over a packet (duplicates included) == reference f, raw."""
+    d = load(name)
+    sc = evr.SolverConfig()
+    st = device_state(d, sc)
+    pk = packets_of(d)
+    prev_u = d["init_u"] if "init_u" in d else np.full(d["u"][0].shape, 1.5)
+    prev_raw = d["init_raw"] if "init_raw" in d else np.zeros(d["u"][0].shape, np.int64)
+    for k in range(len(pk)):
+        st.f = (prev_u if k == 0 else d["u"][k - 1]).copy()
+        st.raw_timestamps = (prev_raw if k == 0 else d["raw_ing"][k - 1]).copy()
+        ctx = evr.pipeline._prepare(st, evr.ManifoldConfig(), sc, evr.Thresholds())
+        from paper_1607_06283_b200 import _lib
+        ctx.call("evr_ingest", _lib.ptr(pk[k]), len(pk[k]))
+        st._after_device_write(in_place=("f", "raw_timestamps"))
+        assert np.array_equal(st.f, d["f_ing"][k])
+        assert np.array_equal(st.raw_timestamps, d["raw_ing"][k])
+
+
+def test_operator_api_bit_exact():
+    o = load("ops.npz")
+    t = evr.normalize_timestamps(o["norm_raw"], 1000, 3.0, 1000.0)
+    assert np.array_equal(t.t, o["norm_t"])
+    td = evr.denoise_timestamps(evr.TimeSurface(o["den_in"], 3.0), 0.3, 50)
+    assert np.array_equal(td.t, o["den_out"])
+    m = evr.compute_metric(o["met_in"])
+    for a, k in ((m.tx, "met_tx"), (m.ty, "met_ty"), (m.G, "met_G"), (m.sqrtG, "met_sqrtG")):
+        assert np.array_equal(a, o[k])
+    assert np.array_equal(np.stack(m.coeffs), o["met_coeffs"])
+    assert np.array_equal(evr.div_xy(o["div_qx"], o["div_qy"]), o["div_out"])
+    assert np.array_equal(evr.surface_gradient(o["sg_u"], m), o["sg_out"])
+    assert np.array_equal(evr.surface_gradient_adjoint(o["sg_p"], m), o["sga_out"])
+    cfg = evr.SolverConfig(lam=3.0)
+    assert np.array_equal(evr.prox_data(o["pd_ubar"], o["pd_f"], m, 0.3, cfg), o["prox_data_out"])
+    assert np.array_equal(evr.prox_dual(o["prox_dual_in"], m), o["prox_dual_out"])
+    assert evr.energy(o["sg_u"], o["pd_f"], m, 0.7) == pytest.approx(o["energy_val"][0], rel=1e-12)
+
+
+def test_operator_solve_warm_start_and_trace():
+    o = load("ops.npz")
+    m = evr.MetricField(tx=o["solve_tx"], ty=o["solve_ty"], G=o["solve_G"], sqrtG=o["solve_sqrtG"])
+    trace = []
+    res = evr.primal_dual_solve(o["solve_f"], m, evr.SolverConfig(lam=0.9, max_iterations=60),
+                                u_init=o["solve_u0"], p_init=o["solve_p0"], trace=trace)
+    assert np.array_equal(res.u, o["solve_u"]) and np.array_equal(res.p, o["solve_p"])
+    tr = np.array(trace)
+    assert np.array_equal(tr[:, 0], o["solve_trace"][:, 0])
+    np.testing.assert_allclose(tr[:, 1], o["solve_trace"][:, 1], rtol=1e-12)
+    np.testing.assert_allclose(tr[:, 2], o["solve_trace"][:, 2], rtol=1e-9)
+
+
+def test_operator_early_stop():
+    o = load("ops.npz")
+    cfg = evr.SolverConfig(lam=0.7, max_iterations=500, convergence_tol=1e-5)
+    res = evr.primal_dual_solve(o["tol_f"], evr.flat_metric((10, 10)), cfg)
+    assert res.iterations == int(o["tol_iters"][0])
+    assert np.array_equal(res.u, o["tol_u"]) and np.array_equal(res.p, o["tol_p"])
+
+
+def test_operator_rof():
+    o = load("ops.npz")
+    out = evr.rof_manifold_solve(o["rof_f"], evr.flat_metric((20, 20)), 8.0, 250)
+    assert np.array_equal(out, o["rof_flat"])
+    out = evr.rof_manifold_solve(o["rof_f"], evr.compute_metric(o["rof_h"]), 4.0, 120)
+    assert np.array_equal(out, o["rof_steep"])
+
+
+def uniform_packets(H, W, n_packets, epp, seed, t_step):
+    rng = np.random.default_rng(seed)
+    n = n_packets * epp
+    ev = evr.make_event_array(rng.integers(0, W, n), rng.integers(0, H, n),
+                              rng.choice([-1, 1], n), np.arange(n, dtype=np.int64) * t_step)
+    return [ev[s:s + epp] for s in range(0, n, epp)]
+
+
+@pytest.mark.parametrize("engine", ENGINES)
+@pytest.mark.parametrize("H,W,epp,iters", [(260, 346, 500, 50), (128, 128, 500, 50),
+                                           (33, 70, 1500, 17)])
+def test_full_size_chained_vs_oracle(H, W, epp, iters, engine):
+    """DAVIS346 / DVS128 generator-U streams, plus a packet
+    larger than one ingest chunk: bit-exact with the C oracle, chained."""
+    sc = evr.SolverConfig(max_iterations=iters)
+    st = evr.init_state(evr.SensorGeometry(W, H), sc, precision=0, engine=engine_id(engine))
+    ref = O.OracleStream(H, W, O.make_config(max_iterations=iters))
+    for pk in uniform_packets(H, W, 3, epp, seed=H + W, t_step=1):
+        _, frame, res = evr.process_packet(st, pk, evr.ManifoldConfig(), sc, evr.Thresholds())
+        it, rel = ref.process(np.ascontiguousarray(pk))
+        assert res.iterations == it
+        assert np.array_equal(frame, ref.u)
+        assert res.rel_change == pytest.approx(rel, rel=1e-9)
+    assert np.array_equal(st.p, ref.p)
+    assert np.array_equal(st.raw_timestamps, ref.raw)
+
+
+def test_float32_engine_within_log_tolerance():
+    """float32 surface+solver: max |log u - log u_ref| <= 1e-4, teacher-forced
+    per packet and chained over the DVS128 S-stream fixture."""
+    d = load("stream_s_dvs128.npz")
+    sc = evr.SolverConfig()
+    st = device_state(d, sc, precision=1)
+    worst = 0.0
+    for k, pk in enumerate(packets_of(d)):
+        _, frame, res = evr.process_packet(st, pk, evr.ManifoldConfig(), sc, evr.Thresholds())
+        worst = max(worst, float(np.abs(np.log(frame) - np.log(d["u"][k])).max()))
+    assert worst <= LOG_TOL, worst
+    # ingest stays float64: f after ingest equals the reference given the same f
+    st.f = d["u"][0].copy()
+    st.raw_timestamps = d["raw_ing"][0].copy()
+    evr.apply_event(st, evr.Event(x=3, y=4, polarity=1, timestamp=10**9), evr.Thresholds(), sc)
+    assert st.f[4, 3] == min(max(d["u"][0][4, 3] * math.exp(0.15), 1.0), 2.0)
+
+
+def test_float32_chained_u_stream_tolerance():
+    H, W = 260, 346
+    sc = evr.SolverConfig()
+    st = evr.init_state(evr.SensorGeometry(W, H), sc, precision=1)
+    ref = O.OracleStream(H, W, O.make_config())
+    worst = 0.0
+    for pk in uniform_packets(H, W, 6, 500, seed=11, t_step=1):
+        _, frame, _ = evr.process_packet(st, pk, evr.ManifoldConfig(), sc, evr.Thresholds())
+        ref.process(np.ascontiguousarray(pk))
+        worst = max(worst, float(np.abs(np.log(frame) - np.log(ref.u)).max()))
+    assert worst <= LOG_TOL, worst
+
+
+def test_duplicates_and_clamp_order():
+    """Multiply-then-clamp per event in stream order."""
+    geom = evr.SensorGeometry(4, 3)
+    sc = evr.SolverConfig()
+    st = evr.init_state(geom, sc)
+    st.f = np.full((3, 4), 1.95)
+    seq = [evr.Event(0, 0, 1, 1), evr.Event(1, 2, -1, 2), evr.Event(0, 0, -1, 3),
+           evr.Event(0, 0, 1, 4), evr.Event(1, 2, -1, 5)] * 300  # 1500 events, 2 chunks
+    ev = evr.events_to_array(seq)
+    ev["t"] = np.arange(len(ev))
+    ctx = evr.pipeline._prepare(st, evr.ManifoldConfig(), sc, evr.Thresholds())
+    from paper_1607_06283_b200 import _lib
+    ctx.call("evr_ingest", _lib.ptr(ev), len(ev))
+    st._after_device_write(in_place=("f", "raw_timestamps"))
+    f = np.full((3, 4), 1.95)
+    raw = np.zeros((3, 4), np.int64)
+    O.ingest(f, raw, ev, O.make_config())
+    assert np.array_equal(st.f, f) and np.array_equal(st.raw_timestamps, raw)
+
+
+def test_out_of_range_event_raises():
+    st = evr.init_state(evr.SensorGeometry(8, 8), evr.SolverConfig())
+    with pytest.raises(IndexError):
+        evr.process_packet(st, [evr.Event(8, 0, 1, 1)], evr.ManifoldConfig(),
+                           evr.SolverConfig(), evr.Thresholds())
+
+
+def test_repeat_runs_bitwise_deterministic():
+    H, W = 96, 80
+    outs = []
+    for _ in range(2):
+        st = evr.init_state(evr.SensorGeometry(W, H), evr.SolverConfig())
+        for pk in uniform_packets(H, W, 2, 700, seed=5, t_step=3):
+            _, frame, _ = evr.process_packet(st, pk, evr.ManifoldConfig(), evr.SolverConfig(),
+                                             evr.Thresholds())
+        outs.append((frame.copy(), st.p.copy()))
+    assert np.array_equal(outs[0][0], outs[1][0]) and np.array_equal(outs[0][1], outs[1][1])
+
+
+def test_engines_agree_bitwise():
+    H, W = 150, 211
+    res = {}
+    for eng in ENGINES:
+        st = evr.init_state(evr.SensorGeometry(W, H), evr.SolverConfig(), engine=engine_id(eng))
+        for pk in uniform_packets(H, W, 3, 500, seed=9, t_step=2):
+            _, frame, _ = evr.process_packet(st, pk, evr.ManifoldConfig(), evr.SolverConfig(),
+                                             evr.Thresholds())
+        res[eng] = (frame.copy(), st.p.copy(), st.engine())
+    assert np.array_equal(res["streaming"][0], res["resident"][0])
+    assert np.array_equal(res["streaming"][1], res["resident"][1])
