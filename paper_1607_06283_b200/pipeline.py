@@ -21,6 +21,7 @@ and ``raw_timestamps`` in place.
 
 from __future__ import annotations
 
+import ctypes
 import math
 import os
 import sys
@@ -300,7 +301,7 @@ def process_packet_arrays(state, events, manifold_cfg, solver_cfg, thresholds, t
     info = _lib.SolveInfo()
     split = (debug_sink is not None or trace is not None or solver_cfg.convergence_tol > 0)
     if not split:
-        ctx.call("evr_process_packet", _lib.ptr(events), n, float(window), info)
+        ctx.call("evr_process_packet", _lib.ptr(events), n, float(window), ctypes.byref(info))
     else:
         ctx.call("evr_packet_begin", _lib.ptr(events), n, float(window))
         if debug_sink is not None:
@@ -317,7 +318,7 @@ def process_packet_arrays(state, events, manifold_cfg, solver_cfg, thresholds, t
         if trace is not None:
             et = np.zeros(solver_cfg.max_iterations)
             rt = np.zeros(solver_cfg.max_iterations)
-        ctx.call("evr_packet_solve", info, _lib.ptr(et), _lib.ptr(rt))
+        ctx.call("evr_packet_solve", ctypes.byref(info), _lib.ptr(et), _lib.ptr(rt))
         if trace is not None:
             for k in range(info.iterations):
                 trace.append((k + 1, float(et[k]), float(rt[k])))
