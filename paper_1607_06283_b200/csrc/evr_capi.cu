@@ -68,10 +68,12 @@ struct evr_ctx {
   int64_t graph_launches[3] = {0, 0, 0};
   int64_t launches = 0;
   int engine = EVR_ENGINE_STREAMING;  // resolved
-  ResidentPlan rplan{};
-  unsigned* d_flags = nullptr;        // resident engine sync words
-  char* d_xchg = nullptr;             // resident engine halo exchange rows
-  size_t xchg_bytes = 0;
+  // resident engine plan + buffers
+  int r_nb = 0, r_R = 0, r_nt = 0;
+  size_t r_smem = 0;
+  unsigned long long* d_flags = nullptr;  // per-CTA progress words
+  void* d_xchg = nullptr;                 // boundary-row ping-pong buffer
+  unsigned* d_ticket = nullptr;
   std::string err;
 
   template <class T> T* fld(int k) const { return reinterpret_cast<T*>(slab + field_stride * k); }
@@ -225,11 +227,114 @@ template <class T> int enqueue_packet(evr_ctx* ctx, int which) {
   return n;
 }
 
+// ---- resident engine glue ---------------------------------------------------
+
+template <class T> int resident_nt(int R, int W) { return (int64_t)R * W >= 512 ? 512 : 256; }
+
+// Does the band decomposition fit on chip?  One CTA per SM, (R+2) rows of
+// every field in shared memory.
+template <class T> bool resident_plan(evr_ctx* ctx) {
+  int sms = 0, optin = 0;
+  if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device) != cudaSuccess ||
+      cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device) !=
+          cudaSuccess)
+    return false;
+  const int H = ctx->H, W = ctx->W;
+  const int nb = std::min(H, sms);
+  const int R = (H + nb - 1) / nb;
+  const int nt = resident_nt<T>(R, W);
+  const size_t smem = resident_smem_bytes<T>(R, W, nt);
+  if (smem + 1024 > (size_t)optin) return false;
+  ctx->r_nb = nb;
+  ctx->r_R = R;
+  ctx->r_nt = nt;
+  ctx->r_smem = smem;
+  return true;
+}
+
+template <class T> int resident_alloc(evr_ctx* ctx) {
+  cudaFree(ctx->d_flags);
+  cudaFree(ctx->d_xchg);
+  cudaFree(ctx->d_ticket);
+  ctx->d_flags = nullptr;
+  ctx->d_xchg = nullptr;
+  ctx->d_ticket = nullptr;
+  CK(cudaMalloc(&ctx->d_flags, sizeof(unsigned long long) * ctx->r_nb));
+  CK(cudaMemset(ctx->d_flags, 0, sizeof(unsigned long long) * ctx->r_nb));
+  CK(cudaMalloc(&ctx->d_xchg, sizeof(T) * 2 * ctx->r_nb * 2 * 3 * (size_t)ctx->W));
+  CK(cudaMalloc(&ctx->d_ticket, sizeof(unsigned)));
+  CK(cudaMemset(ctx->d_ticket, 0, sizeof(unsigned)));
+  auto set_attr = [&](const void* fn) -> cudaError_t {
+    return cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ctx->r_smem);
+  };
+  CK(set_attr(ctx->r_nt == 512 ? (const void*)k_resident<T, 512> : (const void*)k_resident<T, 256>));
+  return EVR_OK;
+}
+
+template <class T> int resident_enqueue(evr_ctx* ctx, int which) {
+  if (which != 2)
+    return fail(ctx, EVR_ERR_UNSUPPORTED, "resident engine runs whole packets only");
+  const evr_config& g = ctx->cfg;
+  ResArgs<T> a;
+  a.hdr = ctx->hdr();
+  a.f = ctx->f;
+  a.raw = ctx->raw;
+  a.u = ctx->fld<T>(F_U);
+  a.p1 = ctx->fld<T>(F_P1);
+  a.p2 = ctx->fld<T>(F_P2);
+  a.p3 = ctx->fld<T>(F_P3);
+  a.t = ctx->fld<T>(F_T);
+  a.tx = ctx->fld<T>(F_TX);
+  a.ty = ctx->fld<T>(F_TY);
+  a.G = ctx->fld<T>(F_G);
+  a.sg = ctx->fld<T>(F_SG);
+  a.xchg = reinterpret_cast<T*>(ctx->d_xchg);
+  a.flags = ctx->d_flags;
+  a.part = ctx->part;
+  a.ticket = ctx->d_ticket;
+  a.info = ctx->d_info;
+  a.err = ctx->d_err;
+  a.H = ctx->H;
+  a.W = ctx->W;
+  a.nb = ctx->r_nb;
+  a.R = ctx->r_R;
+  a.tv_iters = g.denoise_iterations;
+  a.pd_iters = g.max_iterations;
+  a.manifold = g.manifold_enabled;
+  a.t_scale = g.t_scale;
+  a.c_pos = g.c_pos;
+  a.c_neg = g.c_neg;
+  a.u_min = g.u_min;
+  a.u_max = g.u_max;
+  const double step = 1.0 / std::sqrt(8.0);  // surface.py:158
+  a.tau = (T)g.tau;
+  a.sigma = (T)g.sigma;
+  a.tl = (T)(g.tau * g.lam);
+  a.tv_step = (T)step;
+  a.shrink = (T)(step * g.denoise_weight);
+  a.t_scaleT = (T)g.t_scale;
+  a.uminT = (T)g.u_min;
+  a.umaxT = (T)g.u_max;
+  cudaLaunchConfig_t lc = {};
+  lc.gridDim = dim3(ctx->r_nb);
+  lc.blockDim = dim3(ctx->r_nt);
+  lc.dynamicSmemBytes = ctx->r_smem;
+  lc.stream = ctx->stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;  // all CTAs co-resident
+  attr[0].val.cooperative = 1;
+  lc.attrs = attr;
+  lc.numAttrs = 1;
+  cudaError_t e = ctx->r_nt == 512 ? cudaLaunchKernelEx(&lc, k_resident<T, 512>, a)
+                                   : cudaLaunchKernelEx(&lc, k_resident<T, 256>, a);
+  if (e != cudaSuccess) return fail(ctx, EVR_ERR_CUDA, "resident launch: %s", cudaGetErrorString(e));
+  return 1;
+}
+
 int enqueue_packet_any(evr_ctx* ctx, int which) {
   if (ctx->engine == EVR_ENGINE_RESIDENT) {
-    int r = ctx->prec == EVR_PREC_F64 ? resident_enqueue<double>(ctx, which)
-                                      : resident_enqueue<float>(ctx, which);
-    return r;
+    return ctx->prec == EVR_PREC_F64 ? resident_enqueue<double>(ctx, which)
+                                     : resident_enqueue<float>(ctx, which);
   }
   return ctx->prec == EVR_PREC_F64 ? enqueue_packet<double>(ctx, which)
                                    : enqueue_packet<float>(ctx, which);
@@ -578,6 +683,7 @@ void evr_destroy(evr_ctx* ctx) {
   cudaFree(ctx->d_stage);
   cudaFree(ctx->d_flags);
   cudaFree(ctx->d_xchg);
+  cudaFree(ctx->d_ticket);
   for (int i = 0; i < 2; ++i) {
     if (ctx->h_stage[i]) cudaFreeHost(ctx->h_stage[i]);
     if (ctx->stage_done[i]) cudaEventDestroy(ctx->stage_done[i]);
@@ -599,13 +705,12 @@ int evr_set_config(evr_ctx* ctx, const evr_config* cfg) {
   ctx->cfg_set = true;
   drop_graphs(ctx);
   ctx->engine = EVR_ENGINE_STREAMING;
-  if (cfg->engine != EVR_ENGINE_STREAMING && ctx->H >= 2 && ctx->W >= 2) {
-    ResidentPlan plan;
-    const bool ok = ctx->prec == EVR_PREC_F64 ? resident_plan<double>(ctx, plan)
-                                              : resident_plan<float>(ctx, plan);
+  if (cfg->engine != EVR_ENGINE_STREAMING && cfg->convergence_tol <= 0 && ctx->H >= 2 &&
+      ctx->W >= 2) {
+    const bool ok = ctx->prec == EVR_PREC_F64 ? resident_plan<double>(ctx)
+                                              : resident_plan<float>(ctx);
     if (ok) {
       ctx->engine = EVR_ENGINE_RESIDENT;
-      ctx->rplan = plan;
       int rc = ctx->prec == EVR_PREC_F64 ? resident_alloc<double>(ctx) : resident_alloc<float>(ctx);
       if (rc) return rc;
     } else if (cfg->engine == EVR_ENGINE_RESIDENT) {

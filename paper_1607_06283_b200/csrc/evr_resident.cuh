@@ -1,9 +1,460 @@
-// evr_resident.cuh -- persistent on-chip engine (placeholder: never fits)
+// evr_resident.cuh -- the resident engine: ONE persistent kernel per event
+// packet, the whole of process_packet (pipeline.py:142-171) on chip.
+//
+// Decomposition.  CTA b of a cooperative grid (<= 1 CTA per SM) owns the
+// row band [r0, r1) of the sensor (full width).  Every per-pixel field of
+// the band lives in shared memory together with one halo row above (r0-1)
+// and one below (r1); global memory is touched only to load the state at
+// the start, to exchange two boundary rows per iteration, and to write the
+// state back at the end.
+//
+// One neighbour exchange per iteration.  Each iteration recomputes on its
+// halo rows what it would otherwise have to wait for a second time
+// (SURVEY.md Appendix A.6, B.8-B.9):
+//   TV-L1 (dual first): the dual update is also run on halo row r0-1, so
+//     the primal needs no fresh px/py from the CTA above; only u_bar of the
+//     neighbours' boundary rows is exchanged.
+//   KL primal-dual (primal first): the primal (u+, v) is also run on halo
+//     row r1, so the dual needs no fresh v from the CTA below; only p1..p3
+//     of the neighbours' boundary rows are exchanged.
+// Recomputed halo values are bit-identical to the owner's (same inputs,
+// same operation order), so the band decomposition leaves every result
+// bit-identical to the single-domain reference.  Boundary rows go through
+// a ping-pong buffer in global memory (L2) and a per-CTA release/acquire
+// flag; a CTA waits only for its two neighbours, never for the grid.
+//
+// Ingest is fused: every CTA scans the packet, keeps the events of rows
+// [r0-1, r1] in stream order, and applies them with the same ordered
+// leader walk as k_ingest to its private copies of f and of the surface
+// (duplicates compound in order, last timestamp wins); raw timestamps of
+// its own rows go straight to global memory (idempotent for neighbours).
 #pragma once
-struct evr_ctx;
+
+#include <cstdint>
+
+#include "evr_kernels.cuh"
+#include "evr_math.cuh"
+
 namespace evr {
-struct ResidentPlan { int ctas = 0; };
-template <class T> bool resident_plan(evr_ctx*, ResidentPlan&) { return false; }
-template <class T> int resident_alloc(evr_ctx*) { return 0; }
-template <class T> int resident_enqueue(evr_ctx*, int) { return -5; }
+
+template <class T> struct ResArgs {
+  const PacketHdr* hdr;
+  double* f;
+  int64_t* raw;
+  T *u, *p1, *p2, *p3;           // state planes (global)
+  T *t, *tx, *ty, *G, *sg;       // surface / metric planes (global, debug view)
+  T* xchg;                       // [2][nb][2][3][W] boundary rows
+  unsigned long long* flags;     // [nb] release/acquire progress words
+  double* part;                  // [2*nb] rel_change partials
+  unsigned* ticket;              // last-CTA election for the final sum
+  evr_solve_info* info;
+  int* err;
+  int H, W, nb, R;
+  int tv_iters, pd_iters, manifold;
+  double t_scale, c_pos, c_neg, u_min, u_max;
+  T tau, sigma, tl, tv_step, shrink, t_scaleT, uminT, umaxT;
+};
+
+// plane indices in shared memory
+enum : int {
+  RP_U = 0, RP_P1, RP_P2, RP_P3, RP_A11, RP_A12, RP_A22, RP_A31, RP_A32, RP_SG, RP_FB, RP_V,
+  RP_COUNT,
+  // TV-L1 planes alias the coefficient planes (dead until the metric phase)
+  RP_T0 = RP_A11, RP_TU = RP_A12, RP_TUB = RP_A22, RP_TPX = RP_A31, RP_TPY = RP_A32
+};
+
+template <class T> __host__ __device__ inline size_t resident_smem_bytes(int R, int W, int NT) {
+  const size_t ps = (size_t)(R + 2) * W;
+  size_t b = ps * RP_COUNT * sizeof(T);
+  b = (b + 15) / 16 * 16;
+  b += ps * sizeof(double);  // F64 plane (ingest in binary64)
+  b += (size_t)NT * 2 * sizeof(int) + 64 * sizeof(double);
+  return b;
+}
+
+__device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void st_release_u64(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+struct Band {
+  int base, extra;
+  __device__ __forceinline__ int rows(int b) const { return base + (b < extra ? 1 : 0); }
+  __device__ __forceinline__ int start(int b) const { return b * base + (b < extra ? b : extra); }
+  __device__ __forceinline__ int of_row(int r) const {
+    const int big = extra * (base + 1);
+    return r < big ? r / (base + 1) : extra + (r - big) / base;
+  }
+};
+
+template <class T, int NT>
+__global__ void __launch_bounds__(NT, 1) k_resident(const ResArgs<T> a) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int tid = threadIdx.x;
+  const int b = blockIdx.x;
+  const int H = a.H, W = a.W;
+  const Band band{H / a.nb, H % a.nb};
+  const int Rb = band.rows(b);
+  const int r0 = band.start(b);
+  const int r1 = r0 + Rb;
+  const bool has_up = r0 > 0, has_dn = r1 < H;
+  const size_t PS = (size_t)(a.R + 2) * W;
+  T* pl = reinterpret_cast<T*>(smem_raw);
+  T* const U = pl + RP_U * PS;
+  T* const P1 = pl + RP_P1 * PS;
+  T* const P2 = pl + RP_P2 * PS;
+  T* const P3 = pl + RP_P3 * PS;
+  T* const A11 = pl + RP_A11 * PS;
+  T* const A12 = pl + RP_A12 * PS;
+  T* const A22 = pl + RP_A22 * PS;
+  T* const A31 = pl + RP_A31 * PS;
+  T* const A32 = pl + RP_A32 * PS;
+  T* const SG = pl + RP_SG * PS;
+  T* const FB = pl + RP_FB * PS;
+  T* const V = pl + RP_V * PS;
+  T* const T0 = pl + RP_T0 * PS;
+  T* const TU = pl + RP_TU * PS;
+  T* const TUB = pl + RP_TUB * PS;
+  T* const TPX = pl + RP_TPX * PS;
+  T* const TPY = pl + RP_TPY * PS;
+  double* const F64 =
+      reinterpret_cast<double*>(smem_raw + (PS * RP_COUNT * sizeof(T) + 15) / 16 * 16);
+  int* const kpix = reinterpret_cast<int*>(F64 + PS);
+  int* const kev = kpix + NT;
+  double* const red = reinterpret_cast<double*>(kev + NT);
+
+  const PacketHdr* hdr = a.hdr;
+  const evr_event* __restrict__ ev = reinterpret_cast<const evr_event*>(hdr + 1);
+  const int64_t n_ev = hdr->n;
+  const double now = (double)hdr->now;
+  const double window = hdr->window;
+  const unsigned long long epoch = (unsigned long long)hdr->seq << 24;
+  const size_t xrow = (size_t)3 * W;                      // one side of one CTA
+  const size_t xslot = (size_t)a.nb * 2 * xrow;           // one ping-pong slot
+
+  // rows [lo, hi] of the local frame (lr = global row - r0 + 1), flat loop
+#define EVR_FOR_ROWS(lo, hi)                                         \
+  for (int q_ = tid, n_ = ((hi) - (lo) + 1) * W; q_ < n_; q_ += NT) { \
+    const int lr = (lo) + q_ / W;                                     \
+    const int j = q_ - (lr - (lo)) * W;                               \
+    const int gi = r0 - 1 + lr;                                       \
+    const int l = lr * W + j;                                         \
+    const int64_t gk = (int64_t)gi * W + j;
+#define EVR_END_ROWS }
+
+  const int lo_halo = has_up ? 0 : 1;
+  const int hi_halo = has_dn ? Rb + 1 : Rb;
+
+  auto publish = [&](int step, const T* s0, const T* s1, const T* s2, int nf) {
+    const int slot = step & 1;
+    T* dst = a.xchg + slot * xslot + (size_t)b * 2 * xrow;
+    for (int j = tid; j < W; j += NT) {
+      const int lf = 1 * W + j, ll = Rb * W + j;
+      dst[j] = s0[lf];
+      dst[xrow + j] = s0[ll];
+      if (nf > 1) {
+        dst[W + j] = s1[lf];
+        dst[xrow + W + j] = s1[ll];
+        dst[2 * W + j] = s2[lf];
+        dst[xrow + 2 * W + j] = s2[ll];
+      }
+    }
+    __syncthreads();
+    if (tid == 0) {
+      __threadfence();
+      st_release_u64(&a.flags[b], epoch | (unsigned long long)step);
+    }
+  };
+  auto wait_neighbours = [&](int step) {
+    const unsigned long long target = epoch | (unsigned long long)step;
+    if (tid == 0 && has_up)
+      while (ld_acquire_u64(&a.flags[b - 1]) < target) __nanosleep(20);
+    if (tid == 32 && has_dn)
+      while (ld_acquire_u64(&a.flags[b + 1]) < target) __nanosleep(20);
+    __syncthreads();
+  };
+  auto fetch_halo = [&](int step, T* d0, T* d1, T* d2, int nf) {
+    const int slot = step & 1;
+    const T* src_up = a.xchg + slot * xslot + (size_t)(b - 1) * 2 * xrow + xrow;  // last row
+    const T* src_dn = a.xchg + slot * xslot + (size_t)(b + 1) * 2 * xrow;         // first row
+    for (int j = tid; j < W; j += NT) {
+      if (has_up) {
+        d0[j] = __ldcg(src_up + j);
+        if (nf > 1) {
+          d1[j] = __ldcg(src_up + W + j);
+          d2[j] = __ldcg(src_up + 2 * W + j);
+        }
+      }
+      if (has_dn) {
+        const int l = (Rb + 1) * W + j;
+        d0[l] = __ldcg(src_dn + j);
+        if (nf > 1) {
+          d1[l] = __ldcg(src_dn + W + j);
+          d2[l] = __ldcg(src_dn + 2 * W + j);
+        }
+      }
+    }
+    __syncthreads();
+  };
+
+  // ---------------------------------------------------------------- load --
+  EVR_FOR_ROWS(lo_halo, hi_halo)
+    if (a.manifold) {
+      const T v = (T)normalize_at((double)a.raw[gk], now, a.t_scale, window);
+      T0[l] = v;
+      TU[l] = v;
+      TUB[l] = v;
+      TPX[l] = T(0);
+      TPY[l] = T(0);
+    }
+    if (lr >= 1) F64[l] = a.f[gk];
+  EVR_END_ROWS
+  __syncthreads();
+
+  // -------------------------------------------------------------- ingest --
+  // apply_event (pipeline.py:114-121) for the events of rows [r0-1, r1]
+  {
+    const int lane = tid & 31, wid = tid >> 5;
+    for (int64_t base = 0; base < n_ev; base += NT) {
+      int keep = 0, lp = 0;
+      if (base + tid < n_ev) {
+        const evr_event e = ev[base + tid];
+        if (e.x >= 0 && e.x < W && e.y >= 0 && e.y < H) {
+          const int lr = e.y - (r0 - 1);
+          if (lr >= lo_halo && lr <= hi_halo) {
+            keep = 1;
+            lp = lr * W + e.x;
+          }
+        } else if (b == 0) {
+          atomicOr(a.err, 1);
+        }
+      }
+      const unsigned ball = __ballot_sync(0xffffffffu, keep);
+      if (lane == 0) red[wid] = (double)__popc(ball);
+      __syncthreads();
+      int off = 0, m = 0;
+      for (int w = 0; w < NT / 32; ++w) {
+        const int c = (int)red[w];
+        if (w < wid) off += c;
+        m += c;
+      }
+      if (keep) {
+        const int pos = off + __popc(ball & ((1u << lane) - 1u));
+        kpix[pos] = lp;
+        kev[pos] = tid;
+      }
+      __syncthreads();
+      if (tid < m) {
+        const int pix = kpix[tid];
+        bool leader = true;
+        for (int j = tid - 1; j >= 0; --j)
+          if (kpix[j] == pix) { leader = false; break; }
+        if (leader) {
+          const int lr = pix / W;
+          double v = lr >= 1 ? F64[pix] : 0.0;
+          int64_t last_t = 0;
+          for (int j = tid; j < m; ++j) {
+            if (kpix[j] != pix) continue;
+            const evr_event e = ev[base + kev[j]];
+            const double c = e.polarity > 0 ? a.c_pos : a.c_neg;
+            v = v * c;
+            if (a.u_min > v) v = a.u_min;  // Python max(value, u_min)
+            if (a.u_max < v) v = a.u_max;  // Python min(.., u_max)
+            last_t = e.t;
+          }
+          if (lr >= 1) F64[pix] = v;
+          if (a.manifold) {
+            const T tv = (T)normalize_at((double)last_t, now, a.t_scale, window);
+            T0[pix] = tv;
+            TU[pix] = tv;
+            TUB[pix] = tv;
+          }
+          if (lr >= 1 && lr <= Rb) a.raw[(int64_t)(r0 - 1 + lr) * W + (pix - lr * W)] = last_t;
+        }
+      }
+      __syncthreads();
+    }
+  }
+
+  // ------------------------------------------------------------ TV-L1 ----
+  // denoise_timestamps (surface.py:146-196), one exchange per iteration
+  int step = 0;
+  if (a.manifold) {
+    for (int it = 0; it < a.tv_iters; ++it) {
+      if (it > 0) {
+        wait_neighbours(step);
+        fetch_halo(step, TUB, nullptr, nullptr, 1);
+      }
+      EVR_FOR_ROWS(lo_halo, Rb)  // dual, own rows + halo row above
+        const T dx = j < W - 1 ? TUB[l + 1] - TUB[l] : T(0);
+        const T dy = gi < H - 1 ? TUB[l + W] - TUB[l] : T(0);
+        T px = TPX[l], py = TPY[l];
+        tv_dual_step(dx, dy, a.tv_step, px, py);
+        TPX[l] = px;
+        TPY[l] = py;
+      EVR_END_ROWS
+      __syncthreads();
+      EVR_FOR_ROWS(1, Rb)  // primal, own rows
+        const T d = div_at(TPX[l], j > 0 ? TPX[l - 1] : T(0), TPY[l], gi > 0 ? TPY[l - W] : T(0),
+                           gi, j, H, W);
+        T ub;
+        const T un = tv_primal_step(d, TU[l], T0[l], a.tv_step, a.shrink, ub);
+        TU[l] = un;
+        TUB[l] = ub;
+      EVR_END_ROWS
+      __syncthreads();
+      if (it < a.tv_iters - 1) publish(++step, TUB, nullptr, nullptr, 1);
+    }
+    // np.clip(u, 0, t_scale) (surface.py:195) -> global t (own rows)
+    EVR_FOR_ROWS(1, Rb)
+      a.t[gk] = vclip(TU[l], T(0), a.t_scaleT);
+    EVR_END_ROWS
+  }
+  // all rows of the denoised surface this band's metric reads are final
+  __syncthreads();
+  const int s_met = a.tv_iters + 1;
+  if (tid == 0) {
+    __threadfence();
+    st_release_u64(&a.flags[b], epoch | (unsigned long long)s_met);
+  }
+  if (a.manifold) {
+    const int b_lo = band.of_row(has_up ? r0 - 1 : r0);
+    const int b_hi = band.of_row(r1 + 1 < H ? r1 + 1 : H - 1);
+    const int nwait = b_hi - b_lo + 1;
+    if (tid < nwait && b_lo + tid != b)
+      while (ld_acquire_u64(&a.flags[b_lo + tid]) < (epoch | (unsigned long long)s_met))
+        __nanosleep(20);
+  }
+  __syncthreads();
+  step = s_met;
+
+  // ------------------------------------------------------------ metric ---
+  // compute_metric + coeffs (surface.py:81-90, :199-205), solver constants
+  EVR_FOR_ROWS(lo_halo, hi_halo)
+    T gx = T(0), gy = T(0);
+    if (a.manifold) {
+      const T tc = __ldcg(a.t + gk);
+      gx = j < W - 1 ? __ldcg(a.t + gk + 1) - tc : T(0);
+      gy = gi < H - 1 ? __ldcg(a.t + gk + W) - tc : T(0);
+    }
+    const T g = metric_G(gx, gy);
+    const T s = sqrt(g);
+    const Coef<T> c = coeffs_of(gx, gy, g);
+    A11[l] = c.a11;
+    A12[l] = c.a12;
+    A22[l] = c.a22;
+    A31[l] = c.a31;
+    A32[l] = c.a32;
+    SG[l] = s;
+    if (lr >= 1) FB[l] = T(4) * (a.tl * s) * (T)F64[l];
+    if (lr >= 1 && lr <= Rb) {
+      a.tx[gk] = gx;
+      a.ty[gk] = gy;
+      a.G[gk] = g;
+      a.sg[gk] = s;
+    }
+    if (lr >= 1) U[l] = a.u[gk];
+    P1[l] = a.p1[gk];
+    P2[l] = a.p2[gk];
+    P3[l] = a.p3[gk];
+  EVR_END_ROWS
+  __syncthreads();
+
+  // ------------------------------------------------------- primal-dual ---
+  // primal_dual_solve (solve.py:207-261), warm start from the state
+  double rd = 0.0, ro = 0.0;
+  for (int it = 0; it < a.pd_iters; ++it) {
+    const bool last = it == a.pd_iters - 1;
+    if (it > 0) {
+      wait_neighbours(step);
+      fetch_halo(step, P1, P2, P3, 3);
+    }
+    EVR_FOR_ROWS(1, hi_halo)  // primal + over-relaxation, own rows + halo below
+      T qx, qy, qxl = T(0), qyu = T(0), dm;
+      q_of(Coef<T>{A11[l], A12[l], A22[l], A31[l], A32[l]}, P1[l], P2[l], P3[l], qx, qy);
+      if (j > 0)
+        q_of(Coef<T>{A11[l - 1], A12[l - 1], A22[l - 1], A31[l - 1], A32[l - 1]}, P1[l - 1],
+             P2[l - 1], P3[l - 1], qxl, dm);
+      if (gi > 0)
+        q_of(Coef<T>{A11[l - W], A12[l - W], A22[l - W], A31[l - W], A32[l - W]}, P1[l - W],
+             P2[l - W], P3[l - W], dm, qyu);
+      const T d = div_at(qx, qxl, qy, qyu, gi, j, H, W);
+      const T uk = U[l];
+      const T nu = kl_primal(d, uk, a.tl * SG[l], FB[l], a.tau, a.uminT, a.umaxT);
+      V[l] = nu * T(2) - uk;
+      U[l] = nu;
+      if (last && lr <= Rb) {
+        const double e = (double)nu - (double)uk;
+        rd += e * e;
+        ro += (double)uk * (double)uk;
+      }
+    EVR_END_ROWS
+    __syncthreads();
+    EVR_FOR_ROWS(1, Rb)  // dual ascent + ball projection, own rows
+      const T gx = j < W - 1 ? V[l + 1] - V[l] : T(0);
+      const T gy = gi < H - 1 ? V[l + W] - V[l] : T(0);
+      T q1 = P1[l], q2 = P2[l], q3 = P3[l];
+      dual_step(Coef<T>{A11[l], A12[l], A22[l], A31[l], A32[l]}, a.sigma, gx, gy, SG[l], q1, q2,
+                q3);
+      P1[l] = q1;
+      P2[l] = q2;
+      P3[l] = q3;
+    EVR_END_ROWS
+    __syncthreads();
+    if (!last) publish(++step, P1, P2, P3, 3);
+  }
+  if (a.pd_iters < 2) {
+    // neighbours may still be loading our rows of u / p as halos
+    publish(++step, P1, P2, P3, 3);
+    wait_neighbours(step);
+  }
+
+  // ---------------------------------------------------------- epilogue ---
+  // state.u = u+, state.p, state.f = copy(u+) (pipeline.py:167-170)
+  EVR_FOR_ROWS(1, Rb)
+    const T v = U[l];
+    a.u[gk] = v;
+    a.f[gk] = (double)v;
+    a.p1[gk] = P1[l];
+    a.p2[gk] = P2[l];
+    a.p3[gk] = P3[l];
+  EVR_END_ROWS
+#undef EVR_FOR_ROWS
+#undef EVR_END_ROWS
+
+  // rel_change = |u+ - u| / max(|u|, 1e-30) (solve.py:246-249): fixed-order
+  // block tree, per-CTA partials, last CTA folds them in index order
+  const double sd = block_sum<NT>(rd, red);
+  const double so = block_sum<NT>(ro, red);
+  __shared__ bool is_last;
+  if (tid == 0) {
+    a.part[2 * b] = sd;
+    a.part[2 * b + 1] = so;
+    __threadfence();
+    is_last = atomicAdd(a.ticket, 1u) == (unsigned)(a.nb - 1);
+  }
+  __syncthreads();
+  if (is_last) {
+    __threadfence();
+    double d = 0.0, o = 0.0;
+    for (int k = tid; k < a.nb; k += NT) {
+      d += __ldcg(a.part + 2 * k);
+      o += __ldcg(a.part + 2 * k + 1);
+    }
+    d = block_sum<NT>(d, red);
+    o = block_sum<NT>(o, red);
+    if (tid == 0) {
+      const double den = sqrt(o);
+      a.info->rel_change = sqrt(d) / (den > 1e-30 ? den : 1e-30);
+      a.info->iterations = a.pd_iters;
+      *a.ticket = 0u;
+    }
+  }
+}
+
 }  // namespace evr
