@@ -24,7 +24,7 @@ using namespace evr;
 namespace {
 
 constexpr int kNT = 256;          // 1-D block size
-constexpr int kIngestCH = 1024;   // ingest chunk / CTA size
+constexpr int kIngestNT = 256;    // ingest CTA size (events per chunk)
 constexpr int kRedBlocks = 296;   // reduction partial blocks (2 x 148 SMs)
 
 enum Field {
@@ -128,14 +128,23 @@ template <class T> CoefPlanes<T> coefs(const evr_ctx* c) {
 
 // ---- per-packet sequence (streaming engine) -------------------------------
 
+// banded ordered ingest: ~2 CTAs per SM, each owning a block of rows
+void launch_ingest(evr_ctx* ctx) {
+  const int rows_per = std::max(1, (ctx->H + 295) / 296);
+  const int nb = (ctx->H + rows_per - 1) / rows_per;
+  const evr_config& g = ctx->cfg;
+  k_ingest<kIngestNT><<<nb, kIngestNT, 0, ctx->stream>>>(ctx->hdr(), ctx->f, ctx->raw, ctx->H,
+                                                        ctx->W, rows_per, g.c_pos, g.c_neg,
+                                                        g.u_min, g.u_max, ctx->d_err);
+}
+
 // ingest -> normalize -> TV-L1 -> metric (+ solver constants)
 template <class T> int enqueue_surface(evr_ctx* ctx) {
   const evr_config& g = ctx->cfg;
   cudaStream_t s = ctx->stream;
   const int H = ctx->H, W = ctx->W;
   const int64_t N = ctx->N;
-  k_ingest<kIngestCH><<<1, kIngestCH, 0, s>>>(ctx->hdr(), ctx->f, ctx->raw, H, W, g.c_pos,
-                                               g.c_neg, g.u_min, g.u_max, ctx->d_err);
+  launch_ingest(ctx);
   int n = 1;
   if (g.manifold_enabled) {
     T *t = ctx->fld<T>(F_T), *tu = ctx->fld<T>(F_TU), *tub = ctx->fld<T>(F_TUB);
@@ -244,7 +253,10 @@ template <class T> bool resident_plan(evr_ctx* ctx) {
   const int R = (H + nb - 1) / nb;
   const int nt = resident_nt<T>(R, W);
   const size_t smem = resident_smem_bytes<T>(R, W, nt);
-  if (smem + 1024 > (size_t)optin) return false;
+  const size_t static_smem = nt == 512 ? sizeof(IngestSort<512>::Storage) : sizeof(IngestSort<256>::Storage);
+  if (smem + static_smem + 1024 > (size_t)optin) return false;
+  // local pixel keys of the ingest sort must fit 32 bits
+  if ((uint64_t)(R + 2) * W >= (1ull << (32 - IngestSort<512>::LOG_NT)) - 1) return false;
   ctx->r_nb = nb;
   ctx->r_R = R;
   ctx->r_nt = nt;
@@ -767,9 +779,7 @@ int evr_ingest(evr_ctx* ctx, const evr_event* events, int64_t n) {
   if (n <= 0) return EVR_OK;
   if (!events) return fail(ctx, EVR_ERR_INVALID, "null events");
   if ((rc = stage_host_packet(ctx, events, n, 1.0))) return rc;
-  k_ingest<kIngestCH><<<1, kIngestCH, 0, ctx->stream>>>(ctx->hdr(), ctx->f, ctx->raw, ctx->H,
-                                                        ctx->W, ctx->cfg.c_pos, ctx->cfg.c_neg,
-                                                        ctx->cfg.u_min, ctx->cfg.u_max, ctx->d_err);
+  launch_ingest(ctx);
   ctx->launches += 1;
   if ((rc = launch_err(ctx, "ingest"))) return rc;
   CK(cudaStreamSynchronize(ctx->stream));

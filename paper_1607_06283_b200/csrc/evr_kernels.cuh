@@ -11,6 +11,7 @@
 
 #include <cstdint>
 
+#include "evr_ingest.cuh"
 #include "evr_math.cuh"
 #include "../../include/evr.h"
 
@@ -39,55 +40,29 @@ template <class T> struct CoefPlanes {
   const int64_t k = (int64_t)i * W + j;
 
 // ---------------------------------------------------------------- ingest --
-// apply_event (pipeline.py:114-121) for every event of the packet, in
-// stream order, bit-exact including duplicates: one CTA walks the packet in
-// chunks of CH events; inside a chunk the first event of each pixel is the
-// pixel's leader and applies that pixel's events of the chunk in order
-// (multiply, clamp after every step), so the compounding order and the
-// last-wins timestamp (surface.py:124-127) match the sequential reference.
-// Chunks are separated by a CTA barrier, which orders them.
-template <int CH>
-__global__ void __launch_bounds__(CH)
-k_ingest(const PacketHdr* __restrict__ hdr, double* __restrict__ f, int64_t* __restrict__ raw, int H, int W,
-         double c_pos, double c_neg, double u_min, double u_max, int* err) {
-  __shared__ int spix[CH];
+// apply_event (pipeline.py:114-121) for every event of the packet, bit-exact
+// including duplicates (evr_ingest.cuh): CTA b owns rows
+// [b*rows_per, (b+1)*rows_per) and applies the packet's events of those rows
+// in stream order; no two CTAs touch the same pixel.
+template <int NT>
+__global__ void __launch_bounds__(NT)
+k_ingest(const PacketHdr* __restrict__ hdr, double* __restrict__ f, int64_t* __restrict__ raw,
+         int H, int W, int rows_per, double c_pos, double c_neg, double u_min, double u_max,
+         int* err) {
+  __shared__ typename IngestSort<NT>::Storage sm;
   // the packet's events follow the header in the staging buffer
   const evr_event* __restrict__ ev = reinterpret_cast<const evr_event*>(hdr + 1);
-  const int64_t n = hdr->n;
-  const int tid = threadIdx.x;
-  for (int64_t base = 0; base < n; base += CH) {
-    const int m = (int)((n - base) < CH ? (n - base) : CH);
-    int pix = -1 - tid;  // never matches a real pixel or another lane
-    if (tid < m) {
-      const evr_event e = ev[base + tid];
-      if (e.x >= 0 && e.x < W && e.y >= 0 && e.y < H)
-        pix = e.y * W + e.x;
-      else
-        atomicOr(err, 1);
-    }
-    spix[tid] = pix;
-    __syncthreads();
-    if (tid < m && pix >= 0) {
-      bool leader = true;
-      for (int j = tid - 1; j >= 0; --j)
-        if (spix[j] == pix) { leader = false; break; }
-      if (leader) {
-        double v = f[pix];
-        int last = tid;
-        for (int j = tid; j < m; ++j) {
-          if (spix[j] != pix) continue;
-          const double c = ev[base + j].polarity > 0 ? c_pos : c_neg;
-          v = v * c;
-          if (u_min > v) v = u_min;  // Python max(value, u_min)
-          if (u_max < v) v = u_max;  // Python min(.., u_max)
-          last = j;
-        }
-        f[pix] = v;
-        raw[pix] = ev[base + last].t;
-      }
-    }
-    __syncthreads();
-  }
+  const int row_lo = blockIdx.x * rows_per;
+  const int row_hi = min(H, row_lo + rows_per) - 1;
+  double* fb = f + (int64_t)row_lo * W;
+  int64_t* rb = raw + (int64_t)row_lo * W;
+  ordered_ingest<NT>(
+      ev, hdr->n, H, W, row_lo, row_hi, c_pos, c_neg, u_min, u_max, sm,
+      blockIdx.x == 0 ? err : nullptr, [&](int lp) { return fb[lp]; },
+      [&](int lp, double v, int64_t t) {
+        fb[lp] = v;
+        rb[lp] = t;
+      });
 }
 
 // ------------------------------------------------------------- surface --

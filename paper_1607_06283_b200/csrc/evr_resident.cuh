@@ -23,15 +23,16 @@
 // a ping-pong buffer in global memory (L2) and a per-CTA release/acquire
 // flag; a CTA waits only for its two neighbours, never for the grid.
 //
-// Ingest is fused: every CTA scans the packet, keeps the events of rows
-// [r0-1, r1] in stream order, and applies them with the same ordered
-// leader walk as k_ingest to its private copies of f and of the surface
+// Ingest is fused: every CTA scans the packet and applies the events of
+// rows [r0-1, r1] with the same ordered, sort-grouped walk as k_ingest
+// (evr_ingest.cuh) to its private copies of f and of the surface
 // (duplicates compound in order, last timestamp wins); raw timestamps of
 // its own rows go straight to global memory (idempotent for neighbours).
 #pragma once
 
 #include <cstdint>
 
+#include "evr_ingest.cuh"
 #include "evr_kernels.cuh"
 #include "evr_math.cuh"
 
@@ -68,7 +69,7 @@ template <class T> __host__ __device__ inline size_t resident_smem_bytes(int R, 
   size_t b = ps * RP_COUNT * sizeof(T);
   b = (b + 15) / 16 * 16;
   b += ps * sizeof(double);  // F64 plane (ingest in binary64)
-  b += (size_t)NT * 2 * sizeof(int) + 64 * sizeof(double);
+  b += 64 * sizeof(double);  // reduction scratch
   return b;
 }
 
@@ -124,9 +125,7 @@ __global__ void __launch_bounds__(NT, 1) k_resident(const ResArgs<T> a) {
   T* const TPY = pl + RP_TPY * PS;
   double* const F64 =
       reinterpret_cast<double*>(smem_raw + (PS * RP_COUNT * sizeof(T) + 15) / 16 * 16);
-  int* const kpix = reinterpret_cast<int*>(F64 + PS);
-  int* const kev = kpix + NT;
-  double* const red = reinterpret_cast<double*>(kev + NT);
+  double* const red = F64 + PS;
 
   const PacketHdr* hdr = a.hdr;
   const evr_event* __restrict__ ev = reinterpret_cast<const evr_event*>(hdr + 1);
@@ -217,68 +216,27 @@ __global__ void __launch_bounds__(NT, 1) k_resident(const ResArgs<T> a) {
   __syncthreads();
 
   // -------------------------------------------------------------- ingest --
-  // apply_event (pipeline.py:114-121) for the events of rows [r0-1, r1]
+  // apply_event (pipeline.py:114-121) for the events of rows [r0-1, r1]:
+  // private copies of f / the surface, raw of own rows straight to global
   {
-    const int lane = tid & 31, wid = tid >> 5;
-    for (int64_t base = 0; base < n_ev; base += NT) {
-      int keep = 0, lp = 0;
-      if (base + tid < n_ev) {
-        const evr_event e = ev[base + tid];
-        if (e.x >= 0 && e.x < W && e.y >= 0 && e.y < H) {
-          const int lr = e.y - (r0 - 1);
-          if (lr >= lo_halo && lr <= hi_halo) {
-            keep = 1;
-            lp = lr * W + e.x;
-          }
-        } else if (b == 0) {
-          atomicOr(a.err, 1);
-        }
-      }
-      const unsigned ball = __ballot_sync(0xffffffffu, keep);
-      if (lane == 0) red[wid] = (double)__popc(ball);
-      __syncthreads();
-      int off = 0, m = 0;
-      for (int w = 0; w < NT / 32; ++w) {
-        const int c = (int)red[w];
-        if (w < wid) off += c;
-        m += c;
-      }
-      if (keep) {
-        const int pos = off + __popc(ball & ((1u << lane) - 1u));
-        kpix[pos] = lp;
-        kev[pos] = tid;
-      }
-      __syncthreads();
-      if (tid < m) {
-        const int pix = kpix[tid];
-        bool leader = true;
-        for (int j = tid - 1; j >= 0; --j)
-          if (kpix[j] == pix) { leader = false; break; }
-        if (leader) {
-          const int lr = pix / W;
-          double v = lr >= 1 ? F64[pix] : 0.0;
-          int64_t last_t = 0;
-          for (int j = tid; j < m; ++j) {
-            if (kpix[j] != pix) continue;
-            const evr_event e = ev[base + kev[j]];
-            const double c = e.polarity > 0 ? a.c_pos : a.c_neg;
-            v = v * c;
-            if (a.u_min > v) v = a.u_min;  // Python max(value, u_min)
-            if (a.u_max < v) v = a.u_max;  // Python min(.., u_max)
-            last_t = e.t;
-          }
-          if (lr >= 1) F64[pix] = v;
+    __shared__ typename IngestSort<NT>::Storage ingest_sm;
+    const int row_lo = r0 - 1 + lo_halo;
+    ordered_ingest<NT>(
+        ev, n_ev, H, W, row_lo, r0 - 1 + hi_halo, a.c_pos, a.c_neg, a.u_min, a.u_max, ingest_sm,
+        b == 0 ? a.err : nullptr,
+        [&](int lp) { return lp + lo_halo * W >= W ? F64[lp + lo_halo * W] : 0.0; },
+        [&](int lp, double v, int64_t t) {
+          const int l = lp + lo_halo * W;
+          const int lr = l / W;
+          if (lr >= 1) F64[l] = v;
           if (a.manifold) {
-            const T tv = (T)normalize_at((double)last_t, now, a.t_scale, window);
-            T0[pix] = tv;
-            TU[pix] = tv;
-            TUB[pix] = tv;
+            const T tv = (T)normalize_at((double)t, now, a.t_scale, window);
+            T0[l] = tv;
+            TU[l] = tv;
+            TUB[l] = tv;
           }
-          if (lr >= 1 && lr <= Rb) a.raw[(int64_t)(r0 - 1 + lr) * W + (pix - lr * W)] = last_t;
-        }
-      }
-      __syncthreads();
-    }
+          if (lr >= 1 && lr <= Rb) a.raw[(int64_t)(r0 - 1) * W + l] = t;
+        });
   }
 
   // ------------------------------------------------------------ TV-L1 ----
