@@ -249,10 +249,11 @@ template <class T> bool resident_plan(evr_ctx* ctx) {
           cudaSuccess)
     return false;
   const int H = ctx->H, W = ctx->W;
-  const int nb = std::min(H, sms);
-  const int R = (H + nb - 1) / nb;
+  // equal band heights: R rows per CTA, as few CTAs as that needs
+  const int R = (H + std::min(H, sms) - 1) / std::min(H, sms);
+  const int nb = (H + R - 1) / R;
   const int nt = resident_nt<T>(R, W);
-  const size_t smem = resident_smem_bytes<T>(R, W, nt);
+  const size_t smem = resident_smem_bytes<T>(R, W);
   const size_t static_smem = nt == 512 ? sizeof(IngestSort<512>::Storage) : sizeof(IngestSort<256>::Storage);
   if (smem + static_smem + 1024 > (size_t)optin) return false;
   // local pixel keys of the ingest sort must fit 32 bits
@@ -310,6 +311,7 @@ template <class T> int resident_enqueue(evr_ctx* ctx, int which) {
   a.W = ctx->W;
   a.nb = ctx->r_nb;
   a.R = ctx->r_R;
+  a.wdiv = (unsigned)((((uint64_t)1 << 32) + ctx->W - 1) / ctx->W);
   a.tv_iters = g.denoise_iterations;
   a.pd_iters = g.max_iterations;
   a.manifold = g.manifold_enabled;

@@ -2,11 +2,11 @@
 // packet, the whole of process_packet (pipeline.py:142-171) on chip.
 //
 // Decomposition.  CTA b of a cooperative grid (<= 1 CTA per SM) owns the
-// row band [r0, r1) of the sensor (full width).  Every per-pixel field of
-// the band lives in shared memory together with one halo row above (r0-1)
-// and one below (r1); global memory is touched only to load the state at
-// the start, to exchange two boundary rows per iteration, and to write the
-// state back at the end.
+// row band [r0, r1) of the sensor (full width, equal band heights).  Every
+// per-pixel field of the band lives in shared memory together with one halo
+// row above (r0-1) and one below (r1); global memory is touched only to
+// load the state at the start, to exchange two boundary rows per iteration,
+// and to write the state back at the end.
 //
 // One neighbour exchange per iteration.  Each iteration recomputes on its
 // halo rows what it would otherwise have to wait for a second time
@@ -22,6 +22,10 @@
 // bit-identical to the single-domain reference.  Boundary rows go through
 // a ping-pong buffer in global memory (L2) and a per-CTA release/acquire
 // flag; a CTA waits only for its two neighbours, never for the grid.
+//
+// q = A^T p (solve.py:149-158) is kept in two planes and refreshed right
+// after each pixel's dual update, so the primal's divergence reads its
+// left / upper neighbours' q instead of recomputing them.
 //
 // Ingest is fused: every CTA scans the packet and applies the events of
 // rows [r0-1, r1] with the same ordered, sort-grouped walk as k_ingest
@@ -51,6 +55,7 @@ template <class T> struct ResArgs {
   evr_solve_info* info;
   int* err;
   int H, W, nb, R;
+  unsigned wdiv;                 // ceil(2^32 / W): q / W == __umulhi(q, wdiv)
   int tv_iters, pd_iters, manifold;
   double t_scale, c_pos, c_neg, u_min, u_max;
   T tau, sigma, tl, tv_step, shrink, t_scaleT, uminT, umaxT;
@@ -59,18 +64,19 @@ template <class T> struct ResArgs {
 // plane indices in shared memory
 enum : int {
   RP_U = 0, RP_P1, RP_P2, RP_P3, RP_A11, RP_A12, RP_A22, RP_A31, RP_A32, RP_SG, RP_FB, RP_V,
-  RP_COUNT,
+  RP_QX, RP_QY, RP_COUNT,
   // TV-L1 planes alias the coefficient planes (dead until the metric phase)
-  RP_T0 = RP_A11, RP_TU = RP_A12, RP_TUB = RP_A22, RP_TPX = RP_A31, RP_TPY = RP_A32
+  RP_T0 = RP_A11, RP_TU = RP_A12, RP_TUB = RP_A22, RP_TPX = RP_A31, RP_TPY = RP_A32,
+  // the binary64 copy of f (ingest .. metric) aliases V (and QX for float)
+  RP_F64 = RP_V
 };
 
-template <class T> __host__ __device__ inline size_t resident_smem_bytes(int R, int W, int NT) {
-  const size_t ps = (size_t)(R + 2) * W;
-  size_t b = ps * RP_COUNT * sizeof(T);
-  b = (b + 15) / 16 * 16;
-  b += ps * sizeof(double);  // F64 plane (ingest in binary64)
-  b += 64 * sizeof(double);  // reduction scratch
-  return b;
+__host__ __device__ inline int resident_plane_stride(int R, int W) {
+  return ((R + 2) * W + 3) / 4 * 4;
+}
+
+template <class T> __host__ __device__ inline size_t resident_smem_bytes(int R, int W) {
+  return (size_t)resident_plane_stride(R, W) * RP_COUNT * sizeof(T) + 64 * sizeof(double);
 }
 
 __device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* p) {
@@ -104,7 +110,7 @@ __global__ void __launch_bounds__(NT, 1) k_resident(const ResArgs<T> a) {
   const int r0 = band.start(b);
   const int r1 = r0 + Rb;
   const bool has_up = r0 > 0, has_dn = r1 < H;
-  const size_t PS = (size_t)(a.R + 2) * W;
+  const size_t PS = (size_t)resident_plane_stride(a.R, W);
   T* pl = reinterpret_cast<T*>(smem_raw);
   T* const U = pl + RP_U * PS;
   T* const P1 = pl + RP_P1 * PS;
@@ -118,14 +124,15 @@ __global__ void __launch_bounds__(NT, 1) k_resident(const ResArgs<T> a) {
   T* const SG = pl + RP_SG * PS;
   T* const FB = pl + RP_FB * PS;
   T* const V = pl + RP_V * PS;
+  T* const QX = pl + RP_QX * PS;
+  T* const QY = pl + RP_QY * PS;
   T* const T0 = pl + RP_T0 * PS;
   T* const TU = pl + RP_TU * PS;
   T* const TUB = pl + RP_TUB * PS;
   T* const TPX = pl + RP_TPX * PS;
   T* const TPY = pl + RP_TPY * PS;
-  double* const F64 =
-      reinterpret_cast<double*>(smem_raw + (PS * RP_COUNT * sizeof(T) + 15) / 16 * 16);
-  double* const red = F64 + PS;
+  double* const F64 = reinterpret_cast<double*>(pl + RP_F64 * PS);
+  double* const red = reinterpret_cast<double*>(pl + RP_COUNT * PS);
 
   const PacketHdr* hdr = a.hdr;
   const evr_event* __restrict__ ev = reinterpret_cast<const evr_event*>(hdr + 1);
@@ -133,17 +140,17 @@ __global__ void __launch_bounds__(NT, 1) k_resident(const ResArgs<T> a) {
   const double now = (double)hdr->now;
   const double window = hdr->window;
   const unsigned long long epoch = (unsigned long long)hdr->seq << 24;
-  const size_t xrow = (size_t)3 * W;                      // one side of one CTA
-  const size_t xslot = (size_t)a.nb * 2 * xrow;           // one ping-pong slot
+  const size_t xrow = (size_t)3 * W;             // one side of one CTA
+  const size_t xslot = (size_t)a.nb * 2 * xrow;  // one ping-pong slot
 
   // rows [lo, hi] of the local frame (lr = global row - r0 + 1), flat loop
-#define EVR_FOR_ROWS(lo, hi)                                         \
-  for (int q_ = tid, n_ = ((hi) - (lo) + 1) * W; q_ < n_; q_ += NT) { \
-    const int lr = (lo) + q_ / W;                                     \
-    const int j = q_ - (lr - (lo)) * W;                               \
-    const int gi = r0 - 1 + lr;                                       \
-    const int l = lr * W + j;                                         \
-    const int64_t gk = (int64_t)gi * W + j;
+#define EVR_FOR_ROWS(lo, hi)                                              \
+  for (int q_ = tid, n_ = ((hi) - (lo) + 1) * W; q_ < n_; q_ += NT) {      \
+    const int lr = (lo) + (int)__umulhi((unsigned)q_, a.wdiv);             \
+    const int j = q_ - (lr - (lo)) * W;                                    \
+    const int gi = r0 - 1 + lr;                                            \
+    const int l = lr * W + j;
+#define EVR_GK const int64_t gk = (int64_t)gi * W + j;
 #define EVR_END_ROWS }
 
   const int lo_halo = has_up ? 0 : 1;
@@ -177,25 +184,28 @@ __global__ void __launch_bounds__(NT, 1) k_resident(const ResArgs<T> a) {
       while (ld_acquire_u64(&a.flags[b + 1]) < target) __nanosleep(20);
     __syncthreads();
   };
+  // halo rows <- neighbours' boundary rows; for the dual field also refresh
+  // q = A^T p there (the coefficient planes cover the halo rows)
   auto fetch_halo = [&](int step, T* d0, T* d1, T* d2, int nf) {
     const int slot = step & 1;
     const T* src_up = a.xchg + slot * xslot + (size_t)(b - 1) * 2 * xrow + xrow;  // last row
     const T* src_dn = a.xchg + slot * xslot + (size_t)(b + 1) * 2 * xrow;         // first row
-    for (int j = tid; j < W; j += NT) {
-      if (has_up) {
-        d0[j] = __ldcg(src_up + j);
-        if (nf > 1) {
-          d1[j] = __ldcg(src_up + W + j);
-          d2[j] = __ldcg(src_up + 2 * W + j);
-        }
-      }
-      if (has_dn) {
-        const int l = (Rb + 1) * W + j;
-        d0[l] = __ldcg(src_dn + j);
-        if (nf > 1) {
-          d1[l] = __ldcg(src_dn + W + j);
-          d2[l] = __ldcg(src_dn + 2 * W + j);
-        }
+    for (int k = tid; k < 2 * W; k += NT) {
+      const bool up = k < W;
+      const int j = up ? k : k - W;
+      if (up ? !has_up : !has_dn) continue;
+      const T* src = up ? src_up : src_dn;
+      const int l = up ? j : (Rb + 1) * W + j;
+      const T v0 = __ldcg(src + j);
+      d0[l] = v0;
+      if (nf > 1) {
+        const T v1 = __ldcg(src + W + j), v2 = __ldcg(src + 2 * W + j);
+        d1[l] = v1;
+        d2[l] = v2;
+        T qx, qy;
+        q_of(Coef<T>{A11[l], A12[l], A22[l], A31[l], A32[l]}, v0, v1, v2, qx, qy);
+        QX[l] = qx;
+        QY[l] = qy;
       }
     }
     __syncthreads();
@@ -203,6 +213,7 @@ __global__ void __launch_bounds__(NT, 1) k_resident(const ResArgs<T> a) {
 
   // ---------------------------------------------------------------- load --
   EVR_FOR_ROWS(lo_halo, hi_halo)
+    EVR_GK
     if (a.manifold) {
       const T v = (T)normalize_at((double)a.raw[gk], now, a.t_scale, window);
       T0[l] = v;
@@ -270,6 +281,7 @@ __global__ void __launch_bounds__(NT, 1) k_resident(const ResArgs<T> a) {
     }
     // np.clip(u, 0, t_scale) (surface.py:195) -> global t (own rows)
     EVR_FOR_ROWS(1, Rb)
+      EVR_GK
       a.t[gk] = vclip(TU[l], T(0), a.t_scaleT);
     EVR_END_ROWS
   }
@@ -292,8 +304,10 @@ __global__ void __launch_bounds__(NT, 1) k_resident(const ResArgs<T> a) {
   step = s_met;
 
   // ------------------------------------------------------------ metric ---
-  // compute_metric + coeffs (surface.py:81-90, :199-205), solver constants
+  // compute_metric + coeffs (surface.py:81-90, :199-205), solver constants,
+  // warm start u, p from the state
   EVR_FOR_ROWS(lo_halo, hi_halo)
+    EVR_GK
     T gx = T(0), gy = T(0);
     if (a.manifold) {
       const T tc = __ldcg(a.t + gk);
@@ -321,6 +335,13 @@ __global__ void __launch_bounds__(NT, 1) k_resident(const ResArgs<T> a) {
     P2[l] = a.p2[gk];
     P3[l] = a.p3[gk];
   EVR_END_ROWS
+  __syncthreads();  // F64 (aliasing V / QX) is dead from here on
+  EVR_FOR_ROWS(lo_halo, hi_halo)
+    T qx, qy;
+    q_of(Coef<T>{A11[l], A12[l], A22[l], A31[l], A32[l]}, P1[l], P2[l], P3[l], qx, qy);
+    QX[l] = qx;
+    QY[l] = qy;
+  EVR_END_ROWS
   __syncthreads();
 
   // ------------------------------------------------------- primal-dual ---
@@ -333,15 +354,8 @@ __global__ void __launch_bounds__(NT, 1) k_resident(const ResArgs<T> a) {
       fetch_halo(step, P1, P2, P3, 3);
     }
     EVR_FOR_ROWS(1, hi_halo)  // primal + over-relaxation, own rows + halo below
-      T qx, qy, qxl = T(0), qyu = T(0), dm;
-      q_of(Coef<T>{A11[l], A12[l], A22[l], A31[l], A32[l]}, P1[l], P2[l], P3[l], qx, qy);
-      if (j > 0)
-        q_of(Coef<T>{A11[l - 1], A12[l - 1], A22[l - 1], A31[l - 1], A32[l - 1]}, P1[l - 1],
-             P2[l - 1], P3[l - 1], qxl, dm);
-      if (gi > 0)
-        q_of(Coef<T>{A11[l - W], A12[l - W], A22[l - W], A31[l - W], A32[l - W]}, P1[l - W],
-             P2[l - W], P3[l - W], dm, qyu);
-      const T d = div_at(qx, qxl, qy, qyu, gi, j, H, W);
+      const T d = div_at(QX[l], j > 0 ? QX[l - 1] : T(0), QY[l], gi > 0 ? QY[l - W] : T(0), gi,
+                         j, H, W);
       const T uk = U[l];
       const T nu = kl_primal(d, uk, a.tl * SG[l], FB[l], a.tau, a.uminT, a.umaxT);
       V[l] = nu * T(2) - uk;
@@ -353,15 +367,19 @@ __global__ void __launch_bounds__(NT, 1) k_resident(const ResArgs<T> a) {
       }
     EVR_END_ROWS
     __syncthreads();
-    EVR_FOR_ROWS(1, Rb)  // dual ascent + ball projection, own rows
+    EVR_FOR_ROWS(1, Rb)  // dual ascent + ball projection, own rows; refresh q
       const T gx = j < W - 1 ? V[l + 1] - V[l] : T(0);
       const T gy = gi < H - 1 ? V[l + W] - V[l] : T(0);
+      const Coef<T> c{A11[l], A12[l], A22[l], A31[l], A32[l]};
       T q1 = P1[l], q2 = P2[l], q3 = P3[l];
-      dual_step(Coef<T>{A11[l], A12[l], A22[l], A31[l], A32[l]}, a.sigma, gx, gy, SG[l], q1, q2,
-                q3);
+      dual_step(c, a.sigma, gx, gy, SG[l], q1, q2, q3);
       P1[l] = q1;
       P2[l] = q2;
       P3[l] = q3;
+      T qx, qy;
+      q_of(c, q1, q2, q3, qx, qy);
+      QX[l] = qx;
+      QY[l] = qy;
     EVR_END_ROWS
     __syncthreads();
     if (!last) publish(++step, P1, P2, P3, 3);
@@ -375,6 +393,7 @@ __global__ void __launch_bounds__(NT, 1) k_resident(const ResArgs<T> a) {
   // ---------------------------------------------------------- epilogue ---
   // state.u = u+, state.p, state.f = copy(u+) (pipeline.py:167-170)
   EVR_FOR_ROWS(1, Rb)
+    EVR_GK
     const T v = U[l];
     a.u[gk] = v;
     a.f[gk] = (double)v;
@@ -383,6 +402,7 @@ __global__ void __launch_bounds__(NT, 1) k_resident(const ResArgs<T> a) {
     a.p3[gk] = P3[l];
   EVR_END_ROWS
 #undef EVR_FOR_ROWS
+#undef EVR_GK
 #undef EVR_END_ROWS
 
   // rel_change = |u+ - u| / max(|u|, 1e-30) (solve.py:246-249): fixed-order
