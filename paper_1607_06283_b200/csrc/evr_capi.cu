@@ -274,7 +274,9 @@ template <class T> int resident_alloc(evr_ctx* ctx) {
   ctx->d_ticket = nullptr;
   CK(cudaMalloc(&ctx->d_flags, sizeof(unsigned long long) * ctx->r_nb));
   CK(cudaMemset(ctx->d_flags, 0, sizeof(unsigned long long) * ctx->r_nb));
-  CK(cudaMalloc(&ctx->d_xchg, sizeof(T) * 2 * ctx->r_nb * 2 * 3 * (size_t)ctx->W));
+  const size_t xbytes = sizeof(unsigned long long) * LLWords<T>::N * 2 * ctx->r_nb * 2 * 3 * (size_t)ctx->W;
+  CK(cudaMalloc(&ctx->d_xchg, xbytes));
+  CK(cudaMemset(ctx->d_xchg, 0, xbytes));  // no stale tag can match a live one
   CK(cudaMalloc(&ctx->d_ticket, sizeof(unsigned)));
   CK(cudaMemset(ctx->d_ticket, 0, sizeof(unsigned)));
   auto set_attr = [&](const void* fn) -> cudaError_t {

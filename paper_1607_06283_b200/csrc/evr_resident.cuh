@@ -89,6 +89,42 @@ __device__ __forceinline__ void st_release_u64(unsigned long long* p, unsigned l
   asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
+__device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void st_relaxed_u64(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// Low-latency boundary-row exchange: every 64-bit word carries 32 payload
+// bits and a 32-bit tag naming the (packet, step) that wrote it.  A 64-bit
+// store is single-copy atomic, so a reader that sees the expected tag also
+// sees the payload -- no fence, no separate flag, one L2 round trip.
+template <class T> struct LLWords;
+template <> struct LLWords<float> {
+  static constexpr int N = 1;
+  __device__ static void pack(float v, unsigned tag, unsigned long long* w) {
+    w[0] = ((unsigned long long)tag << 32) | __float_as_uint(v);
+  }
+  __device__ static float unpack(const unsigned long long* w) {
+    return __uint_as_float((unsigned)w[0]);
+  }
+};
+template <> struct LLWords<double> {
+  static constexpr int N = 2;
+  __device__ static void pack(double v, unsigned tag, unsigned long long* w) {
+    const unsigned long long bits = (unsigned long long)__double_as_longlong(v);
+    w[0] = ((unsigned long long)tag << 32) | (bits & 0xffffffffull);
+    w[1] = ((unsigned long long)tag << 32) | (bits >> 32);
+  }
+  __device__ static double unpack(const unsigned long long* w) {
+    return __longlong_as_double((long long)((w[1] << 32) | (w[0] & 0xffffffffull)));
+  }
+};
+
 struct Band {
   int base, extra;
   __device__ __forceinline__ int rows(int b) const { return base + (b < extra ? 1 : 0); }
@@ -140,8 +176,11 @@ __global__ void __launch_bounds__(NT, 1) k_resident(const ResArgs<T> a) {
   const double now = (double)hdr->now;
   const double window = hdr->window;
   const unsigned long long epoch = (unsigned long long)hdr->seq << 24;
-  const size_t xrow = (size_t)3 * W;             // one side of one CTA
-  const size_t xslot = (size_t)a.nb * 2 * xrow;  // one ping-pong slot
+  const unsigned tag_base = (unsigned)hdr->seq << 16;
+  constexpr int NWD = LLWords<T>::N;
+  const size_t xside = (size_t)3 * W * NWD;       // words of one side of one CTA
+  const size_t xslot = (size_t)a.nb * 2 * xside;  // words of one ping-pong slot
+  unsigned long long* const xw = reinterpret_cast<unsigned long long*>(a.xchg);
 
   // rows [lo, hi] of the local frame (lr = global row - r0 + 1), flat loop
 #define EVR_FOR_ROWS(lo, hi)                                              \
@@ -156,50 +195,51 @@ __global__ void __launch_bounds__(NT, 1) k_resident(const ResArgs<T> a) {
   const int lo_halo = has_up ? 0 : 1;
   const int hi_halo = has_dn ? Rb + 1 : Rb;
 
-  auto publish = [&](int step, const T* s0, const T* s1, const T* s2, int nf) {
-    const int slot = step & 1;
-    T* dst = a.xchg + slot * xslot + (size_t)b * 2 * xrow;
-    for (int j = tid; j < W; j += NT) {
-      const int lf = 1 * W + j, ll = Rb * W + j;
-      dst[j] = s0[lf];
-      dst[xrow + j] = s0[ll];
-      if (nf > 1) {
-        dst[W + j] = s1[lf];
-        dst[xrow + W + j] = s1[ll];
-        dst[2 * W + j] = s2[lf];
-        dst[xrow + 2 * W + j] = s2[ll];
-      }
+  // boundary-row publish: the thread that produced (lr, j) of the first /
+  // last own row stores it as tagged words for the CTA above / below
+  auto ll_put = [&](int step, int lr, int j, int field, T v) {
+    unsigned long long w[NWD];
+    LLWords<T>::pack(v, tag_base + (unsigned)step, w);
+    unsigned long long* base = xw + (step & 1) * xslot + (size_t)b * 2 * xside;
+    if (lr == 1) {
+      unsigned long long* d = base + ((size_t)field * W + j) * NWD;
+#pragma unroll
+      for (int k = 0; k < NWD; ++k) st_relaxed_u64(d + k, w[k]);
     }
-    __syncthreads();
-    if (tid == 0) {
-      __threadfence();
-      st_release_u64(&a.flags[b], epoch | (unsigned long long)step);
+    if (lr == Rb) {
+      unsigned long long* d = base + xside + ((size_t)field * W + j) * NWD;
+#pragma unroll
+      for (int k = 0; k < NWD; ++k) st_relaxed_u64(d + k, w[k]);
     }
   };
-  auto wait_neighbours = [&](int step) {
-    const unsigned long long target = epoch | (unsigned long long)step;
-    if (tid == 0 && has_up)
-      while (ld_acquire_u64(&a.flags[b - 1]) < target) __nanosleep(20);
-    if (tid == 32 && has_dn)
-      while (ld_acquire_u64(&a.flags[b + 1]) < target) __nanosleep(20);
-    __syncthreads();
-  };
-  // halo rows <- neighbours' boundary rows; for the dual field also refresh
-  // q = A^T p there (the coefficient planes cover the halo rows)
-  auto fetch_halo = [&](int step, T* d0, T* d1, T* d2, int nf) {
-    const int slot = step & 1;
-    const T* src_up = a.xchg + slot * xslot + (size_t)(b - 1) * 2 * xrow + xrow;  // last row
-    const T* src_dn = a.xchg + slot * xslot + (size_t)(b + 1) * 2 * xrow;         // first row
+  // halo rows <- neighbours' boundary rows of `step`, polling the tags; for
+  // the dual field also refresh q = A^T p there (coefficients cover halos)
+  auto ll_fetch = [&](int step, T* d0, T* d1, T* d2, int nf) {
+    const unsigned want = tag_base + (unsigned)step;
+    const unsigned long long* slot = xw + (step & 1) * xslot;
     for (int k = tid; k < 2 * W; k += NT) {
       const bool up = k < W;
       const int j = up ? k : k - W;
       if (up ? !has_up : !has_dn) continue;
-      const T* src = up ? src_up : src_dn;
+      // the CTA above sent its last row (side 1), the one below its first
+      const unsigned long long* src =
+          slot + (size_t)(up ? b - 1 : b + 1) * 2 * xside + (up ? xside : 0) + (size_t)j * NWD;
+      unsigned long long w[3][NWD];
+      bool ready;
+      do {
+        ready = true;
+        for (int f = 0; f < nf; ++f)
+#pragma unroll
+          for (int q = 0; q < NWD; ++q) {
+            w[f][q] = ld_relaxed_u64(src + (size_t)f * W * NWD + q);
+            ready &= (unsigned)(w[f][q] >> 32) == want;
+          }
+      } while (!ready);
       const int l = up ? j : (Rb + 1) * W + j;
-      const T v0 = __ldcg(src + j);
+      const T v0 = LLWords<T>::unpack(w[0]);
       d0[l] = v0;
       if (nf > 1) {
-        const T v1 = __ldcg(src + W + j), v2 = __ldcg(src + 2 * W + j);
+        const T v1 = LLWords<T>::unpack(w[1]), v2 = LLWords<T>::unpack(w[2]);
         d1[l] = v1;
         d2[l] = v2;
         T qx, qy;
@@ -208,6 +248,21 @@ __global__ void __launch_bounds__(NT, 1) k_resident(const ResArgs<T> a) {
         QY[l] = qy;
       }
     }
+    __syncthreads();
+  };
+  // whole-CTA progress flag (used once per packet, not per iteration)
+  auto flag_publish = [&](int step) {
+    __syncthreads();
+    if (tid == 0) {
+      __threadfence();
+      st_release_u64(&a.flags[b], epoch | (unsigned long long)step);
+    }
+  };
+  auto flag_wait = [&](int b_lo, int b_hi, int step) {
+    const unsigned long long target = epoch | (unsigned long long)step;
+    const int nwait = b_hi - b_lo + 1;
+    if (tid < nwait && b_lo + tid != b)
+      while (ld_acquire_u64(&a.flags[b_lo + tid]) < target) __nanosleep(20);
     __syncthreads();
   };
 
@@ -255,10 +310,8 @@ __global__ void __launch_bounds__(NT, 1) k_resident(const ResArgs<T> a) {
   int step = 0;
   if (a.manifold) {
     for (int it = 0; it < a.tv_iters; ++it) {
-      if (it > 0) {
-        wait_neighbours(step);
-        fetch_halo(step, TUB, nullptr, nullptr, 1);
-      }
+      const bool pub = it < a.tv_iters - 1;
+      if (it > 0) ll_fetch(step, TUB, nullptr, nullptr, 1);  // u_bar of step `it`
       EVR_FOR_ROWS(lo_halo, Rb)  // dual, own rows + halo row above
         const T dx = j < W - 1 ? TUB[l + 1] - TUB[l] : T(0);
         const T dy = gi < H - 1 ? TUB[l + W] - TUB[l] : T(0);
@@ -268,17 +321,20 @@ __global__ void __launch_bounds__(NT, 1) k_resident(const ResArgs<T> a) {
         TPY[l] = py;
       EVR_END_ROWS
       __syncthreads();
-      EVR_FOR_ROWS(1, Rb)  // primal, own rows
+      EVR_FOR_ROWS(1, Rb)  // primal, own rows; boundary rows go out at once
         const T d = div_at(TPX[l], j > 0 ? TPX[l - 1] : T(0), TPY[l], gi > 0 ? TPY[l - W] : T(0),
                            gi, j, H, W);
         T ub;
         const T un = tv_primal_step(d, TU[l], T0[l], a.tv_step, a.shrink, ub);
         TU[l] = un;
         TUB[l] = ub;
+        if (pub) ll_put(step + 1, lr, j, 0, ub);
       EVR_END_ROWS
-      __syncthreads();
-      if (it < a.tv_iters - 1) publish(++step, TUB, nullptr, nullptr, 1);
+      // no barrier: the next fetch only writes halo rows of u_bar, which
+      // this primal does not read
+      if (pub) ++step;
     }
+    __syncthreads();
     // np.clip(u, 0, t_scale) (surface.py:195) -> global t (own rows)
     EVR_FOR_ROWS(1, Rb)
       EVR_GK
@@ -288,19 +344,11 @@ __global__ void __launch_bounds__(NT, 1) k_resident(const ResArgs<T> a) {
   // all rows of the denoised surface this band's metric reads are final
   __syncthreads();
   const int s_met = a.tv_iters + 1;
-  if (tid == 0) {
-    __threadfence();
-    st_release_u64(&a.flags[b], epoch | (unsigned long long)s_met);
-  }
-  if (a.manifold) {
-    const int b_lo = band.of_row(has_up ? r0 - 1 : r0);
-    const int b_hi = band.of_row(r1 + 1 < H ? r1 + 1 : H - 1);
-    const int nwait = b_hi - b_lo + 1;
-    if (tid < nwait && b_lo + tid != b)
-      while (ld_acquire_u64(&a.flags[b_lo + tid]) < (epoch | (unsigned long long)s_met))
-        __nanosleep(20);
-  }
-  __syncthreads();
+  flag_publish(s_met);
+  if (a.manifold)
+    flag_wait(band.of_row(has_up ? r0 - 1 : r0), band.of_row(r1 + 1 < H ? r1 + 1 : H - 1), s_met);
+  else
+    __syncthreads();
   step = s_met;
 
   // ------------------------------------------------------------ metric ---
@@ -349,10 +397,7 @@ __global__ void __launch_bounds__(NT, 1) k_resident(const ResArgs<T> a) {
   double rd = 0.0, ro = 0.0;
   for (int it = 0; it < a.pd_iters; ++it) {
     const bool last = it == a.pd_iters - 1;
-    if (it > 0) {
-      wait_neighbours(step);
-      fetch_halo(step, P1, P2, P3, 3);
-    }
+    if (it > 0) ll_fetch(step, P1, P2, P3, 3);  // p of the previous step (+ q)
     EVR_FOR_ROWS(1, hi_halo)  // primal + over-relaxation, own rows + halo below
       const T d = div_at(QX[l], j > 0 ? QX[l - 1] : T(0), QY[l], gi > 0 ? QY[l - W] : T(0), gi,
                          j, H, W);
@@ -380,15 +425,22 @@ __global__ void __launch_bounds__(NT, 1) k_resident(const ResArgs<T> a) {
       q_of(c, q1, q2, q3, qx, qy);
       QX[l] = qx;
       QY[l] = qy;
+      if (!last) {
+        ll_put(step + 1, lr, j, 0, q1);
+        ll_put(step + 1, lr, j, 1, q2);
+        ll_put(step + 1, lr, j, 2, q3);
+      }
     EVR_END_ROWS
-    __syncthreads();
-    if (!last) publish(++step, P1, P2, P3, 3);
+    // no barrier: the next fetch only writes halo rows of p / q, which this
+    // dual step does not read
+    if (!last) ++step;
   }
   if (a.pd_iters < 2) {
     // neighbours may still be loading our rows of u / p as halos
-    publish(++step, P1, P2, P3, 3);
-    wait_neighbours(step);
+    flag_publish(s_met + 1);
+    flag_wait(has_up ? b - 1 : b, has_dn ? b + 1 : b, s_met + 1);
   }
+  __syncthreads();
 
   // ---------------------------------------------------------- epilogue ---
   // state.u = u+, state.p, state.f = copy(u+) (pipeline.py:167-170)
