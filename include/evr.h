@@ -154,6 +154,11 @@ void *evr_stream(evr_ctx *ctx);
 /* Count of kernel launches this context issued (graph nodes included). */
 int64_t evr_launch_count(const evr_ctx *ctx);
 
+/* Diagnostics: enable (1) / disable (0) / keep (-1) the resident engine's
+ * phase timeline (globaltimer ns per phase mark, 256 slots per CTA) and
+ * copy up to n words of it to out (may be NULL). */
+int evr_debug_timeline(evr_ctx *ctx, int enable, uint64_t *out, int64_t n);
+
 /* ---- operator-level API on host arrays of the context's shape ----------- */
 /* grad_x / grad_y (surface.py:93-104) */
 int evr_op_grad(evr_ctx *ctx, const double *u, double *gx, double *gy);

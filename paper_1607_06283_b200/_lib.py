@@ -95,6 +95,7 @@ _SIGNATURES = {
     "evr_get_metric": ([_P, _P, _P, _P, _P], _i32),
     "evr_get_frame_u8": ([_P, _d, _d, _P], _i32),
     "evr_event_buffer": ([_P, _i64, _P], _i32),
+    "evr_debug_timeline": ([_P, _i32, _P, _i64], _i32),
     "evr_stream": ([_P], _P),
     "evr_launch_count": ([_P], _i64),
     "evr_op_grad": ([_P, _P, _P, _P], _i32),

@@ -74,6 +74,7 @@ struct evr_ctx {
   unsigned long long* d_flags = nullptr;  // per-CTA progress words
   void* d_xchg = nullptr;                 // boundary-row ping-pong buffer
   unsigned* d_ticket = nullptr;
+  unsigned long long* d_trace = nullptr;  // optional resident phase timeline
   std::string err;
 
   template <class T> T* fld(int k) const { return reinterpret_cast<T*>(slab + field_stride * k); }
@@ -309,6 +310,7 @@ template <class T> int resident_enqueue(evr_ctx* ctx, int which) {
   a.ticket = ctx->d_ticket;
   a.info = ctx->d_info;
   a.err = ctx->d_err;
+  a.trace = ctx->d_trace;
   a.H = ctx->H;
   a.W = ctx->W;
   a.nb = ctx->r_nb;
@@ -700,6 +702,7 @@ void evr_destroy(evr_ctx* ctx) {
   cudaFree(ctx->d_flags);
   cudaFree(ctx->d_xchg);
   cudaFree(ctx->d_ticket);
+  cudaFree(ctx->d_trace);
   for (int i = 0; i < 2; ++i) {
     if (ctx->h_stage[i]) cudaFreeHost(ctx->h_stage[i]);
     if (ctx->stage_done[i]) cudaEventDestroy(ctx->stage_done[i]);
@@ -924,6 +927,26 @@ int evr_event_buffer(evr_ctx* ctx, int64_t n, evr_event** dev_ptr) {
   int rc = ensure_stage(ctx, n);
   if (rc) return rc;
   *dev_ptr = reinterpret_cast<evr_event*>(ctx->d_stage + sizeof(PacketHdr));
+  return EVR_OK;
+}
+
+int evr_debug_timeline(evr_ctx* ctx, int enable, uint64_t* out, int64_t n) {
+  CHECK_CTX();
+  if (enable >= 0) {
+    if (enable && !ctx->d_trace) {
+      CK(cudaMalloc(&ctx->d_trace, sizeof(unsigned long long) * 256 * std::max(ctx->r_nb, 1)));
+      CK(cudaMemset(ctx->d_trace, 0, sizeof(unsigned long long) * 256 * std::max(ctx->r_nb, 1)));
+    } else if (!enable && ctx->d_trace) {
+      CK(cudaStreamSynchronize(ctx->stream));
+      cudaFree(ctx->d_trace);
+      ctx->d_trace = nullptr;
+    }
+    drop_graphs(ctx);
+  }
+  if (out && ctx->d_trace) {
+    const int64_t m = std::min<int64_t>(n, 256 * (int64_t)std::max(ctx->r_nb, 1));
+    return d2h_sync(ctx, out, ctx->d_trace, sizeof(uint64_t) * m);
+  }
   return EVR_OK;
 }
 

@@ -54,6 +54,7 @@ template <class T> struct ResArgs {
   unsigned* ticket;              // last-CTA election for the final sum
   evr_solve_info* info;
   int* err;
+  unsigned long long* trace;     // optional [nb][256] phase timestamps (ns)
   int H, W, nb, R;
   unsigned wdiv;                 // ceil(2^32 / W): q / W == __umulhi(q, wdiv)
   int tv_iters, pd_iters, manifold;
@@ -192,6 +193,18 @@ __global__ void __launch_bounds__(NT, 1) k_resident(const ResArgs<T> a) {
 #define EVR_GK const int64_t gk = (int64_t)gi * W + j;
 #define EVR_END_ROWS }
 
+  // optional phase timeline (diagnostics): globaltimer at phase marks
+  int tmark = 0;
+  auto mark = [&]() {
+    if (a.trace && tid == 0 && tmark < 256) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      a.trace[(size_t)b * 256 + tmark] = t;
+    }
+    ++tmark;
+  };
+  mark();
+
   const int lo_halo = has_up ? 0 : 1;
   const int hi_halo = has_dn ? Rb + 1 : Rb;
 
@@ -305,6 +318,7 @@ __global__ void __launch_bounds__(NT, 1) k_resident(const ResArgs<T> a) {
         });
   }
 
+  mark();  // 1: loaded + ingested
   // ------------------------------------------------------------ TV-L1 ----
   // denoise_timestamps (surface.py:146-196), one exchange per iteration
   int step = 0;
@@ -312,6 +326,7 @@ __global__ void __launch_bounds__(NT, 1) k_resident(const ResArgs<T> a) {
     for (int it = 0; it < a.tv_iters; ++it) {
       const bool pub = it < a.tv_iters - 1;
       if (it > 0) ll_fetch(step, TUB, nullptr, nullptr, 1);  // u_bar of step `it`
+      mark();
       EVR_FOR_ROWS(lo_halo, Rb)  // dual, own rows + halo row above
         const T dx = j < W - 1 ? TUB[l + 1] - TUB[l] : T(0);
         const T dy = gi < H - 1 ? TUB[l + W] - TUB[l] : T(0);
@@ -351,6 +366,7 @@ __global__ void __launch_bounds__(NT, 1) k_resident(const ResArgs<T> a) {
     __syncthreads();
   step = s_met;
 
+  mark();
   // ------------------------------------------------------------ metric ---
   // compute_metric + coeffs (surface.py:81-90, :199-205), solver constants,
   // warm start u, p from the state
@@ -394,10 +410,12 @@ __global__ void __launch_bounds__(NT, 1) k_resident(const ResArgs<T> a) {
 
   // ------------------------------------------------------- primal-dual ---
   // primal_dual_solve (solve.py:207-261), warm start from the state
+  mark();
   double rd = 0.0, ro = 0.0;
   for (int it = 0; it < a.pd_iters; ++it) {
     const bool last = it == a.pd_iters - 1;
     if (it > 0) ll_fetch(step, P1, P2, P3, 3);  // p of the previous step (+ q)
+    mark();
     EVR_FOR_ROWS(1, hi_halo)  // primal + over-relaxation, own rows + halo below
       const T d = div_at(QX[l], j > 0 ? QX[l - 1] : T(0), QY[l], gi > 0 ? QY[l - W] : T(0), gi,
                          j, H, W);
@@ -442,6 +460,7 @@ __global__ void __launch_bounds__(NT, 1) k_resident(const ResArgs<T> a) {
   }
   __syncthreads();
 
+  mark();
   // ---------------------------------------------------------- epilogue ---
   // state.u = u+, state.p, state.f = copy(u+) (pipeline.py:167-170)
   EVR_FOR_ROWS(1, Rb)
