@@ -255,10 +255,8 @@ template <class T> bool resident_plan(evr_ctx* ctx) {
   const int nb = (H + R - 1) / R;
   const int nt = resident_nt<T>(R, W);
   const size_t smem = resident_smem_bytes<T>(R, W);
-  const size_t static_smem = nt == 512 ? sizeof(IngestSort<512>::Storage) : sizeof(IngestSort<256>::Storage);
+  const size_t static_smem = nt == 512 ? sizeof(IngestShared<512>) : sizeof(IngestShared<256>);
   if (smem + static_smem + 1024 > (size_t)optin) return false;
-  // local pixel keys of the ingest sort must fit 32 bits
-  if ((uint64_t)(R + 2) * W >= (1ull << (32 - IngestSort<512>::LOG_NT)) - 1) return false;
   ctx->r_nb = nb;
   ctx->r_R = R;
   ctx->r_nt = nt;

@@ -6,37 +6,30 @@
 // clamp after every step and the last timestamp wins.  Multiply-then-clamp
 // does not commute, hence the device must preserve the per-pixel order.
 //
-// A CTA takes the packet in chunks of NT events.  Events of the rows it is
-// responsible for get the 32-bit key (local pixel << log2(NT)) | lane, one
-// cub block radix sort groups them by pixel with the stream order kept
-// inside each group, and the first lane of every group walks its group
-// applying the events in order.  Cost per chunk is one sort of NT keys plus
-// the longest duplicate run, independent of how the events cluster; chunks
-// are ordered by CTA barriers.
+// A CTA owns a range of rows and takes the packet in chunks of NT events:
+//   1. every thread tests one event; the events of the CTA's rows are
+//      compacted, in stream order, into a shared list (warp ballots + a
+//      prefix over the per-warp counts);
+//   2. warp 0 walks the list 32 entries at a time: __match_any_sync groups
+//      equal pixels, the lowest lane of each group applies the group's
+//      events in lane (= stream) order, and consecutive 32-entry windows run
+//      in program order, so a pixel's duplicates compound exactly as in the
+//      sequential reference.
+// A row band sees a small share of the packet, so the walk is a handful of
+// warp steps; a band that receives the whole packet costs n/32 of them.
 #pragma once
 
-#include <cub/block/block_radix_sort.cuh>
 #include <cstdint>
 
 #include "../../include/evr.h"
 
 namespace evr {
 
-template <int NT> struct IngestSort {
-  static constexpr int LOG_NT = NT == 1024 ? 10 : NT == 512 ? 9 : NT == 256 ? 8 : 7;
-  static_assert((1 << LOG_NT) == NT, "NT must be 128, 256, 512 or 1024");
-  using Sort = cub::BlockRadixSort<uint32_t, NT, 1>;
-  struct Storage {
-    typename Sort::TempStorage sort;
-    uint32_t keys[NT];
-  };
+template <int NT> struct IngestShared {
+  int pix[NT];    // local pixel of each kept event
+  int idx[NT];    // its index inside the chunk
+  int wcount[NT / 32];
 };
-
-__host__ __device__ inline int bits_for(uint32_t v) {
-  int b = 0;
-  while ((1u << b) < v && b < 32) ++b;
-  return b;
-}
 
 // Apply the packet's events of global rows [row_lo, row_hi] in stream order.
 //   load(lp) -> double   current f at local pixel lp = (row - row_lo) * W + x
@@ -46,43 +39,61 @@ template <int NT, class Load, class Store>
 __device__ __forceinline__ void ordered_ingest(const evr_event* __restrict__ ev, int64_t n, int H,
                                                int W, int row_lo, int row_hi, double c_pos,
                                                double c_neg, double u_min, double u_max,
-                                               typename IngestSort<NT>::Storage& sm, int* err,
-                                               Load load, Store store) {
-  using S = IngestSort<NT>;
-  constexpr uint32_t NONE = 0xffffffffu;
-  const int tid = threadIdx.x;
-  const uint32_t npix = (uint32_t)(row_hi - row_lo + 1) * (uint32_t)W;
-  const int end_bit = S::LOG_NT + bits_for(npix + 1);
+                                               IngestShared<NT>& sm, int* err, Load load,
+                                               Store store) {
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   for (int64_t base = 0; base < n; base += NT) {
-    uint32_t key[1] = {NONE};
+    bool keep = false;
+    int lp = 0;
     if (base + tid < n) {
       const evr_event e = ev[base + tid];
       if (e.x >= 0 && e.x < W && e.y >= 0 && e.y < H) {
-        if (e.y >= row_lo && e.y <= row_hi)
-          key[0] = ((uint32_t)((e.y - row_lo) * W + e.x) << S::LOG_NT) | (uint32_t)tid;
+        if (e.y >= row_lo && e.y <= row_hi) {
+          keep = true;
+          lp = (e.y - row_lo) * W + e.x;
+        }
       } else if (err) {
         atomicOr(err, 1);
       }
     }
-    typename S::Sort(sm.sort).Sort(key, 0, end_bit < 32 ? end_bit : 32);
-    sm.keys[tid] = key[0];
+    const unsigned ball = __ballot_sync(0xffffffffu, keep);
+    if (lane == 0) sm.wcount[wid] = __popc(ball);
     __syncthreads();
-    const uint32_t k = key[0];
-    if (k != NONE && (end_bit >= 32 || k < (1u << end_bit))) {
-      const uint32_t lp = k >> S::LOG_NT;
-      if (tid == 0 || (sm.keys[tid - 1] >> S::LOG_NT) != lp) {
-        double v = load((int)lp);
-        int64_t last_t = 0;
-        for (int s = tid; s < NT; ++s) {
-          const uint32_t ks = sm.keys[s];
-          if (ks == NONE || (ks >> S::LOG_NT) != lp) break;
-          const evr_event e = ev[base + (ks & (NT - 1))];
-          v = v * (e.polarity > 0 ? c_pos : c_neg);
-          if (u_min > v) v = u_min;  // Python max(value, u_min)
-          if (u_max < v) v = u_max;  // Python min(.., u_max)
-          last_t = e.t;
+    int off = 0, m = 0;
+#pragma unroll
+    for (int w = 0; w < NT / 32; ++w) {
+      const int c = sm.wcount[w];
+      off += w < wid ? c : 0;
+      m += c;
+    }
+    if (keep) {
+      const int pos = off + __popc(ball & ((1u << lane) - 1u));
+      sm.pix[pos] = lp;
+      sm.idx[pos] = tid;
+    }
+    __syncthreads();
+    if (wid == 0) {
+      for (int s = 0; s < m; s += 32) {
+        const int k = s + lane;
+        const bool act = k < m;
+        const unsigned live = __ballot_sync(0xffffffffu, act);
+        if (act) {
+          const int pix = sm.pix[k];
+          const unsigned grp = __match_any_sync(live, pix);
+          if (lane == __ffs(grp) - 1) {
+            double v = load(pix);
+            int64_t last_t = 0;
+            for (unsigned g = grp; g; g &= g - 1) {
+              const evr_event e = ev[base + sm.idx[s + __ffs(g) - 1]];
+              v = v * (e.polarity > 0 ? c_pos : c_neg);
+              if (u_min > v) v = u_min;  // Python max(value, u_min)
+              if (u_max < v) v = u_max;  // Python min(.., u_max)
+              last_t = e.t;
+            }
+            store(pix, v, last_t);
+          }
         }
-        store((int)lp, v, last_t);
+        __syncwarp();
       }
     }
     __syncthreads();

@@ -49,7 +49,7 @@ __global__ void __launch_bounds__(NT)
 k_ingest(const PacketHdr* __restrict__ hdr, double* __restrict__ f, int64_t* __restrict__ raw,
          int H, int W, int rows_per, double c_pos, double c_neg, double u_min, double u_max,
          int* err) {
-  __shared__ typename IngestSort<NT>::Storage sm;
+  __shared__ IngestShared<NT> sm;
   // the packet's events follow the header in the staging buffer
   const evr_event* __restrict__ ev = reinterpret_cast<const evr_event*>(hdr + 1);
   const int row_lo = blockIdx.x * rows_per;

@@ -126,6 +126,13 @@ template <> struct LLWords<double> {
   }
 };
 
+// one element global -> shared, asynchronous (LDGSTS)
+template <class T> __device__ __forceinline__ void cp_async_elem(T* dst, const T* src) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], %2;" ::"r"(d), "l"(src), "n"(sizeof(T))
+               : "memory");
+}
+
 struct Band {
   int base, extra;
   __device__ __forceinline__ int rows(int b) const { return base + (b < extra ? 1 : 0); }
@@ -280,25 +287,61 @@ __global__ void __launch_bounds__(NT, 1) k_resident(const ResArgs<T> a) {
   };
 
   // ---------------------------------------------------------------- load --
+  // warm-start u, p: asynchronous copies straight into their (idle until
+  // the solve) planes, in flight during ingest and TV-L1
   EVR_FOR_ROWS(lo_halo, hi_halo)
     EVR_GK
-    if (a.manifold) {
-      const T v = (T)normalize_at((double)a.raw[gk], now, a.t_scale, window);
-      T0[l] = v;
-      TU[l] = v;
-      TUB[l] = v;
-      TPX[l] = T(0);
-      TPY[l] = T(0);
-    }
-    if (lr >= 1) F64[l] = a.f[gk];
+    if (lr >= 1) cp_async_elem(U + l, a.u + gk);
+    cp_async_elem(P1 + l, a.p1 + gk);
+    cp_async_elem(P2 + l, a.p2 + gk);
+    cp_async_elem(P3 + l, a.p3 + gk);
   EVR_END_ROWS
+  asm volatile("cp.async.commit_group;" ::: "memory");
+  // raw timestamps -> surface heights, f -> binary64 plane; loads batched
+  // KB deep per thread so their latencies overlap
+  {
+    constexpr int KB = 4;
+    const int n_ = (hi_halo - lo_halo + 1) * W;
+    for (int q0 = tid; q0 < n_; q0 += NT * KB) {
+      int64_t rv[KB];
+      double fv[KB];
+#pragma unroll
+      for (int k = 0; k < KB; ++k) {
+        const int q = q0 + k * NT;
+        if (q < n_) {
+          const int lr = lo_halo + (int)__umulhi((unsigned)q, a.wdiv);
+          const int j = q - (lr - lo_halo) * W;
+          const int64_t gk = (int64_t)(r0 - 1 + lr) * W + j;
+          rv[k] = a.manifold ? a.raw[gk] : 0;
+          fv[k] = lr >= 1 ? a.f[gk] : 0.0;
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < KB; ++k) {
+        const int q = q0 + k * NT;
+        if (q < n_) {
+          const int lr = lo_halo + (int)__umulhi((unsigned)q, a.wdiv);
+          const int l = lr * W + (q - (lr - lo_halo) * W);
+          if (a.manifold) {
+            const T v = (T)normalize_at((double)rv[k], now, a.t_scale, window);
+            T0[l] = v;
+            TU[l] = v;
+            TUB[l] = v;
+            TPX[l] = T(0);
+            TPY[l] = T(0);
+          }
+          if (lr >= 1) F64[l] = fv[k];
+        }
+      }
+    }
+  }
   __syncthreads();
 
   // -------------------------------------------------------------- ingest --
   // apply_event (pipeline.py:114-121) for the events of rows [r0-1, r1]:
   // private copies of f / the surface, raw of own rows straight to global
   {
-    __shared__ typename IngestSort<NT>::Storage ingest_sm;
+    __shared__ IngestShared<NT> ingest_sm;
     const int row_lo = r0 - 1 + lo_halo;
     ordered_ingest<NT>(
         ev, n_ev, H, W, row_lo, r0 - 1 + hi_halo, a.c_pos, a.c_neg, a.u_min, a.u_max, ingest_sm,
@@ -350,33 +393,45 @@ __global__ void __launch_bounds__(NT, 1) k_resident(const ResArgs<T> a) {
       if (pub) ++step;
     }
     __syncthreads();
-    // np.clip(u, 0, t_scale) (surface.py:195) -> global t (own rows)
+    // np.clip(u, 0, t_scale) (surface.py:195) -> global t (own rows) and
+    // the TD plane (QY is idle until the solve)
     EVR_FOR_ROWS(1, Rb)
       EVR_GK
-      a.t[gk] = vclip(TU[l], T(0), a.t_scaleT);
+      const T td = vclip(TU[l], T(0), a.t_scaleT);
+      a.t[gk] = td;
+      QY[l] = td;
     EVR_END_ROWS
   }
   // all rows of the denoised surface this band's metric reads are final
-  __syncthreads();
   const int s_met = a.tv_iters + 1;
   flag_publish(s_met);
-  if (a.manifold)
+  if (a.manifold) {
     flag_wait(band.of_row(has_up ? r0 - 1 : r0), band.of_row(r1 + 1 < H ? r1 + 1 : H - 1), s_met);
-  else
-    __syncthreads();
+    // neighbours' denoised rows r0-1 and r1 into the TD plane
+    for (int k = tid; k < 2 * W; k += NT) {
+      const bool up = k < W;
+      const int j = up ? k : k - W;
+      if (up ? has_up : has_dn) {
+        const int lr = up ? 0 : Rb + 1;
+        QY[lr * W + j] = __ldcg(a.t + (int64_t)(r0 - 1 + lr) * W + j);
+      }
+    }
+  }
   step = s_met;
+  asm volatile("cp.async.wait_all;" ::: "memory");  // warm-start u, p landed
+  __syncthreads();
 
   mark();
   // ------------------------------------------------------------ metric ---
-  // compute_metric + coeffs (surface.py:81-90, :199-205), solver constants,
-  // warm start u, p from the state
+  // compute_metric + coeffs (surface.py:81-90, :199-205), solver constants
+  T* const TD = QY;
   EVR_FOR_ROWS(lo_halo, hi_halo)
     EVR_GK
     T gx = T(0), gy = T(0);
     if (a.manifold) {
-      const T tc = __ldcg(a.t + gk);
-      gx = j < W - 1 ? __ldcg(a.t + gk + 1) - tc : T(0);
-      gy = gi < H - 1 ? __ldcg(a.t + gk + W) - tc : T(0);
+      const T tc = TD[l];
+      gx = j < W - 1 ? TD[l + 1] - tc : T(0);
+      if (gi < H - 1) gy = (lr <= Rb ? TD[l + W] : __ldcg(a.t + gk + W)) - tc;
     }
     const T g = metric_G(gx, gy);
     const T s = sqrt(g);
@@ -394,12 +449,8 @@ __global__ void __launch_bounds__(NT, 1) k_resident(const ResArgs<T> a) {
       a.G[gk] = g;
       a.sg[gk] = s;
     }
-    if (lr >= 1) U[l] = a.u[gk];
-    P1[l] = a.p1[gk];
-    P2[l] = a.p2[gk];
-    P3[l] = a.p3[gk];
   EVR_END_ROWS
-  __syncthreads();  // F64 (aliasing V / QX) is dead from here on
+  __syncthreads();  // F64 (aliasing V / QX) and TD (QY) are dead from here on
   EVR_FOR_ROWS(lo_halo, hi_halo)
     T qx, qy;
     q_of(Coef<T>{A11[l], A12[l], A22[l], A31[l], A32[l]}, P1[l], P2[l], P3[l], qx, qy);
