@@ -130,7 +130,7 @@ __global__ void k_metric_setup(const T* __restrict__ t, const double* __restrict
     gy = i < H - 1 ? t[k + W] - t[k] : T(0);
   }
   const T g = metric_G(gx, gy);
-  const T s = sqrt(g);
+  const T s = Arith<T>::sqrt(g);
   const Coef<T> a = coeffs_of(gx, gy, g);
   tx[k] = gx;
   ty[k] = gy;

@@ -20,17 +20,35 @@ template <class T> __device__ __forceinline__ T vclip(T x, T lo, T hi) {
   return vmin(vmax(x, lo), hi);
 }
 
+// Division / square root of the iteration kernels.  binary64: IEEE div.rn /
+// sqrt.rn (the bit-exact engine).  binary32: the hardware approximations
+// (MUFU-based, ~2 ulp), which keep the float engine well inside its 1e-4
+// log-intensity tolerance at a fraction of the instruction count.
+template <class T> struct Arith;
+template <> struct Arith<double> {
+  static __device__ __forceinline__ double div(double a, double b) { return a / b; }
+  static __device__ __forceinline__ double sqrt(double x) { return ::sqrt(x); }
+};
+template <> struct Arith<float> {
+  static __device__ __forceinline__ float div(float a, float b) { return __fdividef(a, b); }
+  static __device__ __forceinline__ float sqrt(float x) {
+    float r;
+    asm("sqrt.approx.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+  }
+};
+
 template <class T> struct Coef { T a11, a12, a22, a31, a32; };
 
 // MetricField.coeffs (surface.py:81-90)
 template <class T>
 __device__ __forceinline__ Coef<T> coeffs_of(T tx, T ty, T G) {
   Coef<T> c;
-  c.a11 = (T(1) + ty * ty) / G;
-  c.a12 = -(tx * ty) / G;
-  c.a22 = (T(1) + tx * tx) / G;
-  c.a31 = tx / G;
-  c.a32 = ty / G;
+  c.a11 = Arith<T>::div(T(1) + ty * ty, G);
+  c.a12 = Arith<T>::div(-(tx * ty), G);
+  c.a22 = Arith<T>::div(T(1) + tx * tx, G);
+  c.a31 = Arith<T>::div(tx, G);
+  c.a32 = Arith<T>::div(ty, G);
   return c;
 }
 
@@ -73,7 +91,7 @@ template <class T>
 __device__ __forceinline__ T kl_primal(T divq, T u, T beta, T fb, T tau, T umin, T umax) {
   const T t1 = divq * tau + u;
   const T s = t1 - beta;
-  const T r = (s + sqrt(s * s + fb)) * T(0.5);
+  const T r = (s + Arith<T>::sqrt(s * s + fb)) * T(0.5);
   return vclip(r, umin, umax);
 }
 
@@ -93,12 +111,18 @@ __device__ __forceinline__ void dual_step(const Coef<T>& c, T sigma, T gx, T gy,
   const T q1 = p1 + s11 * gx + s12 * gy;
   const T q2 = p2 + s12 * gx + s22 * gy;
   const T q3 = p3 + s31 * gx + s32 * gy;
-  T n = sqrt(q1 * q1 + q2 * q2 + q3 * q3);
-  n = n / sqrtG;
+  T n = Arith<T>::sqrt(q1 * q1 + q2 * q2 + q3 * q3);
+  if (sqrtG != T(1)) n = Arith<T>::div(n, sqrtG);  // x / 1 == x exactly
   n = vmax(n, T(1));
-  p1 = q1 / n;
-  p2 = q2 / n;
-  p3 = q3 / n;
+  if (n != T(1)) {  // interior point: p / 1 == p exactly
+    p1 = Arith<T>::div(q1, n);
+    p2 = Arith<T>::div(q2, n);
+    p3 = Arith<T>::div(q3, n);
+  } else {
+    p1 = q1;
+    p2 = q2;
+    p3 = q3;
+  }
 }
 
 // denoise_timestamps dual ascent + unit-ball projection (surface.py:168-183)
@@ -106,9 +130,14 @@ template <class T>
 __device__ __forceinline__ void tv_dual_step(T dx, T dy, T sigma, T& px, T& py) {
   const T a = px + dx * sigma;
   const T b = py + dy * sigma;
-  const T n = vmax(sqrt(a * a + b * b), T(1));
-  px = a / n;
-  py = b / n;
+  const T n = vmax(Arith<T>::sqrt(a * a + b * b), T(1));
+  if (n != T(1)) {
+    px = Arith<T>::div(a, n);
+    py = Arith<T>::div(b, n);
+  } else {
+    px = a;
+    py = b;
+  }
 }
 
 // denoise_timestamps primal step with L1 soft shrink (surface.py:185-193);

@@ -434,7 +434,7 @@ __global__ void __launch_bounds__(NT, 1) k_resident(const ResArgs<T> a) {
       if (gi < H - 1) gy = (lr <= Rb ? TD[l + W] : __ldcg(a.t + gk + W)) - tc;
     }
     const T g = metric_G(gx, gy);
-    const T s = sqrt(g);
+    const T s = Arith<T>::sqrt(g);
     const Coef<T> c = coeffs_of(gx, gy, g);
     A11[l] = c.a11;
     A12[l] = c.a12;
