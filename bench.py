@@ -197,8 +197,8 @@ def cpu_port_run(H, W, epp, pd, tv, rate, n_packets, seed, budget_s):
 
 
 def run_reference(args):
-    world, rank, local = dist_init(args)
-    if rank != 0:
+    # CPU arm: rank 0 alone runs (no process group, no GPU work)
+    if int(os.environ.get("RANK", "0")) != 0:
         return 0
     H, W, epp, pd, tv, rate = CONFIGS[args.config]
     os.environ.setdefault("OMP_NUM_THREADS", str(len(os.sched_getaffinity(0))))
@@ -321,6 +321,13 @@ def run_gpu(args):
         pass
     peak = float(peaks.get("hbm_gbs", 6650.0))
     achieved = bpkt / (kern_ms * 1e-3) / 1e9
+    traffic = None
+    try:
+        tr = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))
+        hit = tr.get(f"{args.config}/{args.precision}/{st.engine()}")
+        traffic = hit["bytes_per_launch"] if hit else None
+    except (OSError, ValueError, KeyError):
+        pass
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -350,7 +357,7 @@ def run_gpu(args):
                     "h2d_bytes_per_step": 32 + 16 * epp, "d2h_bytes_per_step": 8 * H * W + 16},
             "gpu_launches": int(launches),
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
-                         "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": None,
+                         "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": traffic,
                          "kernel": "whole packet" if st.engine() != "resident" else
                                    "evr::k_resident (one launch per packet)",
                          "algorithmic_bytes_per_launch": bpkt,
