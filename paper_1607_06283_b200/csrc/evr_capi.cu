@@ -69,7 +69,7 @@ struct evr_ctx {
   int64_t launches = 0;
   int engine = EVR_ENGINE_STREAMING;  // resolved
   // resident engine plan + buffers
-  int r_nb = 0, r_R = 0, r_nt = 0;
+  int r_nb = 0, r_R = 0, r_nt = 0, r_rm = 0;
   size_t r_smem = 0;
   unsigned long long* d_flags = nullptr;  // per-CTA progress words
   void* d_xchg = nullptr;                 // boundary-row ping-pong buffer
@@ -239,7 +239,32 @@ template <class T> int enqueue_packet(evr_ctx* ctx, int which) {
 
 // ---- resident engine glue ---------------------------------------------------
 
-template <class T> int resident_nt(int R, int W) { return (int64_t)R * W >= 512 ? 512 : 256; }
+// Instantiated (threads per CTA, max band rows) shapes of k_resident: a
+// thread per sensor column (NT >= W when possible), rows unrolled to RM.
+template <class T> struct ResidentKernel {
+  int nt, rm;
+  void (*fn)(ResArgs<T>);
+};
+template <class T> const ResidentKernel<T>* resident_kernels(int* n) {
+  static const ResidentKernel<T> table[] = {
+      {128, 1, k_resident<T, 128, 1>},   {128, 2, k_resident<T, 128, 2>},
+      {128, 4, k_resident<T, 128, 4>},   {384, 1, k_resident<T, 384, 1>},
+      {384, 2, k_resident<T, 384, 2>},   {384, 4, k_resident<T, 384, 4>},
+      {512, 1, k_resident<T, 512, 1>},   {512, 2, k_resident<T, 512, 2>},
+      {512, 4, k_resident<T, 512, 4>},
+  };
+  *n = (int)(sizeof(table) / sizeof(table[0]));
+  return table;
+}
+
+template <class T> const ResidentKernel<T>* resident_pick(int R, int W) {
+  int n = 0;
+  const ResidentKernel<T>* t = resident_kernels<T>(&n);
+  const int nt = W <= 128 ? 128 : W <= 384 ? 384 : 512;
+  for (int k = 0; k < n; ++k)
+    if (t[k].nt == nt && t[k].rm >= R) return &t[k];
+  return nullptr;
+}
 
 // Does the band decomposition fit on chip?  One CTA per SM, (R+2) rows of
 // every field in shared memory.
@@ -253,13 +278,15 @@ template <class T> bool resident_plan(evr_ctx* ctx) {
   // equal band heights: R rows per CTA, as few CTAs as that needs
   const int R = (H + std::min(H, sms) - 1) / std::min(H, sms);
   const int nb = (H + R - 1) / R;
-  const int nt = resident_nt<T>(R, W);
+  const ResidentKernel<T>* k = resident_pick<T>(R, W);
+  if (!k) return false;
   const size_t smem = resident_smem_bytes<T>(R, W);
-  const size_t static_smem = nt == 512 ? sizeof(IngestShared<512>) : sizeof(IngestShared<256>);
+  const size_t static_smem = sizeof(int) * 2 * k->nt + sizeof(int) * (k->nt / 32) + 64;
   if (smem + static_smem + 1024 > (size_t)optin) return false;
   ctx->r_nb = nb;
   ctx->r_R = R;
-  ctx->r_nt = nt;
+  ctx->r_nt = k->nt;
+  ctx->r_rm = k->rm;
   ctx->r_smem = smem;
   return true;
 }
@@ -281,7 +308,9 @@ template <class T> int resident_alloc(evr_ctx* ctx) {
   auto set_attr = [&](const void* fn) -> cudaError_t {
     return cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ctx->r_smem);
   };
-  CK(set_attr(ctx->r_nt == 512 ? (const void*)k_resident<T, 512> : (const void*)k_resident<T, 256>));
+  const ResidentKernel<T>* k = resident_pick<T>(ctx->r_R, ctx->W);
+  if (!k) return fail(ctx, EVR_ERR_UNSUPPORTED, "no resident kernel shape");
+  CK(set_attr((const void*)k->fn));
   return EVR_OK;
 }
 
@@ -313,7 +342,6 @@ template <class T> int resident_enqueue(evr_ctx* ctx, int which) {
   a.W = ctx->W;
   a.nb = ctx->r_nb;
   a.R = ctx->r_R;
-  a.wdiv = (unsigned)((((uint64_t)1 << 32) + ctx->W - 1) / ctx->W);
   a.tv_iters = g.denoise_iterations;
   a.pd_iters = g.max_iterations;
   a.manifold = g.manifold_enabled;
@@ -341,8 +369,8 @@ template <class T> int resident_enqueue(evr_ctx* ctx, int which) {
   attr[0].val.cooperative = 1;
   lc.attrs = attr;
   lc.numAttrs = 1;
-  cudaError_t e = ctx->r_nt == 512 ? cudaLaunchKernelEx(&lc, k_resident<T, 512>, a)
-                                   : cudaLaunchKernelEx(&lc, k_resident<T, 256>, a);
+  const ResidentKernel<T>* k = resident_pick<T>(ctx->r_R, ctx->W);
+  cudaError_t e = cudaLaunchKernelEx(&lc, k->fn, a);
   if (e != cudaSuccess) return fail(ctx, EVR_ERR_CUDA, "resident launch: %s", cudaGetErrorString(e));
   return 1;
 }

@@ -2,11 +2,17 @@
 // packet, the whole of process_packet (pipeline.py:142-171) on chip.
 //
 // Decomposition.  CTA b of a cooperative grid (<= 1 CTA per SM) owns the
-// row band [r0, r1) of the sensor (full width, equal band heights).  Every
+// row band [r0, r1) of the sensor (full width, equal band heights R).  Every
 // per-pixel field of the band lives in shared memory together with one halo
 // row above (r0-1) and one below (r1); global memory is touched only to
 // load the state at the start, to exchange two boundary rows per iteration,
 // and to write the state back at the end.
+//
+// Thread mapping.  Thread t owns sensor column(s) j = t, t+NT, ... and walks
+// the (at most RM+2) band rows of its column with every input gathered into
+// registers first, so the rows' float64 div/sqrt chains are independent
+// instructions the scheduler can overlap (ILP = band height) instead of
+// sequential passes.
 //
 // One neighbour exchange per iteration.  Each iteration recomputes on its
 // halo rows what it would otherwise have to wait for a second time
@@ -19,19 +25,21 @@
 //     of the neighbours' boundary rows are exchanged.
 // Recomputed halo values are bit-identical to the owner's (same inputs,
 // same operation order), so the band decomposition leaves every result
-// bit-identical to the single-domain reference.  Boundary rows go through
-// a ping-pong buffer in global memory (L2) and a per-CTA release/acquire
-// flag; a CTA waits only for its two neighbours, never for the grid.
+// bit-identical to the single-domain reference.
+//
+// Exchange protocol (per iteration).  The thread that produces a boundary
+// value stores it at once as 64-bit words of {32-bit payload, 32-bit
+// (packet, step) tag}; the neighbour polls its halo words until the tags
+// match.  A 64-bit store is single-copy atomic, so no fence or flag is
+// needed: one L2 round trip, ping-pong slots by step parity, two CTA
+// barriers per iteration.  A release/acquire progress flag per CTA is used
+// only once per packet (before the metric reads the neighbours' surface).
 //
 // q = A^T p (solve.py:149-158) is kept in two planes and refreshed right
-// after each pixel's dual update, so the primal's divergence reads its
-// left / upper neighbours' q instead of recomputing them.
-//
-// Ingest is fused: every CTA scans the packet and applies the events of
-// rows [r0-1, r1] with the same ordered, sort-grouped walk as k_ingest
-// (evr_ingest.cuh) to its private copies of f and of the surface
-// (duplicates compound in order, last timestamp wins); raw timestamps of
-// its own rows go straight to global memory (idempotent for neighbours).
+// after each pixel's dual update.  Ingest is fused (evr_ingest.cuh): every
+// CTA applies the packet's events of rows [r0-1, r1] in stream order to its
+// private copies of f and of the surface; raw timestamps of its own rows go
+// straight to global memory (idempotent for the neighbours).
 #pragma once
 
 #include <cstdint>
@@ -48,7 +56,7 @@ template <class T> struct ResArgs {
   int64_t* raw;
   T *u, *p1, *p2, *p3;           // state planes (global)
   T *t, *tx, *ty, *G, *sg;       // surface / metric planes (global, debug view)
-  T* xchg;                       // [2][nb][2][3][W] boundary rows
+  T* xchg;                       // tagged boundary words [2][nb][2][3][W][1|2]
   unsigned long long* flags;     // [nb] release/acquire progress words
   double* part;                  // [2*nb] rel_change partials
   unsigned* ticket;              // last-CTA election for the final sum
@@ -56,7 +64,6 @@ template <class T> struct ResArgs {
   int* err;
   unsigned long long* trace;     // optional [nb][256] phase timestamps (ns)
   int H, W, nb, R;
-  unsigned wdiv;                 // ceil(2^32 / W): q / W == __umulhi(q, wdiv)
   int tv_iters, pd_iters, manifold;
   double t_scale, c_pos, c_neg, u_min, u_max;
   T tau, sigma, tl, tv_step, shrink, t_scaleT, uminT, umaxT;
@@ -100,10 +107,7 @@ __device__ __forceinline__ void st_relaxed_u64(unsigned long long* p, unsigned l
   asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
-// Low-latency boundary-row exchange: every 64-bit word carries 32 payload
-// bits and a 32-bit tag naming the (packet, step) that wrote it.  A 64-bit
-// store is single-copy atomic, so a reader that sees the expected tag also
-// sees the payload -- no fence, no separate flag, one L2 round trip.
+// 64-bit words of {payload, tag} for one boundary value
 template <class T> struct LLWords;
 template <> struct LLWords<float> {
   static constexpr int N = 1;
@@ -135,15 +139,21 @@ template <class T> __device__ __forceinline__ void cp_async_elem(T* dst, const T
 
 struct Band {
   int base, extra;
-  __device__ __forceinline__ int rows(int b) const { return base + (b < extra ? 1 : 0); }
-  __device__ __forceinline__ int start(int b) const { return b * base + (b < extra ? b : extra); }
-  __device__ __forceinline__ int of_row(int r) const {
+  __host__ __device__ __forceinline__ int rows(int b) const { return base + (b < extra ? 1 : 0); }
+  __host__ __device__ __forceinline__ int start(int b) const {
+    return b * base + (b < extra ? b : extra);
+  }
+  __host__ __device__ __forceinline__ int of_row(int r) const {
     const int big = extra * (base + 1);
     return r < big ? r / (base + 1) : extra + (r - big) / base;
   }
 };
 
-template <class T, int NT>
+// Local rows lr = 0 .. RM+1 of a column (lr = global row - r0 + 1); the
+// loops are fully unrolled, the runtime band [lo, hi] masks them.
+#define EVR_ROWS(r) _Pragma("unroll") for (int r = 0; r < RM + 2; ++r)
+
+template <class T, int NT, int RM>
 __global__ void __launch_bounds__(NT, 1) k_resident(const ResArgs<T> a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int tid = threadIdx.x;
@@ -154,6 +164,8 @@ __global__ void __launch_bounds__(NT, 1) k_resident(const ResArgs<T> a) {
   const int r0 = band.start(b);
   const int r1 = r0 + Rb;
   const bool has_up = r0 > 0, has_dn = r1 < H;
+  const int lo_halo = has_up ? 0 : 1;
+  const int hi_halo = has_dn ? Rb + 1 : Rb;
   const size_t PS = (size_t)resident_plane_stride(a.R, W);
   T* pl = reinterpret_cast<T*>(smem_raw);
   T* const U = pl + RP_U * PS;
@@ -175,6 +187,7 @@ __global__ void __launch_bounds__(NT, 1) k_resident(const ResArgs<T> a) {
   T* const TUB = pl + RP_TUB * PS;
   T* const TPX = pl + RP_TPX * PS;
   T* const TPY = pl + RP_TPY * PS;
+  T* const TD = QY;  // denoised surface (TV-L1 end .. metric), QY idle then
   double* const F64 = reinterpret_cast<double*>(pl + RP_F64 * PS);
   double* const red = reinterpret_cast<double*>(pl + RP_COUNT * PS);
 
@@ -189,16 +202,8 @@ __global__ void __launch_bounds__(NT, 1) k_resident(const ResArgs<T> a) {
   const size_t xside = (size_t)3 * W * NWD;       // words of one side of one CTA
   const size_t xslot = (size_t)a.nb * 2 * xside;  // words of one ping-pong slot
   unsigned long long* const xw = reinterpret_cast<unsigned long long*>(a.xchg);
-
-  // rows [lo, hi] of the local frame (lr = global row - r0 + 1), flat loop
-#define EVR_FOR_ROWS(lo, hi)                                              \
-  for (int q_ = tid, n_ = ((hi) - (lo) + 1) * W; q_ < n_; q_ += NT) {      \
-    const int lr = (lo) + (int)__umulhi((unsigned)q_, a.wdiv);             \
-    const int j = q_ - (lr - (lo)) * W;                                    \
-    const int gi = r0 - 1 + lr;                                            \
-    const int l = lr * W + j;
-#define EVR_GK const int64_t gk = (int64_t)gi * W + j;
-#define EVR_END_ROWS }
+  auto in = [&](int r, int lo, int hi) { return r >= lo && r <= hi; };
+  auto gk_of = [&](int r, int j) { return (int64_t)(r0 - 1 + r) * W + j; };
 
   // optional phase timeline (diagnostics): globaltimer at phase marks
   int tmark = 0;
@@ -212,65 +217,70 @@ __global__ void __launch_bounds__(NT, 1) k_resident(const ResArgs<T> a) {
   };
   mark();
 
-  const int lo_halo = has_up ? 0 : 1;
-  const int hi_halo = has_dn ? Rb + 1 : Rb;
-
-  // boundary-row publish: the thread that produced (lr, j) of the first /
-  // last own row stores it as tagged words for the CTA above / below
-  auto ll_put = [&](int step, int lr, int j, int field, T v) {
+  // boundary value (r, j) of `field` goes to the CTA above (r == 1) and / or
+  // below (r == Rb) as tagged words
+  auto ll_put = [&](int step, int r, int j, int field, T v) {
     unsigned long long w[NWD];
     LLWords<T>::pack(v, tag_base + (unsigned)step, w);
     unsigned long long* base = xw + (step & 1) * xslot + (size_t)b * 2 * xside;
-    if (lr == 1) {
+    if (r == 1) {
       unsigned long long* d = base + ((size_t)field * W + j) * NWD;
 #pragma unroll
       for (int k = 0; k < NWD; ++k) st_relaxed_u64(d + k, w[k]);
     }
-    if (lr == Rb) {
+    if (r == Rb) {
       unsigned long long* d = base + xside + ((size_t)field * W + j) * NWD;
 #pragma unroll
       for (int k = 0; k < NWD; ++k) st_relaxed_u64(d + k, w[k]);
     }
   };
-  // halo rows <- neighbours' boundary rows of `step`, polling the tags; for
-  // the dual field also refresh q = A^T p there (coefficients cover halos)
+  // halo rows <- neighbours' boundary rows of `step` (both sides of a column
+  // polled together); for the dual field also refresh q = A^T p there
   auto ll_fetch = [&](int step, T* d0, T* d1, T* d2, int nf) {
     const unsigned want = tag_base + (unsigned)step;
     const unsigned long long* slot = xw + (step & 1) * xslot;
-    for (int k = tid; k < 2 * W; k += NT) {
-      const bool up = k < W;
-      const int j = up ? k : k - W;
-      if (up ? !has_up : !has_dn) continue;
-      // the CTA above sent its last row (side 1), the one below its first
-      const unsigned long long* src =
-          slot + (size_t)(up ? b - 1 : b + 1) * 2 * xside + (up ? xside : 0) + (size_t)j * NWD;
-      unsigned long long w[3][NWD];
+    const unsigned long long* up_src = slot + (size_t)(b - 1) * 2 * xside + xside;  // last row
+    const unsigned long long* dn_src = slot + (size_t)(b + 1) * 2 * xside;          // first row
+    for (int j = tid; j < W; j += NT) {
+      unsigned long long w[2][3][NWD];
       bool ready;
       do {
         ready = true;
-        for (int f = 0; f < nf; ++f)
 #pragma unroll
-          for (int q = 0; q < NWD; ++q) {
-            w[f][q] = ld_relaxed_u64(src + (size_t)f * W * NWD + q);
-            ready &= (unsigned)(w[f][q] >> 32) == want;
+        for (int s = 0; s < 2; ++s) {
+          if (s == 0 ? !has_up : !has_dn) continue;
+          const unsigned long long* src = (s == 0 ? up_src : dn_src) + (size_t)j * NWD;
+#pragma unroll
+          for (int f = 0; f < 3; ++f) {
+            if (f >= nf) break;
+#pragma unroll
+            for (int q = 0; q < NWD; ++q) {
+              w[s][f][q] = ld_relaxed_u64(src + (size_t)f * W * NWD + q);
+              ready &= (unsigned)(w[s][f][q] >> 32) == want;
+            }
           }
+        }
       } while (!ready);
-      const int l = up ? j : (Rb + 1) * W + j;
-      const T v0 = LLWords<T>::unpack(w[0]);
-      d0[l] = v0;
-      if (nf > 1) {
-        const T v1 = LLWords<T>::unpack(w[1]), v2 = LLWords<T>::unpack(w[2]);
-        d1[l] = v1;
-        d2[l] = v2;
-        T qx, qy;
-        q_of(Coef<T>{A11[l], A12[l], A22[l], A31[l], A32[l]}, v0, v1, v2, qx, qy);
-        QX[l] = qx;
-        QY[l] = qy;
+#pragma unroll
+      for (int s = 0; s < 2; ++s) {
+        if (s == 0 ? !has_up : !has_dn) continue;
+        const int l = (s == 0 ? 0 : Rb + 1) * W + j;
+        const T v0 = LLWords<T>::unpack(w[s][0]);
+        d0[l] = v0;
+        if (nf > 1) {
+          const T v1 = LLWords<T>::unpack(w[s][1]), v2 = LLWords<T>::unpack(w[s][2]);
+          d1[l] = v1;
+          d2[l] = v2;
+          T qx, qy;
+          q_of(Coef<T>{A11[l], A12[l], A22[l], A31[l], A32[l]}, v0, v1, v2, qx, qy);
+          QX[l] = qx;
+          QY[l] = qy;
+        }
       }
     }
     __syncthreads();
   };
-  // whole-CTA progress flag (used once per packet, not per iteration)
+  // whole-CTA progress flag (once per packet, not per iteration)
   auto flag_publish = [&](int step) {
     __syncthreads();
     if (tid == 0) {
@@ -287,59 +297,41 @@ __global__ void __launch_bounds__(NT, 1) k_resident(const ResArgs<T> a) {
   };
 
   // ---------------------------------------------------------------- load --
-  // warm-start u, p: asynchronous copies straight into their (idle until
-  // the solve) planes, in flight during ingest and TV-L1
-  EVR_FOR_ROWS(lo_halo, hi_halo)
-    EVR_GK
-    if (lr >= 1) cp_async_elem(U + l, a.u + gk);
-    cp_async_elem(P1 + l, a.p1 + gk);
-    cp_async_elem(P2 + l, a.p2 + gk);
-    cp_async_elem(P3 + l, a.p3 + gk);
-  EVR_END_ROWS
-  asm volatile("cp.async.commit_group;" ::: "memory");
-  // raw timestamps -> surface heights, f -> binary64 plane; loads batched
-  // KB deep per thread so their latencies overlap
-  {
-    constexpr int KB = 4;
-    const int n_ = (hi_halo - lo_halo + 1) * W;
-    for (int q0 = tid; q0 < n_; q0 += NT * KB) {
-      int64_t rv[KB];
-      double fv[KB];
-#pragma unroll
-      for (int k = 0; k < KB; ++k) {
-        const int q = q0 + k * NT;
-        if (q < n_) {
-          const int lr = lo_halo + (int)__umulhi((unsigned)q, a.wdiv);
-          const int j = q - (lr - lo_halo) * W;
-          const int64_t gk = (int64_t)(r0 - 1 + lr) * W + j;
-          rv[k] = a.manifold ? a.raw[gk] : 0;
-          fv[k] = lr >= 1 ? a.f[gk] : 0.0;
-        }
+  for (int j = tid; j < W; j += NT) {
+    int64_t rv[RM + 2];
+    double fv[RM + 2];
+    EVR_ROWS(r) {
+      if (!in(r, lo_halo, hi_halo)) continue;
+      const int64_t gk = gk_of(r, j);
+      const int l = r * W + j;
+      // warm-start u, p: asynchronous copies into their (idle until the
+      // solve) planes, in flight during ingest and TV-L1
+      if (r >= 1) cp_async_elem(U + l, a.u + gk);
+      cp_async_elem(P1 + l, a.p1 + gk);
+      cp_async_elem(P2 + l, a.p2 + gk);
+      cp_async_elem(P3 + l, a.p3 + gk);
+      rv[r] = a.manifold ? a.raw[gk] : 0;
+      fv[r] = r >= 1 ? a.f[gk] : 0.0;
+    }
+    EVR_ROWS(r) {
+      if (!in(r, lo_halo, hi_halo)) continue;
+      const int l = r * W + j;
+      if (a.manifold) {
+        const T v = (T)normalize_at((double)rv[r], now, a.t_scale, window);
+        T0[l] = v;
+        TU[l] = v;
+        TUB[l] = v;
+        TPX[l] = T(0);
+        TPY[l] = T(0);
       }
-#pragma unroll
-      for (int k = 0; k < KB; ++k) {
-        const int q = q0 + k * NT;
-        if (q < n_) {
-          const int lr = lo_halo + (int)__umulhi((unsigned)q, a.wdiv);
-          const int l = lr * W + (q - (lr - lo_halo) * W);
-          if (a.manifold) {
-            const T v = (T)normalize_at((double)rv[k], now, a.t_scale, window);
-            T0[l] = v;
-            TU[l] = v;
-            TUB[l] = v;
-            TPX[l] = T(0);
-            TPY[l] = T(0);
-          }
-          if (lr >= 1) F64[l] = fv[k];
-        }
-      }
+      if (r >= 1) F64[l] = fv[r];
     }
   }
+  asm volatile("cp.async.commit_group;" ::: "memory");
   __syncthreads();
 
   // -------------------------------------------------------------- ingest --
-  // apply_event (pipeline.py:114-121) for the events of rows [r0-1, r1]:
-  // private copies of f / the surface, raw of own rows straight to global
+  // apply_event (pipeline.py:114-121) for the events of rows [r0-1, r1]
   {
     __shared__ IngestShared<NT> ingest_sm;
     const int row_lo = r0 - 1 + lo_halo;
@@ -360,8 +352,8 @@ __global__ void __launch_bounds__(NT, 1) k_resident(const ResArgs<T> a) {
           if (lr >= 1 && lr <= Rb) a.raw[(int64_t)(r0 - 1) * W + l] = t;
         });
   }
-
   mark();  // 1: loaded + ingested
+
   // ------------------------------------------------------------ TV-L1 ----
   // denoise_timestamps (surface.py:146-196), one exchange per iteration
   int step = 0;
@@ -370,51 +362,80 @@ __global__ void __launch_bounds__(NT, 1) k_resident(const ResArgs<T> a) {
       const bool pub = it < a.tv_iters - 1;
       if (it > 0) ll_fetch(step, TUB, nullptr, nullptr, 1);  // u_bar of step `it`
       mark();
-      EVR_FOR_ROWS(lo_halo, Rb)  // dual, own rows + halo row above
-        const T dx = j < W - 1 ? TUB[l + 1] - TUB[l] : T(0);
-        const T dy = gi < H - 1 ? TUB[l + W] - TUB[l] : T(0);
-        T px = TPX[l], py = TPY[l];
-        tv_dual_step(dx, dy, a.tv_step, px, py);
-        TPX[l] = px;
-        TPY[l] = py;
-      EVR_END_ROWS
+      // dual ascent + projection (surface.py:168-183), own rows + halo above
+      for (int j = tid; j < W; j += NT) {
+        T ub[RM + 2], ubr[RM + 2], px[RM + 2], py[RM + 2];
+        EVR_ROWS(r) {
+          const int l = r * W + j;
+          if (in(r, lo_halo, hi_halo)) ub[r] = TUB[l];
+          if (in(r, lo_halo, Rb)) {
+            ubr[r] = j < W - 1 ? TUB[l + 1] : T(0);
+            px[r] = TPX[l];
+            py[r] = TPY[l];
+          }
+        }
+        EVR_ROWS(r) {
+          if (!in(r, lo_halo, Rb)) continue;
+          const T dx = j < W - 1 ? ubr[r] - ub[r] : T(0);
+          const T dy = r0 - 1 + r < H - 1 ? ub[r < RM + 1 ? r + 1 : r] - ub[r] : T(0);
+          tv_dual_step(dx, dy, a.tv_step, px[r], py[r]);
+        }
+        EVR_ROWS(r) {
+          if (!in(r, lo_halo, Rb)) continue;
+          TPX[r * W + j] = px[r];
+          TPY[r * W + j] = py[r];
+        }
+      }
       __syncthreads();
-      EVR_FOR_ROWS(1, Rb)  // primal, own rows; boundary rows go out at once
-        const T d = div_at(TPX[l], j > 0 ? TPX[l - 1] : T(0), TPY[l], gi > 0 ? TPY[l - W] : T(0),
-                           gi, j, H, W);
-        T ub;
-        const T un = tv_primal_step(d, TU[l], T0[l], a.tv_step, a.shrink, ub);
-        TU[l] = un;
-        TUB[l] = ub;
-        if (pub) ll_put(step + 1, lr, j, 0, ub);
-      EVR_END_ROWS
+      // primal + L1 shrink (surface.py:185-193), own rows; boundary rows go
+      // out to the neighbours as soon as they are computed
+      for (int j = tid; j < W; j += NT) {
+        T pxc[RM + 2], pxl[RM + 2], pyc[RM + 2], tu[RM + 2], t0[RM + 2];
+        EVR_ROWS(r) {
+          const int l = r * W + j;
+          if (in(r, lo_halo, Rb)) pyc[r] = TPY[l];
+          if (in(r, 1, Rb)) {
+            pxc[r] = TPX[l];
+            pxl[r] = j > 0 ? TPX[l - 1] : T(0);
+            tu[r] = TU[l];
+            t0[r] = T0[l];
+          }
+        }
+        EVR_ROWS(r) {
+          if (!in(r, 1, Rb)) continue;
+          const int gi = r0 - 1 + r;
+          const T d = div_at(pxc[r], pxl[r], pyc[r], gi > 0 ? pyc[r - 1 >= 0 ? r - 1 : 0] : T(0),
+                             gi, j, H, W);
+          T ub;
+          const T un = tv_primal_step(d, tu[r], t0[r], a.tv_step, a.shrink, ub);
+          TU[r * W + j] = un;
+          TUB[r * W + j] = ub;
+          if (pub) ll_put(step + 1, r, j, 0, ub);
+        }
+      }
       // no barrier: the next fetch only writes halo rows of u_bar, which
       // this primal does not read
       if (pub) ++step;
     }
     __syncthreads();
-    // np.clip(u, 0, t_scale) (surface.py:195) -> global t (own rows) and
-    // the TD plane (QY is idle until the solve)
-    EVR_FOR_ROWS(1, Rb)
-      EVR_GK
-      const T td = vclip(TU[l], T(0), a.t_scaleT);
-      a.t[gk] = td;
-      QY[l] = td;
-    EVR_END_ROWS
+    // np.clip(u, 0, t_scale) (surface.py:195) -> global t and the TD plane
+    for (int j = tid; j < W; j += NT) {
+      EVR_ROWS(r) {
+        if (!in(r, 1, Rb)) continue;
+        const T td = vclip(TU[r * W + j], T(0), a.t_scaleT);
+        a.t[gk_of(r, j)] = td;
+        TD[r * W + j] = td;
+      }
+    }
   }
   // all rows of the denoised surface this band's metric reads are final
   const int s_met = a.tv_iters + 1;
   flag_publish(s_met);
   if (a.manifold) {
     flag_wait(band.of_row(has_up ? r0 - 1 : r0), band.of_row(r1 + 1 < H ? r1 + 1 : H - 1), s_met);
-    // neighbours' denoised rows r0-1 and r1 into the TD plane
-    for (int k = tid; k < 2 * W; k += NT) {
-      const bool up = k < W;
-      const int j = up ? k : k - W;
-      if (up ? has_up : has_dn) {
-        const int lr = up ? 0 : Rb + 1;
-        QY[lr * W + j] = __ldcg(a.t + (int64_t)(r0 - 1 + lr) * W + j);
-      }
+    for (int j = tid; j < W; j += NT) {  // neighbours' denoised rows r0-1, r1
+      if (has_up) TD[j] = __ldcg(a.t + gk_of(0, j));
+      if (has_dn) TD[(Rb + 1) * W + j] = __ldcg(a.t + gk_of(Rb + 1, j));
     }
   }
   step = s_met;
@@ -424,39 +445,47 @@ __global__ void __launch_bounds__(NT, 1) k_resident(const ResArgs<T> a) {
   mark();
   // ------------------------------------------------------------ metric ---
   // compute_metric + coeffs (surface.py:81-90, :199-205), solver constants
-  T* const TD = QY;
-  EVR_FOR_ROWS(lo_halo, hi_halo)
-    EVR_GK
-    T gx = T(0), gy = T(0);
-    if (a.manifold) {
-      const T tc = TD[l];
-      gx = j < W - 1 ? TD[l + 1] - tc : T(0);
-      if (gi < H - 1) gy = (lr <= Rb ? TD[l + W] : __ldcg(a.t + gk + W)) - tc;
+  for (int j = tid; j < W; j += NT) {
+    EVR_ROWS(r) {
+      if (!in(r, lo_halo, hi_halo)) continue;
+      const int l = r * W + j;
+      const int gi = r0 - 1 + r;
+      T gx = T(0), gy = T(0);
+      if (a.manifold) {
+        const T tc = TD[l];
+        gx = j < W - 1 ? TD[l + 1] - tc : T(0);
+        if (gi < H - 1) gy = (r <= Rb ? TD[l + W] : __ldcg(a.t + gk_of(r + 1, j))) - tc;
+      }
+      const T g = metric_G(gx, gy);
+      const T s = Arith<T>::sqrt(g);
+      const Coef<T> c = coeffs_of(gx, gy, g);
+      A11[l] = c.a11;
+      A12[l] = c.a12;
+      A22[l] = c.a22;
+      A31[l] = c.a31;
+      A32[l] = c.a32;
+      SG[l] = s;
+      if (r >= 1) FB[l] = T(4) * (a.tl * s) * (T)F64[l];
+      if (r >= 1 && r <= Rb) {
+        const int64_t gk = gk_of(r, j);
+        a.tx[gk] = gx;
+        a.ty[gk] = gy;
+        a.G[gk] = g;
+        a.sg[gk] = s;
+      }
     }
-    const T g = metric_G(gx, gy);
-    const T s = Arith<T>::sqrt(g);
-    const Coef<T> c = coeffs_of(gx, gy, g);
-    A11[l] = c.a11;
-    A12[l] = c.a12;
-    A22[l] = c.a22;
-    A31[l] = c.a31;
-    A32[l] = c.a32;
-    SG[l] = s;
-    if (lr >= 1) FB[l] = T(4) * (a.tl * s) * (T)F64[l];
-    if (lr >= 1 && lr <= Rb) {
-      a.tx[gk] = gx;
-      a.ty[gk] = gy;
-      a.G[gk] = g;
-      a.sg[gk] = s;
-    }
-  EVR_END_ROWS
+  }
   __syncthreads();  // F64 (aliasing V / QX) and TD (QY) are dead from here on
-  EVR_FOR_ROWS(lo_halo, hi_halo)
-    T qx, qy;
-    q_of(Coef<T>{A11[l], A12[l], A22[l], A31[l], A32[l]}, P1[l], P2[l], P3[l], qx, qy);
-    QX[l] = qx;
-    QY[l] = qy;
-  EVR_END_ROWS
+  for (int j = tid; j < W; j += NT) {
+    EVR_ROWS(r) {
+      if (!in(r, lo_halo, hi_halo)) continue;
+      const int l = r * W + j;
+      T qx, qy;
+      q_of(Coef<T>{A11[l], A12[l], A22[l], A31[l], A32[l]}, P1[l], P2[l], P3[l], qx, qy);
+      QX[l] = qx;
+      QY[l] = qy;
+    }
+  }
   __syncthreads();
 
   // ------------------------------------------------------- primal-dual ---
@@ -467,39 +496,77 @@ __global__ void __launch_bounds__(NT, 1) k_resident(const ResArgs<T> a) {
     const bool last = it == a.pd_iters - 1;
     if (it > 0) ll_fetch(step, P1, P2, P3, 3);  // p of the previous step (+ q)
     mark();
-    EVR_FOR_ROWS(1, hi_halo)  // primal + over-relaxation, own rows + halo below
-      const T d = div_at(QX[l], j > 0 ? QX[l - 1] : T(0), QY[l], gi > 0 ? QY[l - W] : T(0), gi,
-                         j, H, W);
-      const T uk = U[l];
-      const T nu = kl_primal(d, uk, a.tl * SG[l], FB[l], a.tau, a.uminT, a.umaxT);
-      V[l] = nu * T(2) - uk;
-      U[l] = nu;
-      if (last && lr <= Rb) {
-        const double e = (double)nu - (double)uk;
-        rd += e * e;
-        ro += (double)uk * (double)uk;
+    // KL prox + over-relaxation (solve.py:234-252), own rows + halo below
+    for (int j = tid; j < W; j += NT) {
+      T qxc[RM + 2], qxl[RM + 2], qyc[RM + 2], uu[RM + 2], sgv[RM + 2], fbv[RM + 2];
+      EVR_ROWS(r) {
+        const int l = r * W + j;
+        if (in(r, lo_halo, hi_halo)) qyc[r] = QY[l];
+        if (in(r, 1, hi_halo)) {
+          qxc[r] = QX[l];
+          qxl[r] = j > 0 ? QX[l - 1] : T(0);
+          uu[r] = U[l];
+          sgv[r] = SG[l];
+          fbv[r] = FB[l];
+        }
       }
-    EVR_END_ROWS
+      EVR_ROWS(r) {
+        if (!in(r, 1, hi_halo)) continue;
+        const int gi = r0 - 1 + r;
+        const T d = div_at(qxc[r], qxl[r], qyc[r], gi > 0 ? qyc[r - 1 >= 0 ? r - 1 : 0] : T(0),
+                           gi, j, H, W);
+        const T uk = uu[r];
+        const T nu = kl_primal(d, uk, a.tl * sgv[r], fbv[r], a.tau, a.uminT, a.umaxT);
+        V[r * W + j] = nu * T(2) - uk;
+        U[r * W + j] = nu;
+        if (last && r <= Rb) {
+          const double e = (double)nu - (double)uk;
+          rd += e * e;
+          ro += (double)uk * (double)uk;
+        }
+      }
+    }
     __syncthreads();
-    EVR_FOR_ROWS(1, Rb)  // dual ascent + ball projection, own rows; refresh q
-      const T gx = j < W - 1 ? V[l + 1] - V[l] : T(0);
-      const T gy = gi < H - 1 ? V[l + W] - V[l] : T(0);
-      const Coef<T> c{A11[l], A12[l], A22[l], A31[l], A32[l]};
-      T q1 = P1[l], q2 = P2[l], q3 = P3[l];
-      dual_step(c, a.sigma, gx, gy, SG[l], q1, q2, q3);
-      P1[l] = q1;
-      P2[l] = q2;
-      P3[l] = q3;
-      T qx, qy;
-      q_of(c, q1, q2, q3, qx, qy);
-      QX[l] = qx;
-      QY[l] = qy;
-      if (!last) {
-        ll_put(step + 1, lr, j, 0, q1);
-        ll_put(step + 1, lr, j, 1, q2);
-        ll_put(step + 1, lr, j, 2, q3);
+    // dual ascent + ball projection (solve.py:170-201), own rows; refresh q;
+    // boundary rows go out to the neighbours as soon as they are computed
+    for (int j = tid; j < W; j += NT) {
+      T vv[RM + 2], vr[RM + 2], p1[RM + 2], p2[RM + 2], p3[RM + 2], sgv[RM + 2];
+      Coef<T> c[RM + 2];
+      EVR_ROWS(r) {
+        const int l = r * W + j;
+        if (in(r, 1, hi_halo)) vv[r] = V[l];
+        if (in(r, 1, Rb)) {
+          vr[r] = j < W - 1 ? V[l + 1] : T(0);
+          p1[r] = P1[l];
+          p2[r] = P2[l];
+          p3[r] = P3[l];
+          sgv[r] = SG[l];
+          c[r] = Coef<T>{A11[l], A12[l], A22[l], A31[l], A32[l]};
+        }
       }
-    EVR_END_ROWS
+      EVR_ROWS(r) {
+        if (!in(r, 1, Rb)) continue;
+        const T gx = j < W - 1 ? vr[r] - vv[r] : T(0);
+        const T gy = r0 - 1 + r < H - 1 ? vv[r < RM + 1 ? r + 1 : r] - vv[r] : T(0);
+        dual_step(c[r], a.sigma, gx, gy, sgv[r], p1[r], p2[r], p3[r]);
+      }
+      EVR_ROWS(r) {
+        if (!in(r, 1, Rb)) continue;
+        const int l = r * W + j;
+        P1[l] = p1[r];
+        P2[l] = p2[r];
+        P3[l] = p3[r];
+        T qx, qy;
+        q_of(c[r], p1[r], p2[r], p3[r], qx, qy);
+        QX[l] = qx;
+        QY[l] = qy;
+        if (!last) {
+          ll_put(step + 1, r, j, 0, p1[r]);
+          ll_put(step + 1, r, j, 1, p2[r]);
+          ll_put(step + 1, r, j, 2, p3[r]);
+        }
+      }
+    }
     // no barrier: the next fetch only writes halo rows of p / q, which this
     // dual step does not read
     if (!last) ++step;
@@ -510,22 +577,23 @@ __global__ void __launch_bounds__(NT, 1) k_resident(const ResArgs<T> a) {
     flag_wait(has_up ? b - 1 : b, has_dn ? b + 1 : b, s_met + 1);
   }
   __syncthreads();
-
   mark();
+
   // ---------------------------------------------------------- epilogue ---
   // state.u = u+, state.p, state.f = copy(u+) (pipeline.py:167-170)
-  EVR_FOR_ROWS(1, Rb)
-    EVR_GK
-    const T v = U[l];
-    a.u[gk] = v;
-    a.f[gk] = (double)v;
-    a.p1[gk] = P1[l];
-    a.p2[gk] = P2[l];
-    a.p3[gk] = P3[l];
-  EVR_END_ROWS
-#undef EVR_FOR_ROWS
-#undef EVR_GK
-#undef EVR_END_ROWS
+  for (int j = tid; j < W; j += NT) {
+    EVR_ROWS(r) {
+      if (!in(r, 1, Rb)) continue;
+      const int l = r * W + j;
+      const int64_t gk = gk_of(r, j);
+      const T v = U[l];
+      a.u[gk] = v;
+      a.f[gk] = (double)v;
+      a.p1[gk] = P1[l];
+      a.p2[gk] = P2[l];
+      a.p3[gk] = P3[l];
+    }
+  }
 
   // rel_change = |u+ - u| / max(|u|, 1e-30) (solve.py:246-249): fixed-order
   // block tree, per-CTA partials, last CTA folds them in index order
@@ -556,5 +624,7 @@ __global__ void __launch_bounds__(NT, 1) k_resident(const ResArgs<T> a) {
     }
   }
 }
+
+#undef EVR_ROWS
 
 }  // namespace evr
