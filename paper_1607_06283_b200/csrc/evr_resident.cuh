@@ -527,6 +527,7 @@ __global__ void __launch_bounds__(NT, 1) k_resident(const ResArgs<T> a) {
       }
     }
     __syncthreads();
+    mark();  // primal done
     // dual ascent + ball projection (solve.py:170-201), own rows; refresh q;
     // boundary rows go out to the neighbours as soon as they are computed
     for (int j = tid; j < W; j += NT) {
@@ -569,6 +570,7 @@ __global__ void __launch_bounds__(NT, 1) k_resident(const ResArgs<T> a) {
     }
     // no barrier: the next fetch only writes halo rows of p / q, which this
     // dual step does not read
+    mark();  // dual issued (thread 0)
     if (!last) ++step;
   }
   if (a.pd_iters < 2) {
