@@ -50,7 +50,9 @@ typedef enum { EVR_PREC_F64 = 0, EVR_PREC_F32 = 1 } evr_precision;
 typedef enum {
     EVR_ENGINE_AUTO = 0,      /* resident when it fits, else streaming */
     EVR_ENGINE_STREAMING = 1, /* one launch per half-step, fields in HBM/L2 */
-    EVR_ENGINE_RESIDENT = 2   /* persistent on-chip kernel (row bands) */
+    EVR_ENGINE_RESIDENT = 2,  /* persistent kernel, row bands in shared memory */
+    EVR_ENGINE_RESIDENT_GMEM = 3 /* persistent kernel, band frames in L2/HBM
+                                    (reported only; requested as RESIDENT/AUTO) */
 } evr_engine;
 
 /* One camera event: events.py:35-43 Event(x, y, polarity, timestamp).

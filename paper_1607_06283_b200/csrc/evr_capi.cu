@@ -69,8 +69,9 @@ struct evr_ctx {
   int64_t launches = 0;
   int engine = EVR_ENGINE_STREAMING;  // resolved
   // resident engine plan + buffers
-  int r_nb = 0, r_R = 0, r_nt = 0, r_rm = 0;
-  size_t r_smem = 0;
+  int r_nb = 0, r_R = 0, r_nt = 0, r_ms = 0;
+  size_t r_smem = 0, r_frame = 0;
+  void* d_frames = nullptr;               // PLANES_GMEM per-CTA plane frames
   unsigned long long* d_flags = nullptr;  // per-CTA progress words
   void* d_xchg = nullptr;                 // boundary-row ping-pong buffer
   unsigned* d_ticket = nullptr;
@@ -239,55 +240,54 @@ template <class T> int enqueue_packet(evr_ctx* ctx, int which) {
 
 // ---- resident engine glue ---------------------------------------------------
 
-// Instantiated (threads per CTA, max band rows) shapes of k_resident: a
-// thread per sensor column (NT >= W when possible), rows unrolled to RM.
+// Instantiated shapes of k_resident: threads per CTA (a thread per sensor
+// column when W <= NT), CH = 2 rows per register chunk, and where the CTA's
+// frame of planes lives (shared memory, else a global-memory slice).
+constexpr int kResidentCH = 2;
 template <class T> struct ResidentKernel {
-  int nt, rm;
+  int nt, ms;
   void (*fn)(ResArgs<T>);
 };
-template <class T> const ResidentKernel<T>* resident_kernels(int* n) {
+template <class T> const ResidentKernel<T>* resident_pick(int W, int ms) {
   static const ResidentKernel<T> table[] = {
-      {128, 1, k_resident<T, 128, 1>},   {128, 2, k_resident<T, 128, 2>},
-      {128, 4, k_resident<T, 128, 4>},   {384, 1, k_resident<T, 384, 1>},
-      {384, 2, k_resident<T, 384, 2>},   {384, 4, k_resident<T, 384, 4>},
-      {512, 1, k_resident<T, 512, 1>},   {512, 2, k_resident<T, 512, 2>},
-      {512, 4, k_resident<T, 512, 4>},
+      {128, PLANES_SMEM, k_resident<T, 128, kResidentCH, PLANES_SMEM>},
+      {384, PLANES_SMEM, k_resident<T, 384, kResidentCH, PLANES_SMEM>},
+      {512, PLANES_SMEM, k_resident<T, 512, kResidentCH, PLANES_SMEM>},
+      {128, PLANES_GMEM, k_resident<T, 128, kResidentCH, PLANES_GMEM>},
+      {384, PLANES_GMEM, k_resident<T, 384, kResidentCH, PLANES_GMEM>},
+      {512, PLANES_GMEM, k_resident<T, 512, kResidentCH, PLANES_GMEM>},
   };
-  *n = (int)(sizeof(table) / sizeof(table[0]));
-  return table;
-}
-
-template <class T> const ResidentKernel<T>* resident_pick(int R, int W) {
-  int n = 0;
-  const ResidentKernel<T>* t = resident_kernels<T>(&n);
   const int nt = W <= 128 ? 128 : W <= 384 ? 384 : 512;
-  for (int k = 0; k < n; ++k)
-    if (t[k].nt == nt && t[k].rm >= R) return &t[k];
+  for (const auto& k : table)
+    if (k.nt == nt && k.ms == ms) return &k;
   return nullptr;
 }
 
-// Does the band decomposition fit on chip?  One CTA per SM, (R+2) rows of
-// every field in shared memory.
-template <class T> bool resident_plan(evr_ctx* ctx) {
+// Band decomposition: one CTA per SM at most, equal band heights R.  The
+// frame goes to shared memory when it fits, else to global memory.
+template <class T> bool resident_plan(evr_ctx* ctx, bool allow_gmem, bool force_gmem = false) {
   int sms = 0, optin = 0;
   if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device) != cudaSuccess ||
       cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device) !=
           cudaSuccess)
     return false;
   const int H = ctx->H, W = ctx->W;
-  // equal band heights: R rows per CTA, as few CTAs as that needs
   const int R = (H + std::min(H, sms) - 1) / std::min(H, sms);
   const int nb = (H + R - 1) / R;
-  const ResidentKernel<T>* k = resident_pick<T>(R, W);
-  if (!k) return false;
-  const size_t smem = resident_smem_bytes<T>(R, W);
-  const size_t static_smem = sizeof(int) * 2 * k->nt + sizeof(int) * (k->nt / 32) + 64;
-  if (smem + static_smem + 1024 > (size_t)optin) return false;
+  const size_t frame = resident_frame_bytes<T>(R, W);
+  const int nt = W <= 128 ? 128 : W <= 384 ? 384 : 512;
+  const size_t static_smem = sizeof(IngestShared<512>) + 64 * sizeof(double) + 64;
+  int ms = PLANES_SMEM;
+  if (force_gmem || frame + static_smem + 1024 > (size_t)optin) {
+    if (!allow_gmem) return false;
+    ms = PLANES_GMEM;
+  }
   ctx->r_nb = nb;
   ctx->r_R = R;
-  ctx->r_nt = k->nt;
-  ctx->r_rm = k->rm;
-  ctx->r_smem = smem;
+  ctx->r_nt = nt;
+  ctx->r_ms = ms;
+  ctx->r_smem = ms == PLANES_SMEM ? frame : 0;
+  ctx->r_frame = frame;
   return true;
 }
 
@@ -295,9 +295,11 @@ template <class T> int resident_alloc(evr_ctx* ctx) {
   cudaFree(ctx->d_flags);
   cudaFree(ctx->d_xchg);
   cudaFree(ctx->d_ticket);
+  cudaFree(ctx->d_frames);
   ctx->d_flags = nullptr;
   ctx->d_xchg = nullptr;
   ctx->d_ticket = nullptr;
+  ctx->d_frames = nullptr;
   CK(cudaMalloc(&ctx->d_flags, sizeof(unsigned long long) * ctx->r_nb));
   CK(cudaMemset(ctx->d_flags, 0, sizeof(unsigned long long) * ctx->r_nb));
   const size_t xbytes = sizeof(unsigned long long) * LLWords<T>::N * 2 * ctx->r_nb * 2 * 3 * (size_t)ctx->W;
@@ -305,12 +307,11 @@ template <class T> int resident_alloc(evr_ctx* ctx) {
   CK(cudaMemset(ctx->d_xchg, 0, xbytes));  // no stale tag can match a live one
   CK(cudaMalloc(&ctx->d_ticket, sizeof(unsigned)));
   CK(cudaMemset(ctx->d_ticket, 0, sizeof(unsigned)));
-  auto set_attr = [&](const void* fn) -> cudaError_t {
-    return cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ctx->r_smem);
-  };
-  const ResidentKernel<T>* k = resident_pick<T>(ctx->r_R, ctx->W);
+  if (ctx->r_ms == PLANES_GMEM) CK(cudaMalloc(&ctx->d_frames, ctx->r_frame * ctx->r_nb));
+  const ResidentKernel<T>* k = resident_pick<T>(ctx->W, ctx->r_ms);
   if (!k) return fail(ctx, EVR_ERR_UNSUPPORTED, "no resident kernel shape");
-  CK(set_attr((const void*)k->fn));
+  CK(cudaFuncSetAttribute((const void*)k->fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          (int)ctx->r_smem));
   return EVR_OK;
 }
 
@@ -332,6 +333,7 @@ template <class T> int resident_enqueue(evr_ctx* ctx, int which) {
   a.G = ctx->fld<T>(F_G);
   a.sg = ctx->fld<T>(F_SG);
   a.xchg = reinterpret_cast<T*>(ctx->d_xchg);
+  a.frames = reinterpret_cast<T*>(ctx->d_frames);
   a.flags = ctx->d_flags;
   a.part = ctx->part;
   a.ticket = ctx->d_ticket;
@@ -369,14 +371,14 @@ template <class T> int resident_enqueue(evr_ctx* ctx, int which) {
   attr[0].val.cooperative = 1;
   lc.attrs = attr;
   lc.numAttrs = 1;
-  const ResidentKernel<T>* k = resident_pick<T>(ctx->r_R, ctx->W);
+  const ResidentKernel<T>* k = resident_pick<T>(ctx->W, ctx->r_ms);
   cudaError_t e = cudaLaunchKernelEx(&lc, k->fn, a);
   if (e != cudaSuccess) return fail(ctx, EVR_ERR_CUDA, "resident launch: %s", cudaGetErrorString(e));
   return 1;
 }
 
 int enqueue_packet_any(evr_ctx* ctx, int which) {
-  if (ctx->engine == EVR_ENGINE_RESIDENT) {
+  if (ctx->engine >= EVR_ENGINE_RESIDENT) {
     return ctx->prec == EVR_PREC_F64 ? resident_enqueue<double>(ctx, which)
                                      : resident_enqueue<float>(ctx, which);
   }
@@ -728,6 +730,7 @@ void evr_destroy(evr_ctx* ctx) {
   cudaFree(ctx->d_flags);
   cudaFree(ctx->d_xchg);
   cudaFree(ctx->d_ticket);
+  cudaFree(ctx->d_frames);
   cudaFree(ctx->d_trace);
   for (int i = 0; i < 2; ++i) {
     if (ctx->h_stage[i]) cudaFreeHost(ctx->h_stage[i]);
@@ -752,10 +755,10 @@ int evr_set_config(evr_ctx* ctx, const evr_config* cfg) {
   ctx->engine = EVR_ENGINE_STREAMING;
   if (cfg->engine != EVR_ENGINE_STREAMING && cfg->convergence_tol <= 0 && ctx->H >= 2 &&
       ctx->W >= 2) {
-    const bool ok = ctx->prec == EVR_PREC_F64 ? resident_plan<double>(ctx)
-                                              : resident_plan<float>(ctx);
+    const bool ok = ctx->prec == EVR_PREC_F64 ? resident_plan<double>(ctx, true, cfg->engine == EVR_ENGINE_RESIDENT_GMEM)
+                                              : resident_plan<float>(ctx, true, cfg->engine == EVR_ENGINE_RESIDENT_GMEM);
     if (ok) {
-      ctx->engine = EVR_ENGINE_RESIDENT;
+      ctx->engine = ctx->r_ms == PLANES_SMEM ? EVR_ENGINE_RESIDENT : EVR_ENGINE_RESIDENT_GMEM;
       int rc = ctx->prec == EVR_PREC_F64 ? resident_alloc<double>(ctx) : resident_alloc<float>(ctx);
       if (rc) return rc;
     } else if (cfg->engine == EVR_ENGINE_RESIDENT) {
@@ -827,7 +830,7 @@ int evr_packet_begin(evr_ctx* ctx, const evr_event* events, int64_t n, double wi
   if ((rc = require_config(ctx))) return rc;
   if (n <= 0 || !events) return fail(ctx, EVR_ERR_INVALID, "empty packet");
   if ((rc = stage_host_packet(ctx, events, n, window))) return rc;
-  if (ctx->engine == EVR_ENGINE_RESIDENT) {
+  if (ctx->engine >= EVR_ENGINE_RESIDENT) {
     // the resident kernel fuses the whole packet; run the streaming
     // surface stage here so the host can look at it between the halves
     int r = ctx->prec == EVR_PREC_F64 ? enqueue_surface<double>(ctx) : enqueue_surface<float>(ctx);
@@ -843,7 +846,7 @@ int evr_packet_solve(evr_ctx* ctx, evr_solve_info* info, double* energy_trace,
   CHECK_CTX();
   int rc;
   if ((rc = require_config(ctx))) return rc;
-  if (solve_needs_host_loop(ctx) || energy_trace || rel_trace || ctx->engine == EVR_ENGINE_RESIDENT) {
+  if (solve_needs_host_loop(ctx) || energy_trace || rel_trace || ctx->engine >= EVR_ENGINE_RESIDENT) {
     rc = ctx->prec == EVR_PREC_F64
              ? solve_host_loop<double>(ctx, ctx->cfg, info, energy_trace, rel_trace, true)
              : solve_host_loop<float>(ctx, ctx->cfg, info, energy_trace, rel_trace, true);

@@ -1,18 +1,19 @@
 // evr_resident.cuh -- the resident engine: ONE persistent kernel per event
-// packet, the whole of process_packet (pipeline.py:142-171) on chip.
+// packet, the whole of process_packet (pipeline.py:142-171) in one launch.
 //
 // Decomposition.  CTA b of a cooperative grid (<= 1 CTA per SM) owns the
-// row band [r0, r1) of the sensor (full width, equal band heights R).  Every
-// per-pixel field of the band lives in shared memory together with one halo
-// row above (r0-1) and one below (r1); global memory is touched only to
-// load the state at the start, to exchange two boundary rows per iteration,
-// and to write the state back at the end.
+// row band [r0, r1) of the sensor (full width, equal band heights).  Every
+// per-pixel field of the band -- plus one halo row above (r0-1) and one
+// below (r1) -- lives in a private frame of planes: in shared memory when
+// the band fits (PLANES_SMEM), otherwise in a per-CTA slice of global
+// memory that stays L1/L2-resident (PLANES_GMEM).  Global memory outside the
+// frame is touched only to load the state at the start, to exchange two
+// boundary rows per iteration, and to write the state back at the end.
 //
 // Thread mapping.  Thread t owns sensor column(s) j = t, t+NT, ... and walks
-// the (at most RM+2) band rows of its column with every input gathered into
+// its column's band rows CH at a time, every input of a chunk gathered into
 // registers first, so the rows' float64 div/sqrt chains are independent
-// instructions the scheduler can overlap (ILP = band height) instead of
-// sequential passes.
+// instructions the scheduler overlaps (ILP = CH).
 //
 // One neighbour exchange per iteration.  Each iteration recomputes on its
 // halo rows what it would otherwise have to wait for a second time
@@ -57,6 +58,7 @@ template <class T> struct ResArgs {
   T *u, *p1, *p2, *p3;           // state planes (global)
   T *t, *tx, *ty, *G, *sg;       // surface / metric planes (global, debug view)
   T* xchg;                       // tagged boundary words [2][nb][2][3][W][1|2]
+  T* frames;                     // PLANES_GMEM: per-CTA plane frames
   unsigned long long* flags;     // [nb] release/acquire progress words
   double* part;                  // [2*nb] rel_change partials
   unsigned* ticket;              // last-CTA election for the final sum
@@ -69,7 +71,7 @@ template <class T> struct ResArgs {
   T tau, sigma, tl, tv_step, shrink, t_scaleT, uminT, umaxT;
 };
 
-// plane indices in shared memory
+// plane indices of a CTA's frame
 enum : int {
   RP_U = 0, RP_P1, RP_P2, RP_P3, RP_A11, RP_A12, RP_A22, RP_A31, RP_A32, RP_SG, RP_FB, RP_V,
   RP_QX, RP_QY, RP_COUNT,
@@ -79,12 +81,15 @@ enum : int {
   RP_F64 = RP_V
 };
 
+enum : int { PLANES_SMEM = 0, PLANES_GMEM = 1 };
+
 __host__ __device__ inline int resident_plane_stride(int R, int W) {
   return ((R + 2) * W + 3) / 4 * 4;
 }
 
-template <class T> __host__ __device__ inline size_t resident_smem_bytes(int R, int W) {
-  return (size_t)resident_plane_stride(R, W) * RP_COUNT * sizeof(T) + 64 * sizeof(double);
+// bytes of one CTA's frame of planes
+template <class T> __host__ __device__ inline size_t resident_frame_bytes(int R, int W) {
+  return (size_t)resident_plane_stride(R, W) * RP_COUNT * sizeof(T);
 }
 
 __device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* p) {
@@ -130,11 +135,16 @@ template <> struct LLWords<double> {
   }
 };
 
-// one element global -> shared, asynchronous (LDGSTS)
-template <class T> __device__ __forceinline__ void cp_async_elem(T* dst, const T* src) {
-  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
-  asm volatile("cp.async.ca.shared.global [%0], [%1], %2;" ::"r"(d), "l"(src), "n"(sizeof(T))
-               : "memory");
+// one element global -> frame; asynchronous (LDGSTS) when the frame is
+// shared memory
+template <int MS, class T> __device__ __forceinline__ void copy_in(T* dst, const T* src) {
+  if (MS == PLANES_SMEM) {
+    const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], %2;" ::"r"(d), "l"(src), "n"(sizeof(T))
+                 : "memory");
+  } else {
+    *dst = *src;
+  }
 }
 
 struct Band {
@@ -149,13 +159,16 @@ struct Band {
   }
 };
 
-// Local rows lr = 0 .. RM+1 of a column (lr = global row - r0 + 1); the
-// loops are fully unrolled, the runtime band [lo, hi] masks them.
-#define EVR_ROWS(r) _Pragma("unroll") for (int r = 0; r < RM + 2; ++r)
+// Chunks of CH local rows (lr = global row - r0 + 1) of [lo, hi]; inside a
+// chunk k = 0..CH-1 is fully unrolled and row rb+k exists iff rb+k <= hi.
+#define EVR_CHUNKS(rb, lo, hi) for (int rb = (lo); rb <= (hi); rb += CH)
+#define EVR_K(k) _Pragma("unroll") for (int k = 0; k < CH; ++k)
+#define EVR_K1(k) _Pragma("unroll") for (int k = 0; k <= CH; ++k)
 
-template <class T, int NT, int RM>
+template <class T, int NT, int CH, int MS>
 __global__ void __launch_bounds__(NT, 1) k_resident(const ResArgs<T> a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ double red[64];
   const int tid = threadIdx.x;
   const int b = blockIdx.x;
   const int H = a.H, W = a.W;
@@ -167,7 +180,8 @@ __global__ void __launch_bounds__(NT, 1) k_resident(const ResArgs<T> a) {
   const int lo_halo = has_up ? 0 : 1;
   const int hi_halo = has_dn ? Rb + 1 : Rb;
   const size_t PS = (size_t)resident_plane_stride(a.R, W);
-  T* pl = reinterpret_cast<T*>(smem_raw);
+  T* pl = MS == PLANES_SMEM ? reinterpret_cast<T*>(smem_raw)
+                            : a.frames + (size_t)b * RP_COUNT * PS;
   T* const U = pl + RP_U * PS;
   T* const P1 = pl + RP_P1 * PS;
   T* const P2 = pl + RP_P2 * PS;
@@ -189,7 +203,6 @@ __global__ void __launch_bounds__(NT, 1) k_resident(const ResArgs<T> a) {
   T* const TPY = pl + RP_TPY * PS;
   T* const TD = QY;  // denoised surface (TV-L1 end .. metric), QY idle then
   double* const F64 = reinterpret_cast<double*>(pl + RP_F64 * PS);
-  double* const red = reinterpret_cast<double*>(pl + RP_COUNT * PS);
 
   const PacketHdr* hdr = a.hdr;
   const evr_event* __restrict__ ev = reinterpret_cast<const evr_event*>(hdr + 1);
@@ -202,7 +215,6 @@ __global__ void __launch_bounds__(NT, 1) k_resident(const ResArgs<T> a) {
   const size_t xside = (size_t)3 * W * NWD;       // words of one side of one CTA
   const size_t xslot = (size_t)a.nb * 2 * xside;  // words of one ping-pong slot
   unsigned long long* const xw = reinterpret_cast<unsigned long long*>(a.xchg);
-  auto in = [&](int r, int lo, int hi) { return r >= lo && r <= hi; };
   auto gk_of = [&](int r, int j) { return (int64_t)(r0 - 1 + r) * W + j; };
 
   // optional phase timeline (diagnostics): globaltimer at phase marks
@@ -298,36 +310,40 @@ __global__ void __launch_bounds__(NT, 1) k_resident(const ResArgs<T> a) {
 
   // ---------------------------------------------------------------- load --
   for (int j = tid; j < W; j += NT) {
-    int64_t rv[RM + 2];
-    double fv[RM + 2];
-    EVR_ROWS(r) {
-      if (!in(r, lo_halo, hi_halo)) continue;
-      const int64_t gk = gk_of(r, j);
-      const int l = r * W + j;
-      // warm-start u, p: asynchronous copies into their (idle until the
-      // solve) planes, in flight during ingest and TV-L1
-      if (r >= 1) cp_async_elem(U + l, a.u + gk);
-      cp_async_elem(P1 + l, a.p1 + gk);
-      cp_async_elem(P2 + l, a.p2 + gk);
-      cp_async_elem(P3 + l, a.p3 + gk);
-      rv[r] = a.manifold ? a.raw[gk] : 0;
-      fv[r] = r >= 1 ? a.f[gk] : 0.0;
-    }
-    EVR_ROWS(r) {
-      if (!in(r, lo_halo, hi_halo)) continue;
-      const int l = r * W + j;
-      if (a.manifold) {
-        const T v = (T)normalize_at((double)rv[r], now, a.t_scale, window);
-        T0[l] = v;
-        TU[l] = v;
-        TUB[l] = v;
-        TPX[l] = T(0);
-        TPY[l] = T(0);
+    EVR_CHUNKS(rb, lo_halo, hi_halo) {
+      int64_t rv[CH];
+      double fv[CH];
+      EVR_K(k) {
+        const int r = rb + k;
+        if (r > hi_halo) continue;
+        const int64_t gk = gk_of(r, j);
+        const int l = r * W + j;
+        // warm-start u, p into their planes (idle until the solve); async
+        // for shared frames, in flight during ingest and TV-L1
+        if (r >= 1) copy_in<MS>(U + l, a.u + gk);
+        copy_in<MS>(P1 + l, a.p1 + gk);
+        copy_in<MS>(P2 + l, a.p2 + gk);
+        copy_in<MS>(P3 + l, a.p3 + gk);
+        rv[k] = a.manifold ? a.raw[gk] : 0;
+        fv[k] = r >= 1 ? a.f[gk] : 0.0;
       }
-      if (r >= 1) F64[l] = fv[r];
+      EVR_K(k) {
+        const int r = rb + k;
+        if (r > hi_halo) continue;
+        const int l = r * W + j;
+        if (a.manifold) {
+          const T v = (T)normalize_at((double)rv[k], now, a.t_scale, window);
+          T0[l] = v;
+          TU[l] = v;
+          TUB[l] = v;
+          TPX[l] = T(0);
+          TPY[l] = T(0);
+        }
+        if (r >= 1) F64[l] = fv[k];
+      }
     }
   }
-  asm volatile("cp.async.commit_group;" ::: "memory");
+  if (MS == PLANES_SMEM) asm volatile("cp.async.commit_group;" ::: "memory");
   __syncthreads();
 
   // -------------------------------------------------------------- ingest --
@@ -364,53 +380,61 @@ __global__ void __launch_bounds__(NT, 1) k_resident(const ResArgs<T> a) {
       mark();
       // dual ascent + projection (surface.py:168-183), own rows + halo above
       for (int j = tid; j < W; j += NT) {
-        T ub[RM + 2], ubr[RM + 2], px[RM + 2], py[RM + 2];
-        EVR_ROWS(r) {
-          const int l = r * W + j;
-          if (in(r, lo_halo, hi_halo)) ub[r] = TUB[l];
-          if (in(r, lo_halo, Rb)) {
-            ubr[r] = j < W - 1 ? TUB[l + 1] : T(0);
-            px[r] = TPX[l];
-            py[r] = TPY[l];
+        EVR_CHUNKS(rb, lo_halo, Rb) {
+          T ub[CH + 1], ubr[CH], px[CH], py[CH];
+          EVR_K1(k) {
+            if (rb + k <= hi_halo) ub[k] = TUB[(rb + k) * W + j];
           }
-        }
-        EVR_ROWS(r) {
-          if (!in(r, lo_halo, Rb)) continue;
-          const T dx = j < W - 1 ? ubr[r] - ub[r] : T(0);
-          const T dy = r0 - 1 + r < H - 1 ? ub[r < RM + 1 ? r + 1 : r] - ub[r] : T(0);
-          tv_dual_step(dx, dy, a.tv_step, px[r], py[r]);
-        }
-        EVR_ROWS(r) {
-          if (!in(r, lo_halo, Rb)) continue;
-          TPX[r * W + j] = px[r];
-          TPY[r * W + j] = py[r];
+          EVR_K(k) {
+            const int l = (rb + k) * W + j;
+            if (rb + k > Rb) continue;
+            ubr[k] = j < W - 1 ? TUB[l + 1] : T(0);
+            px[k] = TPX[l];
+            py[k] = TPY[l];
+          }
+          EVR_K(k) {
+            const int r = rb + k;
+            if (r > Rb) continue;
+            const T dx = j < W - 1 ? ubr[k] - ub[k] : T(0);
+            const T dy = r0 - 1 + r < H - 1 ? ub[k + 1] - ub[k] : T(0);
+            tv_dual_step(dx, dy, a.tv_step, px[k], py[k]);
+          }
+          EVR_K(k) {
+            if (rb + k > Rb) continue;
+            TPX[(rb + k) * W + j] = px[k];
+            TPY[(rb + k) * W + j] = py[k];
+          }
         }
       }
       __syncthreads();
       // primal + L1 shrink (surface.py:185-193), own rows; boundary rows go
       // out to the neighbours as soon as they are computed
       for (int j = tid; j < W; j += NT) {
-        T pxc[RM + 2], pxl[RM + 2], pyc[RM + 2], tu[RM + 2], t0[RM + 2];
-        EVR_ROWS(r) {
-          const int l = r * W + j;
-          if (in(r, lo_halo, Rb)) pyc[r] = TPY[l];
-          if (in(r, 1, Rb)) {
-            pxc[r] = TPX[l];
-            pxl[r] = j > 0 ? TPX[l - 1] : T(0);
-            tu[r] = TU[l];
-            t0[r] = T0[l];
+        EVR_CHUNKS(rb, 1, Rb) {
+          T pyc[CH + 1], pxc[CH], pxl[CH], tu[CH], t0[CH];  // pyc[k] = row rb-1+k
+          EVR_K1(k) {
+            const int r = rb - 1 + k;
+            if (r >= lo_halo && r <= Rb) pyc[k] = TPY[r * W + j];
           }
-        }
-        EVR_ROWS(r) {
-          if (!in(r, 1, Rb)) continue;
-          const int gi = r0 - 1 + r;
-          const T d = div_at(pxc[r], pxl[r], pyc[r], gi > 0 ? pyc[r - 1 >= 0 ? r - 1 : 0] : T(0),
-                             gi, j, H, W);
-          T ub;
-          const T un = tv_primal_step(d, tu[r], t0[r], a.tv_step, a.shrink, ub);
-          TU[r * W + j] = un;
-          TUB[r * W + j] = ub;
-          if (pub) ll_put(step + 1, r, j, 0, ub);
+          EVR_K(k) {
+            const int l = (rb + k) * W + j;
+            if (rb + k > Rb) continue;
+            pxc[k] = TPX[l];
+            pxl[k] = j > 0 ? TPX[l - 1] : T(0);
+            tu[k] = TU[l];
+            t0[k] = T0[l];
+          }
+          EVR_K(k) {
+            const int r = rb + k;
+            if (r > Rb) continue;
+            const int gi = r0 - 1 + r;
+            const T d = div_at(pxc[k], pxl[k], pyc[k + 1], gi > 0 ? pyc[k] : T(0), gi, j, H, W);
+            T ub;
+            const T un = tv_primal_step(d, tu[k], t0[k], a.tv_step, a.shrink, ub);
+            TU[r * W + j] = un;
+            TUB[r * W + j] = ub;
+            if (pub) ll_put(step + 1, r, j, 0, ub);
+          }
         }
       }
       // no barrier: the next fetch only writes halo rows of u_bar, which
@@ -419,14 +443,12 @@ __global__ void __launch_bounds__(NT, 1) k_resident(const ResArgs<T> a) {
     }
     __syncthreads();
     // np.clip(u, 0, t_scale) (surface.py:195) -> global t and the TD plane
-    for (int j = tid; j < W; j += NT) {
-      EVR_ROWS(r) {
-        if (!in(r, 1, Rb)) continue;
+    for (int j = tid; j < W; j += NT)
+      for (int r = 1; r <= Rb; ++r) {
         const T td = vclip(TU[r * W + j], T(0), a.t_scaleT);
         a.t[gk_of(r, j)] = td;
         TD[r * W + j] = td;
       }
-    }
   }
   // all rows of the denoised surface this band's metric reads are final
   const int s_met = a.tv_iters + 1;
@@ -439,15 +461,14 @@ __global__ void __launch_bounds__(NT, 1) k_resident(const ResArgs<T> a) {
     }
   }
   step = s_met;
-  asm volatile("cp.async.wait_all;" ::: "memory");  // warm-start u, p landed
+  if (MS == PLANES_SMEM) asm volatile("cp.async.wait_all;" ::: "memory");  // warm start landed
   __syncthreads();
 
   mark();
   // ------------------------------------------------------------ metric ---
   // compute_metric + coeffs (surface.py:81-90, :199-205), solver constants
-  for (int j = tid; j < W; j += NT) {
-    EVR_ROWS(r) {
-      if (!in(r, lo_halo, hi_halo)) continue;
+  for (int j = tid; j < W; j += NT)
+    for (int r = lo_halo; r <= hi_halo; ++r) {
       const int l = r * W + j;
       const int gi = r0 - 1 + r;
       T gx = T(0), gy = T(0);
@@ -474,18 +495,15 @@ __global__ void __launch_bounds__(NT, 1) k_resident(const ResArgs<T> a) {
         a.sg[gk] = s;
       }
     }
-  }
   __syncthreads();  // F64 (aliasing V / QX) and TD (QY) are dead from here on
-  for (int j = tid; j < W; j += NT) {
-    EVR_ROWS(r) {
-      if (!in(r, lo_halo, hi_halo)) continue;
+  for (int j = tid; j < W; j += NT)
+    for (int r = lo_halo; r <= hi_halo; ++r) {
       const int l = r * W + j;
       T qx, qy;
       q_of(Coef<T>{A11[l], A12[l], A22[l], A31[l], A32[l]}, P1[l], P2[l], P3[l], qx, qy);
       QX[l] = qx;
       QY[l] = qy;
     }
-  }
   __syncthreads();
 
   // ------------------------------------------------------- primal-dual ---
@@ -498,31 +516,35 @@ __global__ void __launch_bounds__(NT, 1) k_resident(const ResArgs<T> a) {
     mark();
     // KL prox + over-relaxation (solve.py:234-252), own rows + halo below
     for (int j = tid; j < W; j += NT) {
-      T qxc[RM + 2], qxl[RM + 2], qyc[RM + 2], uu[RM + 2], sgv[RM + 2], fbv[RM + 2];
-      EVR_ROWS(r) {
-        const int l = r * W + j;
-        if (in(r, lo_halo, hi_halo)) qyc[r] = QY[l];
-        if (in(r, 1, hi_halo)) {
-          qxc[r] = QX[l];
-          qxl[r] = j > 0 ? QX[l - 1] : T(0);
-          uu[r] = U[l];
-          sgv[r] = SG[l];
-          fbv[r] = FB[l];
+      EVR_CHUNKS(rb, 1, hi_halo) {
+        T qyc[CH + 1], qxc[CH], qxl[CH], uu[CH], sgv[CH], fbv[CH];  // qyc[k] = row rb-1+k
+        EVR_K1(k) {
+          const int r = rb - 1 + k;
+          if (r >= lo_halo && r <= hi_halo) qyc[k] = QY[r * W + j];
         }
-      }
-      EVR_ROWS(r) {
-        if (!in(r, 1, hi_halo)) continue;
-        const int gi = r0 - 1 + r;
-        const T d = div_at(qxc[r], qxl[r], qyc[r], gi > 0 ? qyc[r - 1 >= 0 ? r - 1 : 0] : T(0),
-                           gi, j, H, W);
-        const T uk = uu[r];
-        const T nu = kl_primal(d, uk, a.tl * sgv[r], fbv[r], a.tau, a.uminT, a.umaxT);
-        V[r * W + j] = nu * T(2) - uk;
-        U[r * W + j] = nu;
-        if (last && r <= Rb) {
-          const double e = (double)nu - (double)uk;
-          rd += e * e;
-          ro += (double)uk * (double)uk;
+        EVR_K(k) {
+          const int l = (rb + k) * W + j;
+          if (rb + k > hi_halo) continue;
+          qxc[k] = QX[l];
+          qxl[k] = j > 0 ? QX[l - 1] : T(0);
+          uu[k] = U[l];
+          sgv[k] = SG[l];
+          fbv[k] = FB[l];
+        }
+        EVR_K(k) {
+          const int r = rb + k;
+          if (r > hi_halo) continue;
+          const int gi = r0 - 1 + r;
+          const T d = div_at(qxc[k], qxl[k], qyc[k + 1], gi > 0 ? qyc[k] : T(0), gi, j, H, W);
+          const T uk = uu[k];
+          const T nu = kl_primal(d, uk, a.tl * sgv[k], fbv[k], a.tau, a.uminT, a.umaxT);
+          V[r * W + j] = nu * T(2) - uk;
+          U[r * W + j] = nu;
+          if (last && r <= Rb) {
+            const double e = (double)nu - (double)uk;
+            rd += e * e;
+            ro += (double)uk * (double)uk;
+          }
         }
       }
     }
@@ -531,40 +553,45 @@ __global__ void __launch_bounds__(NT, 1) k_resident(const ResArgs<T> a) {
     // dual ascent + ball projection (solve.py:170-201), own rows; refresh q;
     // boundary rows go out to the neighbours as soon as they are computed
     for (int j = tid; j < W; j += NT) {
-      T vv[RM + 2], vr[RM + 2], p1[RM + 2], p2[RM + 2], p3[RM + 2], sgv[RM + 2];
-      Coef<T> c[RM + 2];
-      EVR_ROWS(r) {
-        const int l = r * W + j;
-        if (in(r, 1, hi_halo)) vv[r] = V[l];
-        if (in(r, 1, Rb)) {
-          vr[r] = j < W - 1 ? V[l + 1] : T(0);
-          p1[r] = P1[l];
-          p2[r] = P2[l];
-          p3[r] = P3[l];
-          sgv[r] = SG[l];
-          c[r] = Coef<T>{A11[l], A12[l], A22[l], A31[l], A32[l]};
+      EVR_CHUNKS(rb, 1, Rb) {
+        T vv[CH + 1], vr[CH], p1[CH], p2[CH], p3[CH], sgv[CH];  // vv[k] = row rb+k
+        Coef<T> c[CH];
+        EVR_K1(k) {
+          if (rb + k <= hi_halo) vv[k] = V[(rb + k) * W + j];
         }
-      }
-      EVR_ROWS(r) {
-        if (!in(r, 1, Rb)) continue;
-        const T gx = j < W - 1 ? vr[r] - vv[r] : T(0);
-        const T gy = r0 - 1 + r < H - 1 ? vv[r < RM + 1 ? r + 1 : r] - vv[r] : T(0);
-        dual_step(c[r], a.sigma, gx, gy, sgv[r], p1[r], p2[r], p3[r]);
-      }
-      EVR_ROWS(r) {
-        if (!in(r, 1, Rb)) continue;
-        const int l = r * W + j;
-        P1[l] = p1[r];
-        P2[l] = p2[r];
-        P3[l] = p3[r];
-        T qx, qy;
-        q_of(c[r], p1[r], p2[r], p3[r], qx, qy);
-        QX[l] = qx;
-        QY[l] = qy;
-        if (!last) {
-          ll_put(step + 1, r, j, 0, p1[r]);
-          ll_put(step + 1, r, j, 1, p2[r]);
-          ll_put(step + 1, r, j, 2, p3[r]);
+        EVR_K(k) {
+          const int l = (rb + k) * W + j;
+          if (rb + k > Rb) continue;
+          vr[k] = j < W - 1 ? V[l + 1] : T(0);
+          p1[k] = P1[l];
+          p2[k] = P2[l];
+          p3[k] = P3[l];
+          sgv[k] = SG[l];
+          c[k] = Coef<T>{A11[l], A12[l], A22[l], A31[l], A32[l]};
+        }
+        EVR_K(k) {
+          const int r = rb + k;
+          if (r > Rb) continue;
+          const T gx = j < W - 1 ? vr[k] - vv[k] : T(0);
+          const T gy = r0 - 1 + r < H - 1 ? vv[k + 1] - vv[k] : T(0);
+          dual_step(c[k], a.sigma, gx, gy, sgv[k], p1[k], p2[k], p3[k]);
+        }
+        EVR_K(k) {
+          const int r = rb + k;
+          if (r > Rb) continue;
+          const int l = r * W + j;
+          P1[l] = p1[k];
+          P2[l] = p2[k];
+          P3[l] = p3[k];
+          T qx, qy;
+          q_of(c[k], p1[k], p2[k], p3[k], qx, qy);
+          QX[l] = qx;
+          QY[l] = qy;
+          if (!last) {
+            ll_put(step + 1, r, j, 0, p1[k]);
+            ll_put(step + 1, r, j, 1, p2[k]);
+            ll_put(step + 1, r, j, 2, p3[k]);
+          }
         }
       }
     }
@@ -583,9 +610,8 @@ __global__ void __launch_bounds__(NT, 1) k_resident(const ResArgs<T> a) {
 
   // ---------------------------------------------------------- epilogue ---
   // state.u = u+, state.p, state.f = copy(u+) (pipeline.py:167-170)
-  for (int j = tid; j < W; j += NT) {
-    EVR_ROWS(r) {
-      if (!in(r, 1, Rb)) continue;
+  for (int j = tid; j < W; j += NT)
+    for (int r = 1; r <= Rb; ++r) {
       const int l = r * W + j;
       const int64_t gk = gk_of(r, j);
       const T v = U[l];
@@ -595,7 +621,6 @@ __global__ void __launch_bounds__(NT, 1) k_resident(const ResArgs<T> a) {
       a.p2[gk] = P2[l];
       a.p3[gk] = P3[l];
     }
-  }
 
   // rel_change = |u+ - u| / max(|u|, 1e-30) (solve.py:246-249): fixed-order
   // block tree, per-CTA partials, last CTA folds them in index order
@@ -627,6 +652,8 @@ __global__ void __launch_bounds__(NT, 1) k_resident(const ResArgs<T> a) {
   }
 }
 
-#undef EVR_ROWS
+#undef EVR_CHUNKS
+#undef EVR_K
+#undef EVR_K1
 
 }  // namespace evr

@@ -40,7 +40,7 @@ STREAMS = {
                               evr.Thresholds(0.2, 0.1)),
 }
 
-ENGINES = ["streaming", "resident"]
+ENGINES = ["streaming", "resident", "resident_gmem"]
 
 
 def device_state(d, cfg, precision=0, engine=None):
@@ -56,7 +56,7 @@ def device_state(d, cfg, precision=0, engine=None):
 
 
 def engine_id(name):
-    return {"streaming": 1, "resident": 2}[name]
+    return {"streaming": 1, "resident": 2, "resident_gmem": 3}[name]
 
 
 @pytest.mark.parametrize("engine", ENGINES)
@@ -261,5 +261,6 @@ def test_engines_agree_bitwise():
             _, frame, _ = evr.process_packet(st, pk, evr.ManifoldConfig(), evr.SolverConfig(),
                                              evr.Thresholds())
         res[eng] = (frame.copy(), st.p.copy(), st.engine())
-    assert np.array_equal(res["streaming"][0], res["resident"][0])
-    assert np.array_equal(res["streaming"][1], res["resident"][1])
+    for eng in ENGINES[1:]:
+        assert np.array_equal(res["streaming"][0], res[eng][0]), eng
+        assert np.array_equal(res["streaming"][1], res[eng][1]), eng
