@@ -755,8 +755,12 @@ int evr_set_config(evr_ctx* ctx, const evr_config* cfg) {
   ctx->engine = EVR_ENGINE_STREAMING;
   if (cfg->engine != EVR_ENGINE_STREAMING && cfg->convergence_tol <= 0 && ctx->H >= 2 &&
       ctx->W >= 2) {
-    const bool ok = ctx->prec == EVR_PREC_F64 ? resident_plan<double>(ctx, true, cfg->engine == EVR_ENGINE_RESIDENT_GMEM)
-                                              : resident_plan<float>(ctx, true, cfg->engine == EVR_ENGINE_RESIDENT_GMEM);
+    // AUTO / RESIDENT: shared-memory frames or nothing (measured: for
+    // sensors beyond SMEM the streaming engine beats global frames, see
+    // profiles/r01_summary.md); RESIDENT_GMEM forces global frames.
+    const bool gmem = cfg->engine == EVR_ENGINE_RESIDENT_GMEM;
+    const bool ok = ctx->prec == EVR_PREC_F64 ? resident_plan<double>(ctx, gmem, gmem)
+                                              : resident_plan<float>(ctx, gmem, gmem);
     if (ok) {
       ctx->engine = ctx->r_ms == PLANES_SMEM ? EVR_ENGINE_RESIDENT : EVR_ENGINE_RESIDENT_GMEM;
       int rc = ctx->prec == EVR_PREC_F64 ? resident_alloc<double>(ctx) : resident_alloc<float>(ctx);
