@@ -161,6 +161,30 @@ int64_t evr_launch_count(const evr_ctx *ctx);
  * copy up to n words of it to out (may be NULL). */
 int evr_debug_timeline(evr_ctx *ctx, int enable, uint64_t *out, int64_t n);
 
+/* ---- event text front-end (host only, no device) ------------------------ */
+/* Text event parser: the grammar and validation of parse_event_line /
+ * read_stream (events.py:65-130) straight into packed events.  `st` carries
+ * the 1-based line number, the event index and the running maximum
+ * timestamp across calls (zero-initialise it for a new stream).  Parsing
+ * stops at the end of `text`, after `cap` events, or at the first invalid
+ * line: then EVR_ERR_INVALID, *err_kind = EVR_PARSE_BAD_LINE (malformed,
+ * negative or out-of-sensor: the reference's EventParseError) or
+ * EVR_PARSE_ORDER (timestamp below running_max - slack: StreamOrderError),
+ * *err_offset = byte offset of that line, `st` as before that line.
+ * *consumed = bytes of whole lines consumed. */
+enum { EVR_PARSE_OK = 0, EVR_PARSE_BAD_LINE = 1, EVR_PARSE_ORDER = 2 };
+typedef struct {
+    int64_t line_no;
+    int64_t index;
+    int64_t running_max;
+    int32_t have_max;
+    int32_t _pad;
+} evr_parse_state;
+int evr_parse_events(const char *text, int64_t len, int width, int height,
+                     int64_t slack, evr_parse_state *st, evr_event *out,
+                     int64_t cap, int64_t *n_out, int64_t *consumed,
+                     int64_t *err_offset, int32_t *err_kind);
+
 /* ---- operator-level API on host arrays of the context's shape ----------- */
 /* grad_x / grad_y (surface.py:93-104) */
 int evr_op_grad(evr_ctx *ctx, const double *u, double *gx, double *gy);
@@ -206,6 +230,10 @@ int evr_op_pd_solve(evr_ctx *ctx, const evr_config *cfg, const double *f,
                     const double *p_init, double *u_out, double *p_out,
                     evr_solve_info *info, double *energy_trace,
                     double *rel_trace);
+/* to_gray (pgm.py:14-22): floor(255*(image-lo)/(hi-lo) + 0.5) clipped to
+ * [0, 255], uint8 (H, W) */
+int evr_op_to_gray(evr_ctx *ctx, const double *image, double lo, double hi,
+                   uint8_t *out);
 /* rof_manifold_solve (solve.py:264-293) */
 int evr_op_rof_solve(evr_ctx *ctx, const double *f, const double *tx,
                      const double *ty, const double *G, const double *sqrtG,

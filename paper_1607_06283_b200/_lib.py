@@ -98,6 +98,7 @@ _SIGNATURES = {
     "evr_get_frame_u8": ([_P, _d, _d, _P], _i32),
     "evr_event_buffer": ([_P, _i64, _P], _i32),
     "evr_debug_timeline": ([_P, _i32, _P, _i64], _i32),
+    "evr_parse_events": ([_P, _i64, _i32, _i32, _i64, _P, _P, _i64, _P, _P, _P, _P], _i32),
     "evr_stream": ([_P], _P),
     "evr_launch_count": ([_P], _i64),
     "evr_op_grad": ([_P, _P, _P, _P], _i32),
@@ -112,6 +113,7 @@ _SIGNATURES = {
     "evr_op_prox_dual": ([_P, _P, _P, _P], _i32),
     "evr_op_energy": ([_P, _P, _P, _P, _P, _P, _P, _d, _P], _i32),
     "evr_op_pd_solve": ([_P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P], _i32),
+    "evr_op_to_gray": ([_P, _P, _d, _d, _P], _i32),
     "evr_op_rof_solve": ([_P, _P, _P, _P, _P, _P, _d, _i32, _P], _i32),
 }
 

@@ -1209,6 +1209,18 @@ int evr_op_pd_solve(evr_ctx* ctx, const evr_config* cfg, const double* f, const 
   return d2h_sync(ctx, p_out, ctx->aos_a, 3 * B);
 }
 
+int evr_op_to_gray(evr_ctx* ctx, const double* image, double lo, double hi, uint8_t* out) {
+  OP_PROLOGUE(false);
+  if (!(hi > lo)) return fail(ctx, EVR_ERR_INVALID, "bounds must satisfy u_min < u_max");
+  int rc;
+  if ((rc = h2d(ctx, ctx->fld<double>(F_T), image, B))) return rc;
+  uint8_t* d = reinterpret_cast<uint8_t*>(ctx->aos_a);
+  k_to_gray<double><<<grid1d(N), kNT, 0, s>>>(ctx->fld<double>(F_T), lo, hi, d, N);
+  ctx->launches += 1;
+  if ((rc = launch_err(ctx, "to_gray"))) return rc;
+  return d2h_sync(ctx, out, d, (size_t)N);
+}
+
 int evr_op_rof_solve(evr_ctx* ctx, const double* f, const double* tx, const double* ty, const double* G,
                      const double* sqrtG, double lam, int iterations, double* u_out) {
   OP_PROLOGUE(true);

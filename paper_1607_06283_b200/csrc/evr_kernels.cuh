@@ -385,9 +385,9 @@ template <class T>
 __global__ void k_to_gray(const T* __restrict__ u, double lo, double hi, uint8_t* out, int64_t N) {
   const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= N) return;
-  double s = ((double)u[k] - lo) / (hi - lo);
-  s = floor(s * 255.0 + 0.5);
-  out[k] = (uint8_t)vclip(s, 0.0, 255.0);
+  // scaled = 255.0 * (image - u_min) / (u_max - u_min), left to right
+  const double s = 255.0 * ((double)u[k] - lo) / (hi - lo);
+  out[k] = (uint8_t)vclip(floor(s + 0.5), 0.0, 255.0);
 }
 
 // ------------------------------------------------- operator kernels --

@@ -227,6 +227,44 @@ def main():
     ops["rof_h"] = hr
     ops["rof_steep"] = so.rof_manifold_solve(f, mr, 4.0, 120)
     np.savez_compressed(os.path.join(OUT, "ops.npz"), **ops)
+
+    # 5. text event front-end (events.py:65-130) and gray mapping (pgm.py:14-22)
+    import json
+
+    cases = {
+        "clean": ("# hdr\n0 1 2 1\n5 3 4 0\n\n5 0 0 -1\n", 8, 6, 0),
+        "crlf_and_signs": ("1 +2 3 1\r\n2 1_0 0 0\r\n3\t4   5 -1\n", 16, 8, 0),
+        "slack_ok": ("10 1 1 1\n8 1 1 1\n12 0 0 0\n", 4, 4, 3),
+        "slack_fail": ("10 1 1 1\n8 1 1 1\n6 0 0 0\n", 4, 4, 3),
+        "order": ("5 1 1 1\n4 1 1 1\n", 4, 4, 0),
+        "bounds": ("1 1 1 1\n2 9 0 1\n", 8, 8, 0),
+        "fields": ("1 1 1\n", 4, 4, 0),
+        "token": ("1 1 x 1\n", 4, 4, 0),
+        "neg_t": ("-1 1 1 1\n", 4, 4, 0),
+        "neg_xy": ("1 -1 1 1\n", 4, 4, 0),
+        "polarity": ("1 1 1 2\n", 4, 4, 0),
+        "comment_only": ("# a\n   # b\n\n", 4, 4, 0),
+    }
+    out_cases = {}
+    for name, (text, w, h, slack) in cases.items():
+        geom = ev.SensorGeometry(width=w, height=h)
+        rec = {"text": text, "width": w, "height": h, "slack": slack}
+        try:
+            evs = ev.events_from_text(text, geom, slack=slack)
+            rec["events"] = [[e.timestamp, e.x, e.y, e.polarity] for e in evs]
+        except Exception as exc:  # the reference's own error
+            rec["error"] = type(exc).__name__
+            rec["message"] = str(exc)
+            rec["line_no"] = getattr(exc, "line_no", None)
+            rec["index"] = getattr(exc, "index", None)
+        out_cases[name] = rec
+    with open(os.path.join(OUT, "events_cases.json"), "w") as fh:
+        json.dump(out_cases, fh, indent=1)
+    pgm = sys.modules["evrecon.pgm"]
+    img = np.concatenate([1.0 + (np.arange(256) + 0.5) / 255.0, 1.0 + np.arange(256) / 255.0,
+                          rng.uniform(0.5, 2.5, 512)]).reshape(32, 32)
+    np.savez_compressed(os.path.join(OUT, "gray.npz"), image=img,
+                        gray=pgm.to_gray(img, (1.0, 2.0)))
     for name in sorted(os.listdir(OUT)):
         if name.endswith(".npz"):
             print(name, os.path.getsize(os.path.join(OUT, name)))
