@@ -157,13 +157,14 @@ def dist_init(args):
     return world, rank, local
 
 
-def allmax(x, world):
+def allmax(x, world, device="cuda"):
+    """Max over ranks (the job's time is its slowest rank's)."""
     if world == 1:
         return x
     import torch
     import torch.distributed as dist
 
-    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    t = torch.tensor([x], dtype=torch.float64, device=device)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 

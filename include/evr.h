@@ -161,6 +161,31 @@ int64_t evr_launch_count(const evr_ctx *ctx);
  * copy up to n words of it to out (may be NULL). */
 int evr_debug_timeline(evr_ctx *ctx, int enable, uint64_t *out, int64_t n);
 
+/* ---- row-band groups: one sensor over several contexts / GPUs ------------ */
+/* The megapixel configuration (BASELINE configs[4]): the
+ * sensor's rows are split into n_bands contiguous bands, band b on
+ * devices[b] (NULL: all on device 0); every packet runs the streaming step
+ * list on all bands in lock step with one halo row exchanged per half-step
+ * over peer copies (NVLink between GPUs).  Bit-identical to evr_ctx. */
+typedef struct evr_group evr_group;
+int evr_group_create(evr_group **out, int n_bands, const int *devices,
+                     int height, int width, int precision);
+void evr_group_destroy(evr_group *grp);
+const char *evr_group_last_error(const evr_group *grp);
+int evr_group_band(evr_group *grp, int b, int *y0, int *y1, int *device);
+int evr_group_set_config(evr_group *grp, const evr_config *cfg);
+int evr_group_init_state(evr_group *grp);
+/* full-sensor host arrays, as evr_set_state / evr_get_state */
+int evr_group_set_state(evr_group *grp, const double *u, const double *f,
+                        const int64_t *raw, const double *p);
+int evr_group_get_state(evr_group *grp, double *u, double *f, int64_t *raw,
+                        double *p);
+/* process_packet (pipeline.py:142-171) over all bands; synchronous */
+int evr_group_process_packet(evr_group *grp, const evr_event *events,
+                             int64_t n, double window, evr_solve_info *info);
+int evr_group_get_frame(evr_group *grp, double *u_out);
+int64_t evr_group_launch_count(const evr_group *grp);
+
 /* ---- event text front-end (host only, no device) ------------------------ */
 /* Text event parser: the grammar and validation of parse_event_line /
  * read_stream (events.py:65-130) straight into packed events.  `st` carries

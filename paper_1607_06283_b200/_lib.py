@@ -98,6 +98,17 @@ _SIGNATURES = {
     "evr_get_frame_u8": ([_P, _d, _d, _P], _i32),
     "evr_event_buffer": ([_P, _i64, _P], _i32),
     "evr_debug_timeline": ([_P, _i32, _P, _i64], _i32),
+    "evr_group_create": ([_P, _i32, _P, _i32, _i32, _i32], _i32),
+    "evr_group_destroy": ([_P], None),
+    "evr_group_last_error": ([_P], ctypes.c_char_p),
+    "evr_group_band": ([_P, _i32, _P, _P, _P], _i32),
+    "evr_group_set_config": ([_P, _P], _i32),
+    "evr_group_init_state": ([_P], _i32),
+    "evr_group_set_state": ([_P, _P, _P, _P, _P], _i32),
+    "evr_group_get_state": ([_P, _P, _P, _P, _P], _i32),
+    "evr_group_process_packet": ([_P, _P, _i64, _d, _P], _i32),
+    "evr_group_get_frame": ([_P, _P], _i32),
+    "evr_group_launch_count": ([_P], _i64),
     "evr_parse_events": ([_P, _i64, _i32, _i32, _i64, _P, _P, _i64, _P, _P, _P, _P], _i32),
     "evr_stream": ([_P], _P),
     "evr_launch_count": ([_P], _i64),

@@ -76,10 +76,20 @@ struct evr_ctx {
   void* d_xchg = nullptr;                 // boundary-row ping-pong buffer
   unsigned* d_ticket = nullptr;
   unsigned long long* d_trace = nullptr;  // optional resident phase timeline
+  // band geometry: local plane rows [0, H) are global rows row0 + [0, H);
+  // own rows [own_lo, own_hi]; a whole-sensor context owns all its rows
+  int row0 = 0, Htot = 0, own_lo = 0, own_hi = -1;
+  bool banded = false;
   std::string err;
 
   template <class T> T* fld(int k) const { return reinterpret_cast<T*>(slab + field_stride * k); }
   PacketHdr* hdr() const { return reinterpret_cast<PacketHdr*>(d_stage); }
+  Geo geo(int ilo, int ihi) const { return Geo{W, row0, Htot, ilo, ihi}; }
+  Geo geo_own() const { return geo(own_lo, own_hi); }
+  // the metric also covers the halo row above (its q feeds the first row)
+  Geo geo_metric() const { return geo(banded && row0 + own_lo > 0 ? own_lo - 1 : own_lo, own_hi); }
+  int64_t own_off() const { return (int64_t)own_lo * W; }
+  int64_t own_n() const { return (int64_t)(own_hi - own_lo + 1) * W; }
 };
 
 namespace {
@@ -111,6 +121,7 @@ int fail(evr_ctx* c, int code, const char* fmt, ...) {
   } while (0)
 
 inline dim3 grid2d(const evr_ctx* c) { return dim3((c->W + 31) / 32, (c->H + 7) / 8); }
+inline dim3 grid_geo(const Geo& g) { return dim3((g.W + 31) / 32, (g.ihi - g.ilo + 1 + 7) / 8); }
 inline dim3 block2d() { return dim3(32, 8); }
 inline unsigned grid1d(int64_t n) { return (unsigned)((n + kNT - 1) / kNT); }
 inline int red_blocks(int64_t n) {
@@ -130,112 +141,126 @@ template <class T> CoefPlanes<T> coefs(const evr_ctx* c) {
 
 // ---- per-packet sequence (streaming engine) -------------------------------
 
-// banded ordered ingest: ~2 CTAs per SM, each owning a block of rows
+// banded ordered ingest: ~2 CTAs per SM, each owning a block of own rows
 void launch_ingest(evr_ctx* ctx) {
-  const int rows_per = std::max(1, (ctx->H + 295) / 296);
-  const int nb = (ctx->H + rows_per - 1) / rows_per;
+  const int nrows = ctx->own_hi - ctx->own_lo + 1;
+  const int rows_per = std::max(1, (nrows + 295) / 296);
+  const int nb = (nrows + rows_per - 1) / rows_per;
   const evr_config& g = ctx->cfg;
-  k_ingest<kIngestNT><<<nb, kIngestNT, 0, ctx->stream>>>(ctx->hdr(), ctx->f, ctx->raw, ctx->H,
-                                                        ctx->W, rows_per, g.c_pos, g.c_neg,
-                                                        g.u_min, g.u_max, ctx->d_err);
+  k_ingest<kIngestNT><<<nb, kIngestNT, 0, ctx->stream>>>(
+      ctx->hdr(), ctx->f + ctx->own_off(), ctx->raw + ctx->own_off(), ctx->Htot, ctx->W,
+      ctx->row0 + ctx->own_lo, nrows, rows_per, g.c_pos, g.c_neg, g.u_min, g.u_max, ctx->d_err);
 }
 
-// ingest -> normalize -> TV-L1 -> metric (+ solver constants)
-template <class T> int enqueue_surface(evr_ctx* ctx) {
-  const evr_config& g = ctx->cfg;
-  cudaStream_t s = ctx->stream;
-  const int H = ctx->H, W = ctx->W;
-  const int64_t N = ctx->N;
-  launch_ingest(ctx);
-  int n = 1;
-  if (g.manifold_enabled) {
-    T *t = ctx->fld<T>(F_T), *tu = ctx->fld<T>(F_TU), *tub = ctx->fld<T>(F_TUB);
-    T *px = ctx->fld<T>(F_TPX), *py = ctx->fld<T>(F_TPY);
-    k_normalize_tvinit<T><<<grid1d(N), kNT, 0, s>>>(ctx->raw, ctx->hdr(), g.t_scale, t, tu, tub,
-                                                    px, py, N);
-    const double step = 1.0 / std::sqrt(8.0);  // surface.py:158
-    const T sigma = (T)step, tau = (T)step, shrink = (T)(step * g.denoise_weight);
-    for (int it = 0; it < g.denoise_iterations; ++it) {
-      k_tv_dual<T><<<grid2d(ctx), block2d(), 0, s>>>(tub, px, py, H, W, sigma);
-      k_tv_primal<T><<<grid2d(ctx), block2d(), 0, s>>>(px, py, tu, tub, t, H, W, tau, shrink);
+// The per-packet sequence of the streaming engine as a list of steps, one
+// launch each (evr_group runs the same list on every band in lock step and
+// exchanges halo rows between steps).
+enum StepKind {
+  ST_INGEST, ST_NORM, ST_TVD, ST_TVP, ST_TVFIN, ST_METRIC, ST_PDP, ST_REL, ST_PDD, ST_EPI
+};
+struct Step {
+  int kind, it;
+};
+
+// which: 0 = surface (ingest .. metric), 1 = solve (primal-dual + epilogue), 2 = both
+std::vector<Step> packet_steps(const evr_config& g, int which) {
+  std::vector<Step> v;
+  if (which != 1) {
+    v.push_back({ST_INGEST, 0});
+    if (g.manifold_enabled) {
+      v.push_back({ST_NORM, 0});
+      for (int k = 0; k < g.denoise_iterations; ++k) {
+        v.push_back({ST_TVD, k});
+        v.push_back({ST_TVP, k});
+      }
+      v.push_back({ST_TVFIN, 0});
     }
-    k_tv_finish<T><<<grid1d(N), kNT, 0, s>>>(tu, t, (T)g.t_scale, N);
-    n += 2 + 2 * g.denoise_iterations;
+    v.push_back({ST_METRIC, 0});
   }
-  k_metric_setup<T><<<grid2d(ctx), block2d(), 0, s>>>(
-      ctx->fld<T>(F_T), ctx->f, ctx->fld<T>(F_TX), ctx->fld<T>(F_TY), ctx->fld<T>(F_G),
-      ctx->fld<T>(F_SG), coefs<T>(ctx), ctx->fld<T>(F_BETA), ctx->fld<T>(F_FB), H, W,
-      (T)(g.tau * g.lam), g.manifold_enabled ? 0 : 1);
-  n += 1;
-  int rc = launch_err(ctx, "surface");
-  return rc ? rc : n;
-}
-
-// one KL primal-dual iteration: u (in `cur`) -> u+ (in `nxt`), p updated
-template <class T> void pd_iteration(evr_ctx* ctx, T* cur, T* nxt) {
-  const evr_config& g = ctx->cfg;
-  cudaStream_t s = ctx->stream;
-  T* v = ctx->fld<T>(F_V);
-  k_pd_primal<T><<<grid2d(ctx), block2d(), 0, s>>>(
-      ctx->fld<T>(F_P1), ctx->fld<T>(F_P2), ctx->fld<T>(F_P3), coefs<T>(ctx), cur,
-      ctx->fld<T>(F_BETA), ctx->fld<T>(F_FB), nxt, v, ctx->H, ctx->W, (T)g.tau, (T)g.u_min,
-      (T)g.u_max);
-  k_pd_dual<T><<<grid2d(ctx), block2d(), 0, s>>>(v, ctx->fld<T>(F_P1), ctx->fld<T>(F_P2),
-                                                 ctx->fld<T>(F_P3), coefs<T>(ctx),
-                                                 ctx->fld<T>(F_SG), ctx->H, ctx->W,
-                                                 (T)g.sigma);
+  if (which != 0) {
+    for (int k = 0; k < g.max_iterations; ++k) {
+      v.push_back({ST_PDP, k});
+      if (k == g.max_iterations - 1) v.push_back({ST_REL, k});
+      v.push_back({ST_PDD, k});
+    }
+    v.push_back({ST_EPI, 0});
+  }
+  return v;
 }
 
 template <class T> void relchange(evr_ctx* ctx, const T* un, const T* u, int iterations) {
-  const int nb = red_blocks(ctx->N);
-  k_relchange_partial<T, kNT><<<nb, kNT, 0, ctx->stream>>>(un, u, ctx->N, ctx->part);
-  k_relchange_final<kNT><<<1, kNT, 0, ctx->stream>>>(ctx->part, nb, ctx->d_info, iterations);
+  const int nb = red_blocks(ctx->own_n());
+  k_relchange_partial<T, kNT><<<nb, kNT, 0, ctx->stream>>>(un + ctx->own_off(), u + ctx->own_off(),
+                                                          ctx->own_n(), ctx->part);
+  k_relchange_final<kNT><<<1, kNT, 0, ctx->stream>>>(ctx->part, nb, ctx->d_info, iterations,
+                                                    ctx->d_scalar + 2);
 }
 
-// fixed-iteration solve (convergence_tol == 0) + epilogue, graph-capturable
-template <class T> int enqueue_solve(evr_ctx* ctx) {
-  const int iters = ctx->cfg.max_iterations;
+// launches of one step (returns the kernel count)
+template <class T> int launch_step(evr_ctx* ctx, const Step& st) {
+  const evr_config& g = ctx->cfg;
+  cudaStream_t s = ctx->stream;
+  const Geo own = ctx->geo_own();
+  const int64_t off = ctx->own_off(), n = ctx->own_n();
+  const double step = 1.0 / std::sqrt(8.0);  // surface.py:158
+  T *t = ctx->fld<T>(F_T), *tu = ctx->fld<T>(F_TU), *tub = ctx->fld<T>(F_TUB);
+  T *px = ctx->fld<T>(F_TPX), *py = ctx->fld<T>(F_TPY);
   T* bufs[2] = {ctx->fld<T>(F_U), ctx->fld<T>(F_UN)};
-  int n = 0;
-  for (int it = 0; it < iters; ++it) {
-    T* cur = bufs[it & 1];
-    T* nxt = bufs[(it + 1) & 1];
-    if (it == iters - 1) {
-      // rel_change needs u_old and u+ both alive: run the primal, reduce, dual
-      const evr_config& g = ctx->cfg;
-      T* v = ctx->fld<T>(F_V);
-      k_pd_primal<T><<<grid2d(ctx), block2d(), 0, ctx->stream>>>(
-          ctx->fld<T>(F_P1), ctx->fld<T>(F_P2), ctx->fld<T>(F_P3), coefs<T>(ctx), cur,
-          ctx->fld<T>(F_BETA), ctx->fld<T>(F_FB), nxt, v, ctx->H, ctx->W, (T)g.tau,
-          (T)g.u_min, (T)g.u_max);
-      relchange<T>(ctx, nxt, cur, iters);
-      k_pd_dual<T><<<grid2d(ctx), block2d(), 0, ctx->stream>>>(
-          v, ctx->fld<T>(F_P1), ctx->fld<T>(F_P2), ctx->fld<T>(F_P3), coefs<T>(ctx),
-          ctx->fld<T>(F_SG), ctx->H, ctx->W, (T)g.sigma);
-      n += 4;
-    } else {
-      pd_iteration<T>(ctx, cur, nxt);
-      n += 2;
+  switch (st.kind) {
+    case ST_INGEST:
+      launch_ingest(ctx);
+      return 1;
+    case ST_NORM:
+      k_normalize_tvinit<T><<<grid1d(n), kNT, 0, s>>>(ctx->raw + off, ctx->hdr(), g.t_scale,
+                                                      t + off, tu + off, tub + off, px + off,
+                                                      py + off, n);
+      return 1;
+    case ST_TVD:
+      k_tv_dual<T><<<grid_geo(own), block2d(), 0, s>>>(tub, px, py, own, (T)step);
+      return 1;
+    case ST_TVP:
+      k_tv_primal<T><<<grid_geo(own), block2d(), 0, s>>>(px, py, tu, tub, t, own, (T)step,
+                                                         (T)(step * g.denoise_weight));
+      return 1;
+    case ST_TVFIN:
+      k_tv_finish<T><<<grid1d(n), kNT, 0, s>>>(tu + off, t + off, (T)g.t_scale, n);
+      return 1;
+    case ST_METRIC: {
+      const Geo mg = ctx->geo_metric();
+      k_metric_setup<T><<<grid_geo(mg), block2d(), 0, s>>>(
+          t, ctx->f, ctx->fld<T>(F_TX), ctx->fld<T>(F_TY), ctx->fld<T>(F_G), ctx->fld<T>(F_SG),
+          coefs<T>(ctx), ctx->fld<T>(F_BETA), ctx->fld<T>(F_FB), mg, (T)(g.tau * g.lam),
+          g.manifold_enabled ? 0 : 1);
+      return 1;
+    }
+    case ST_PDP:
+      k_pd_primal<T><<<grid_geo(own), block2d(), 0, s>>>(
+          ctx->fld<T>(F_P1), ctx->fld<T>(F_P2), ctx->fld<T>(F_P3), coefs<T>(ctx),
+          bufs[st.it & 1], ctx->fld<T>(F_BETA), ctx->fld<T>(F_FB), bufs[(st.it + 1) & 1],
+          ctx->fld<T>(F_V), own, (T)g.tau, (T)g.u_min, (T)g.u_max);
+      return 1;
+    case ST_REL:
+      relchange<T>(ctx, bufs[(st.it + 1) & 1], bufs[st.it & 1], st.it + 1);
+      return 2;
+    case ST_PDD:
+      k_pd_dual<T><<<grid_geo(own), block2d(), 0, s>>>(
+          ctx->fld<T>(F_V), ctx->fld<T>(F_P1), ctx->fld<T>(F_P2), ctx->fld<T>(F_P3),
+          coefs<T>(ctx), ctx->fld<T>(F_SG), own, (T)g.sigma);
+      return 1;
+    case ST_EPI: {
+      T* last = bufs[g.max_iterations & 1];
+      k_epilogue<T><<<grid1d(n), kNT, 0, s>>>(last + off, ctx->fld<T>(F_U) + off, ctx->f + off, n);
+      return 1;
     }
   }
-  T* last = bufs[iters & 1];
-  k_epilogue<T><<<grid1d(ctx->N), kNT, 0, ctx->stream>>>(last, ctx->fld<T>(F_U), ctx->f, ctx->N);
-  n += 1;
-  int rc = launch_err(ctx, "solve");
-  return rc ? rc : n;
+  return 0;
 }
 
 template <class T> int enqueue_packet(evr_ctx* ctx, int which) {
-  int n = 0, r;
-  if (which == 0 || which == 2) {
-    if ((r = enqueue_surface<T>(ctx)) < 0) return r;
-    n += r;
-  }
-  if (which == 1 || which == 2) {
-    if ((r = enqueue_solve<T>(ctx)) < 0) return r;
-    n += r;
-  }
-  return n;
+  int n = 0;
+  for (const Step& st : packet_steps(ctx->cfg, which)) n += launch_step<T>(ctx, st);
+  int rc = launch_err(ctx, "packet");
+  return rc ? rc : n;
 }
 
 // ---- resident engine glue ---------------------------------------------------
@@ -499,19 +524,19 @@ int solve_host_loop(evr_ctx* ctx, const evr_config& g, evr_solve_info* info, dou
     T* cur = bufs[cur_i];
     T* nxt = bufs[cur_i ^ 1];
     T* v = ctx->fld<T>(F_V);
-    k_pd_primal<T><<<grid2d(ctx), block2d(), 0, ctx->stream>>>(
+    const Geo own = ctx->geo_own();
+    k_pd_primal<T><<<grid_geo(own), block2d(), 0, ctx->stream>>>(
         ctx->fld<T>(F_P1), ctx->fld<T>(F_P2), ctx->fld<T>(F_P3), coefs<T>(ctx), cur,
-        ctx->fld<T>(F_BETA), ctx->fld<T>(F_FB), nxt, v, ctx->H, ctx->W, (T)g.tau, (T)g.u_min,
-        (T)g.u_max);
+        ctx->fld<T>(F_BETA), ctx->fld<T>(F_FB), nxt, v, own, (T)g.tau, (T)g.u_min, (T)g.u_max);
     iterations = it + 1;
     ctx->launches += 1;
     if (track || it == g.max_iterations - 1) {
       relchange<T>(ctx, nxt, cur, iterations);
       ctx->launches += 2;
     }
-    k_pd_dual<T><<<grid2d(ctx), block2d(), 0, ctx->stream>>>(
+    k_pd_dual<T><<<grid_geo(own), block2d(), 0, ctx->stream>>>(
         v, ctx->fld<T>(F_P1), ctx->fld<T>(F_P2), ctx->fld<T>(F_P3), coefs<T>(ctx),
-        ctx->fld<T>(F_SG), ctx->H, ctx->W, (T)g.sigma);
+        ctx->fld<T>(F_SG), own, (T)g.sigma);
     ctx->launches += 1;
     cur_i ^= 1;
     if (etrace) {
@@ -583,20 +608,22 @@ int require_stencil(evr_ctx* ctx) {
   return EVR_OK;
 }
 
+// State I/O covers the context's own rows (all rows of a whole-sensor
+// context; a band's rows without its halos).
 template <class T> int set_state_t(evr_ctx* ctx, const double* u, const double* f,
                                    const int64_t* raw, const double* p) {
-  const int64_t N = ctx->N;
+  const int64_t N = ctx->own_n(), o = ctx->own_off();
   cudaStream_t s = ctx->stream;
   if (u) {
     CK(cudaMemcpyAsync(ctx->aos_a, u, sizeof(double) * N, cudaMemcpyHostToDevice, s));
-    k_convert<double, T><<<grid1d(N), kNT, 0, s>>>(ctx->aos_a, ctx->fld<T>(F_U), N);
+    k_convert<double, T><<<grid1d(N), kNT, 0, s>>>(ctx->aos_a, ctx->fld<T>(F_U) + o, N);
   }
-  if (f) CK(cudaMemcpyAsync(ctx->f, f, sizeof(double) * N, cudaMemcpyHostToDevice, s));
-  if (raw) CK(cudaMemcpyAsync(ctx->raw, raw, sizeof(int64_t) * N, cudaMemcpyHostToDevice, s));
+  if (f) CK(cudaMemcpyAsync(ctx->f + o, f, sizeof(double) * N, cudaMemcpyHostToDevice, s));
+  if (raw) CK(cudaMemcpyAsync(ctx->raw + o, raw, sizeof(int64_t) * N, cudaMemcpyHostToDevice, s));
   if (p) {
     CK(cudaMemcpyAsync(ctx->aos_b, p, sizeof(double) * 3 * N, cudaMemcpyHostToDevice, s));
-    k_aos_to_planes<T><<<grid1d(N), kNT, 0, s>>>(ctx->aos_b, ctx->fld<T>(F_P1), ctx->fld<T>(F_P2),
-                                                 ctx->fld<T>(F_P3), N);
+    k_aos_to_planes<T><<<grid1d(N), kNT, 0, s>>>(ctx->aos_b, ctx->fld<T>(F_P1) + o,
+                                                 ctx->fld<T>(F_P2) + o, ctx->fld<T>(F_P3) + o, N);
   }
   int rc = launch_err(ctx, "set_state");
   if (rc) return rc;
@@ -605,17 +632,17 @@ template <class T> int set_state_t(evr_ctx* ctx, const double* u, const double* 
 }
 
 template <class T> int get_state_t(evr_ctx* ctx, double* u, double* f, int64_t* raw, double* p) {
-  const int64_t N = ctx->N;
+  const int64_t N = ctx->own_n(), o = ctx->own_off();
   cudaStream_t s = ctx->stream;
   if (u) {
-    k_convert<T, double><<<grid1d(N), kNT, 0, s>>>(ctx->fld<T>(F_U), ctx->aos_a, N);
+    k_convert<T, double><<<grid1d(N), kNT, 0, s>>>(ctx->fld<T>(F_U) + o, ctx->aos_a, N);
     CK(cudaMemcpyAsync(u, ctx->aos_a, sizeof(double) * N, cudaMemcpyDeviceToHost, s));
   }
-  if (f) CK(cudaMemcpyAsync(f, ctx->f, sizeof(double) * N, cudaMemcpyDeviceToHost, s));
-  if (raw) CK(cudaMemcpyAsync(raw, ctx->raw, sizeof(int64_t) * N, cudaMemcpyDeviceToHost, s));
+  if (f) CK(cudaMemcpyAsync(f, ctx->f + o, sizeof(double) * N, cudaMemcpyDeviceToHost, s));
+  if (raw) CK(cudaMemcpyAsync(raw, ctx->raw + o, sizeof(int64_t) * N, cudaMemcpyDeviceToHost, s));
   if (p) {
-    k_planes_to_aos<T><<<grid1d(N), kNT, 0, s>>>(ctx->fld<T>(F_P1), ctx->fld<T>(F_P2),
-                                                 ctx->fld<T>(F_P3), ctx->aos_b, N);
+    k_planes_to_aos<T><<<grid1d(N), kNT, 0, s>>>(ctx->fld<T>(F_P1) + o, ctx->fld<T>(F_P2) + o,
+                                                 ctx->fld<T>(F_P3) + o, ctx->aos_b, N);
     CK(cudaMemcpyAsync(p, ctx->aos_b, sizeof(double) * 3 * N, cudaMemcpyDeviceToHost, s));
   }
   int rc = launch_err(ctx, "get_state");
@@ -625,10 +652,9 @@ template <class T> int get_state_t(evr_ctx* ctx, double* u, double* f, int64_t* 
 }
 
 template <class T> int get_plane_t(evr_ctx* ctx, int field, double* out) {
-  k_convert<T, double><<<grid1d(ctx->N), kNT, 0, ctx->stream>>>(ctx->fld<T>(field), ctx->aos_a,
-                                                                ctx->N);
-  CK(cudaMemcpyAsync(out, ctx->aos_a, sizeof(double) * ctx->N, cudaMemcpyDeviceToHost,
-                     ctx->stream));
+  const int64_t N = ctx->own_n(), o = ctx->own_off();
+  k_convert<T, double><<<grid1d(N), kNT, 0, ctx->stream>>>(ctx->fld<T>(field) + o, ctx->aos_a, N);
+  CK(cudaMemcpyAsync(out, ctx->aos_a, sizeof(double) * N, cudaMemcpyDeviceToHost, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
   return launch_err(ctx, "get_plane");
 }
@@ -674,6 +700,10 @@ int evr_create(evr_ctx** out, int device, int height, int width, int precision) 
   ctx->W = width;
   ctx->N = (int64_t)height * width;
   ctx->prec = precision;
+  ctx->row0 = 0;
+  ctx->Htot = height;
+  ctx->own_lo = 0;
+  ctx->own_hi = height - 1;
   auto bail = [&](int rc) {
     std::string msg = ctx->err;
     evr_destroy(ctx);
@@ -837,7 +867,7 @@ int evr_packet_begin(evr_ctx* ctx, const evr_event* events, int64_t n, double wi
   if (ctx->engine >= EVR_ENGINE_RESIDENT) {
     // the resident kernel fuses the whole packet; run the streaming
     // surface stage here so the host can look at it between the halves
-    int r = ctx->prec == EVR_PREC_F64 ? enqueue_surface<double>(ctx) : enqueue_surface<float>(ctx);
+    int r = ctx->prec == EVR_PREC_F64 ? enqueue_packet<double>(ctx, 0) : enqueue_packet<float>(ctx, 0);
     if (r < 0) return r;
     ctx->launches += r;
     return EVR_OK;
@@ -1051,8 +1081,8 @@ int evr_op_denoise(evr_ctx* ctx, const double* t_in, double weight, int iteratio
   CK(cudaMemsetAsync(py, 0, B, s));
   const double step = 1.0 / std::sqrt(8.0);
   for (int it = 0; it < iterations; ++it) {
-    k_tv_dual<double><<<grid2d(ctx), block2d(), 0, s>>>(tub, px, py, ctx->H, ctx->W, step);
-    k_tv_primal<double><<<grid2d(ctx), block2d(), 0, s>>>(px, py, tu, tub, t, ctx->H, ctx->W, step,
+    k_tv_dual<double><<<grid2d(ctx), block2d(), 0, s>>>(tub, px, py, ctx->geo_own(), step);
+    k_tv_primal<double><<<grid2d(ctx), block2d(), 0, s>>>(px, py, tu, tub, t, ctx->geo_own(), step,
                                                           step * weight);
   }
   k_tv_finish<double><<<grid1d(N), kNT, 0, s>>>(tu, tub, t_scale, N);
@@ -1242,14 +1272,312 @@ int evr_op_rof_solve(evr_ctx* ctx, const double* f, const double* tx, const doub
     double* v = ctx->fld<double>(F_V);
     k_rof_primal<double><<<grid2d(ctx), block2d(), 0, s>>>(
         ctx->fld<double>(F_P1), ctx->fld<double>(F_P2), ctx->fld<double>(F_P3), coefs<double>(ctx),
-        cur, ctx->fld<double>(F_BETA), ctx->fld<double>(F_FB), nxt, v, ctx->H, ctx->W, step);
+        cur, ctx->fld<double>(F_BETA), ctx->fld<double>(F_FB), nxt, v, ctx->geo_own(), step);
     k_pd_dual<double><<<grid2d(ctx), block2d(), 0, s>>>(v, ctx->fld<double>(F_P1), ctx->fld<double>(F_P2),
                                                         ctx->fld<double>(F_P3), coefs<double>(ctx),
-                                                        ctx->fld<double>(F_SG), ctx->H, ctx->W, step);
+                                                        ctx->fld<double>(F_SG), ctx->geo_own(), step);
   }
   ctx->launches += 1 + 2 * (int64_t)iterations;
   if ((rc = launch_err(ctx, "rof"))) return rc;
   return d2h_sync(ctx, u_out, bufs[iterations & 1], B);
+}
+
+}  // extern "C"
+
+// =========================================================================
+// evr_group: one sensor split into row bands over several contexts (one per
+// GPU, or several on one GPU), the megapixel configuration of SURVEY.md
+// 8(e).  Every band runs the streaming step list in lock step; after each
+// step the boundary rows its neighbours need travel as device-to-device
+// (peer, over NVLink between GPUs) copies ordered by CUDA events:
+//   after NORM / TVP : u_bar  of a band's first row -> the band above's halo below
+//   after TVD        : py     of a band's last row  -> the band below's halo above
+//   after TVFIN      : t      both ways (the metric's ty and the halo-row q)
+//   after METRIC/PDD : p1..p3 of a band's last row  -> the band below's halo above
+//   after PDP        : v      of a band's first row -> the band above's halo below
+// No reduction happens inside the iterations; rel_change folds the bands'
+// partial sums on the host.  Every boundary rule uses global row indices,
+// so the result is bit-identical to the single-context run.
+// =========================================================================
+struct evr_group {
+  int n = 0, H = 0, W = 0, prec = EVR_PREC_F64;
+  std::vector<evr_ctx*> band;
+  std::vector<int> y0;
+  std::vector<cudaEvent_t> done, copied;
+  evr_config cfg{};
+  bool cfg_set = false;
+  std::string err;
+};
+
+namespace {
+
+int gfail(evr_group* g, int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  if (g) g->err = buf;
+  return code;
+}
+
+#define GCK(call)                                                                      \
+  do {                                                                                 \
+    cudaError_t e_ = (call);                                                           \
+    if (e_ != cudaSuccess)                                                             \
+      return gfail(grp, EVR_ERR_CUDA, "%s failed: %s", #call, cudaGetErrorString(e_)); \
+  } while (0)
+
+#define GBAND(b, rc_expr)                                                              \
+  do {                                                                                 \
+    int rc_ = (rc_expr);                                                               \
+    if (rc_) return gfail(grp, rc_, "band %d: %s", (b), grp->band[b]->err.c_str());   \
+  } while (0)
+
+// copy one row of `field` (T elements) from band src local row rs into band
+// dst local row rd, on dst's stream after src's last step
+int copy_row(evr_group* grp, int dst, int rd, int src, int rs, int field) {
+  evr_ctx* D = grp->band[dst];
+  evr_ctx* S = grp->band[src];
+  const size_t es = grp->prec == EVR_PREC_F64 ? 8 : 4;
+  char* dp = D->slab + D->field_stride * field + (size_t)rd * grp->W * es;
+  const char* sp = S->slab + S->field_stride * field + (size_t)rs * grp->W * es;
+  GCK(cudaSetDevice(D->device));
+  GCK(cudaStreamWaitEvent(D->stream, grp->done[src], 0));
+  GCK(cudaMemcpyPeerAsync(dp, D->device, sp, S->device, grp->W * es, D->stream));
+  return EVR_OK;
+}
+
+// halo exchanges that follow a step (see the table above)
+int exchange_after(evr_group* grp, int kind) {
+  const int n = grp->n;
+  auto from_below = [&](int field) -> int {  // first own row of b+1 -> halo below of b
+    for (int b = 0; b + 1 < n; ++b) {
+      int rc = copy_row(grp, b, grp->band[b]->own_hi + 1, b + 1, grp->band[b + 1]->own_lo, field);
+      if (rc) return rc;
+    }
+    return EVR_OK;
+  };
+  auto from_above = [&](int field) -> int {  // last own row of b-1 -> halo above of b
+    for (int b = 1; b < n; ++b) {
+      int rc = copy_row(grp, b, 0, b - 1, grp->band[b - 1]->own_hi, field);
+      if (rc) return rc;
+    }
+    return EVR_OK;
+  };
+  int rc = EVR_OK;
+  switch (kind) {
+    case ST_NORM:
+    case ST_TVP:
+      rc = from_below(F_TUB);
+      break;
+    case ST_TVD:
+      rc = from_above(F_TPY);
+      break;
+    case ST_TVFIN:
+      if (!(rc = from_above(F_T))) rc = from_below(F_T);
+      break;
+    case ST_METRIC:
+    case ST_PDD:
+      for (int f : {F_P1, F_P2, F_P3})
+        if ((rc = from_above(f))) break;
+      break;
+    case ST_PDP:
+      rc = from_below(F_V);
+      break;
+    default:
+      break;
+  }
+  return rc;
+}
+
+template <class T> int group_packet(evr_group* grp) {
+  const std::vector<Step> steps = packet_steps(grp->cfg, 2);
+  const int n = grp->n;
+  for (const Step& st : steps) {
+    for (int b = 0; b < n; ++b) {
+      evr_ctx* ctx = grp->band[b];
+      GCK(cudaSetDevice(ctx->device));
+      // neighbours must have copied this band's rows before it overwrites them
+      if (b > 0) GCK(cudaStreamWaitEvent(ctx->stream, grp->copied[b - 1], 0));
+      if (b + 1 < n) GCK(cudaStreamWaitEvent(ctx->stream, grp->copied[b + 1], 0));
+      ctx->launches += launch_step<T>(ctx, st);
+      GBAND(b, launch_err(ctx, "group step"));
+      GCK(cudaEventRecord(grp->done[b], ctx->stream));
+    }
+    int rc = exchange_after(grp, st.kind);
+    if (rc) return rc;
+    for (int b = 0; b < n; ++b) {
+      GCK(cudaSetDevice(grp->band[b]->device));
+      GCK(cudaEventRecord(grp->copied[b], grp->band[b]->stream));
+    }
+  }
+  return EVR_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int evr_group_create(evr_group** out, int n_bands, const int* devices, int height, int width,
+                     int precision) {
+  if (!out || n_bands < 1 || height < 2 || width < 2 || n_bands > height)
+    return EVR_ERR_INVALID;
+  evr_group* grp = new evr_group();
+  grp->n = n_bands;
+  grp->H = height;
+  grp->W = width;
+  grp->prec = precision;
+  for (int b = 0; b < n_bands; ++b) {
+    const int y0 = (int)((int64_t)height * b / n_bands);
+    const int y1 = (int)((int64_t)height * (b + 1) / n_bands);
+    const int dev = devices ? devices[b] : 0;
+    evr_ctx* ctx = nullptr;
+    int rc = evr_create(&ctx, dev, y1 - y0 + 2, width, precision);
+    if (rc) {
+      evr_group_destroy(grp);
+      return rc;
+    }
+    ctx->banded = true;
+    ctx->row0 = y0 - 1;
+    ctx->Htot = height;
+    ctx->own_lo = 1;
+    ctx->own_hi = y1 - y0;
+    grp->band.push_back(ctx);
+    grp->y0.push_back(y0);
+    cudaSetDevice(dev);
+    cudaEvent_t e1, e2;
+    cudaEventCreateWithFlags(&e1, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&e2, cudaEventDisableTiming);
+    cudaEventRecord(e2, ctx->stream);
+    grp->done.push_back(e1);
+    grp->copied.push_back(e2);
+  }
+  // peer access between neighbouring GPUs (NVLink); same-device bands need none
+  for (int b = 0; b + 1 < n_bands; ++b) {
+    const int d0 = grp->band[b]->device, d1 = grp->band[b + 1]->device;
+    if (d0 == d1) continue;
+    int ok = 0;
+    cudaDeviceCanAccessPeer(&ok, d0, d1);
+    if (ok) {
+      cudaSetDevice(d0);
+      cudaDeviceEnablePeerAccess(d1, 0);
+      cudaSetDevice(d1);
+      cudaDeviceEnablePeerAccess(d0, 0);
+      cudaGetLastError();  // already-enabled is fine
+    }
+  }
+  *out = grp;
+  return EVR_OK;
+}
+
+void evr_group_destroy(evr_group* grp) {
+  if (!grp) return;
+  for (size_t b = 0; b < grp->band.size(); ++b) {
+    cudaSetDevice(grp->band[b]->device);
+    if (b < grp->done.size()) cudaEventDestroy(grp->done[b]);
+    if (b < grp->copied.size()) cudaEventDestroy(grp->copied[b]);
+    evr_destroy(grp->band[b]);
+  }
+  delete grp;
+}
+
+const char* evr_group_last_error(const evr_group* grp) {
+  return grp ? grp->err.c_str() : "null group";
+}
+
+int evr_group_band(evr_group* grp, int b, int* y0, int* y1, int* device) {
+  if (!grp || b < 0 || b >= grp->n) return EVR_ERR_INVALID;
+  if (y0) *y0 = grp->y0[b];
+  if (y1) *y1 = grp->y0[b] + grp->band[b]->own_hi;
+  if (device) *device = grp->band[b]->device;
+  return EVR_OK;
+}
+
+int evr_group_set_config(evr_group* grp, const evr_config* cfg) {
+  if (!grp || !cfg) return EVR_ERR_INVALID;
+  if (cfg->convergence_tol > 0)
+    return gfail(grp, EVR_ERR_UNSUPPORTED, "banded solve runs fixed iterations only");
+  evr_config c = *cfg;
+  c.engine = EVR_ENGINE_STREAMING;
+  for (int b = 0; b < grp->n; ++b) GBAND(b, evr_set_config(grp->band[b], &c));
+  grp->cfg = c;
+  grp->cfg_set = true;
+  return EVR_OK;
+}
+
+int evr_group_init_state(evr_group* grp) {
+  if (!grp) return EVR_ERR_INVALID;
+  for (int b = 0; b < grp->n; ++b) GBAND(b, evr_init_state(grp->band[b]));
+  return EVR_OK;
+}
+
+// full-sensor host arrays; band b reads / writes its own rows
+int evr_group_set_state(evr_group* grp, const double* u, const double* f, const int64_t* raw,
+                        const double* p) {
+  if (!grp) return EVR_ERR_INVALID;
+  for (int b = 0; b < grp->n; ++b) {
+    const int64_t o = (int64_t)grp->y0[b] * grp->W;
+    GBAND(b, evr_set_state(grp->band[b], u ? u + o : nullptr, f ? f + o : nullptr,
+                           raw ? raw + o : nullptr, p ? p + 3 * o : nullptr));
+  }
+  return EVR_OK;
+}
+
+int evr_group_get_state(evr_group* grp, double* u, double* f, int64_t* raw, double* p) {
+  if (!grp) return EVR_ERR_INVALID;
+  for (int b = 0; b < grp->n; ++b) {
+    const int64_t o = (int64_t)grp->y0[b] * grp->W;
+    GBAND(b, evr_get_state(grp->band[b], u ? u + o : nullptr, f ? f + o : nullptr,
+                           raw ? raw + o : nullptr, p ? p + 3 * o : nullptr));
+  }
+  return EVR_OK;
+}
+
+int evr_group_process_packet(evr_group* grp, const evr_event* events, int64_t n, double window,
+                             evr_solve_info* info) {
+  if (!grp) return EVR_ERR_INVALID;
+  if (!grp->cfg_set) return gfail(grp, EVR_ERR_INVALID, "evr_group_set_config has not been called");
+  if (n <= 0 || !events) return gfail(grp, EVR_ERR_INVALID, "empty packet");
+  for (int b = 0; b < grp->n; ++b) {
+    evr_ctx* ctx = grp->band[b];
+    cudaSetDevice(ctx->device);
+    GBAND(b, stage_host_packet(ctx, events, n, window));
+  }
+  int rc = grp->prec == EVR_PREC_F64 ? group_packet<double>(grp) : group_packet<float>(grp);
+  if (rc) return rc;
+  double d = 0.0, o = 0.0;
+  int iters = 0;
+  for (int b = 0; b < grp->n; ++b) {
+    evr_ctx* ctx = grp->band[b];
+    GCK(cudaSetDevice(ctx->device));
+    double sums[2];
+    GCK(cudaMemcpyAsync(sums, ctx->d_scalar + 2, sizeof sums, cudaMemcpyDeviceToHost, ctx->stream));
+    GCK(cudaMemcpyAsync(ctx->h_info, ctx->d_info, sizeof(evr_solve_info), cudaMemcpyDeviceToHost,
+                        ctx->stream));
+    GCK(cudaStreamSynchronize(ctx->stream));
+    GBAND(b, check_err_flag(ctx));
+    d += sums[0];
+    o += sums[1];
+    iters = ctx->h_info->iterations;
+  }
+  if (info) {
+    const double den = std::sqrt(o);
+    info->iterations = iters;
+    info->rel_change = std::sqrt(d) / (den > 1e-30 ? den : 1e-30);
+  }
+  return EVR_OK;
+}
+
+int evr_group_get_frame(evr_group* grp, double* u_out) {
+  return evr_group_get_state(grp, u_out, nullptr, nullptr, nullptr);
+}
+
+int64_t evr_group_launch_count(const evr_group* grp) {
+  int64_t n = 0;
+  if (grp)
+    for (auto* c : grp->band) n += c->launches;
+  return n;
 }
 
 }  // extern "C"

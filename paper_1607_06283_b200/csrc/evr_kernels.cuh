@@ -39,6 +39,22 @@ template <class T> struct CoefPlanes {
   if (i >= H || j >= W) return;                        \
   const int64_t k = (int64_t)i * W + j;
 
+// Rows [ilo, ihi] of a context's planes, local row i being global sensor row
+// row0 + i of a Htot-row sensor.  A whole-sensor context has row0 = 0 and
+// Htot = its height; a band context (evr_group) keeps one halo row above and
+// below its own rows, and every boundary rule of the reference is applied
+// by GLOBAL row index.
+struct Geo {
+  int W, row0, Htot, ilo, ihi;
+};
+#define EVR_GEO_INDEX                                                         \
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;                        \
+  const int i = g.ilo + (int)(blockIdx.y * blockDim.y + threadIdx.y);         \
+  if (i > g.ihi || j >= g.W) return;                                          \
+  const int W = g.W;                                                          \
+  const int gi = g.row0 + i;                                                  \
+  const int64_t k = (int64_t)i * W + j;
+
 // ---------------------------------------------------------------- ingest --
 // apply_event (pipeline.py:114-121) for every event of the packet, bit-exact
 // including duplicates (evr_ingest.cuh): CTA b owns rows
@@ -47,17 +63,18 @@ template <class T> struct CoefPlanes {
 template <int NT>
 __global__ void __launch_bounds__(NT)
 k_ingest(const PacketHdr* __restrict__ hdr, double* __restrict__ f, int64_t* __restrict__ raw,
-         int H, int W, int rows_per, double c_pos, double c_neg, double u_min, double u_max,
-         int* err) {
+         int Htot, int W, int y0, int nrows, int rows_per, double c_pos, double c_neg,
+         double u_min, double u_max, int* err) {
   __shared__ IngestShared<NT> sm;
   // the packet's events follow the header in the staging buffer
   const evr_event* __restrict__ ev = reinterpret_cast<const evr_event*>(hdr + 1);
-  const int row_lo = blockIdx.x * rows_per;
-  const int row_hi = min(H, row_lo + rows_per) - 1;
-  double* fb = f + (int64_t)row_lo * W;
-  int64_t* rb = raw + (int64_t)row_lo * W;
+  // f / raw point at global row y0; this CTA takes global rows [row_lo, row_hi]
+  const int row_lo = y0 + blockIdx.x * rows_per;
+  const int row_hi = min(y0 + nrows, row_lo + rows_per) - 1;
+  double* fb = f + (int64_t)(row_lo - y0) * W;
+  int64_t* rb = raw + (int64_t)(row_lo - y0) * W;
   ordered_ingest<NT>(
-      ev, hdr->n, H, W, row_lo, row_hi, c_pos, c_neg, u_min, u_max, sm,
+      ev, hdr->n, Htot, W, row_lo, row_hi, c_pos, c_neg, u_min, u_max, sm,
       blockIdx.x == 0 ? err : nullptr, [&](int lp) { return fb[lp]; },
       [&](int lp, double v, int64_t t) {
         fb[lp] = v;
@@ -84,11 +101,11 @@ __global__ void k_normalize_tvinit(const int64_t* __restrict__ raw,
 
 // TV-L1 dual half-step (surface.py:168-183)
 template <class T>
-__global__ void k_tv_dual(const T* __restrict__ ub, T* __restrict__ px, T* __restrict__ py,
-                          int H, int W, T sigma) {
-  EVR_2D_INDEX
+__global__ void k_tv_dual(const T* __restrict__ ub, T* __restrict__ px, T* __restrict__ py, Geo g,
+                          T sigma) {
+  EVR_GEO_INDEX
   const T dx = j < W - 1 ? ub[k + 1] - ub[k] : T(0);
-  const T dy = i < H - 1 ? ub[k + W] - ub[k] : T(0);
+  const T dy = gi < g.Htot - 1 ? ub[k + W] - ub[k] : T(0);
   T a = px[k], b = py[k];
   tv_dual_step(dx, dy, sigma, a, b);
   px[k] = a;
@@ -98,10 +115,10 @@ __global__ void k_tv_dual(const T* __restrict__ ub, T* __restrict__ px, T* __res
 // TV-L1 primal half-step (surface.py:185-193)
 template <class T>
 __global__ void k_tv_primal(const T* __restrict__ px, const T* __restrict__ py, T* u, T* ub,
-                            const T* __restrict__ f0, int H, int W, T tau, T shrink) {
-  EVR_2D_INDEX
-  const T d = div_at(px[k], j > 0 ? px[k - 1] : T(0), py[k], i > 0 ? py[k - W] : T(0), i, j,
-                     H, W);
+                            const T* __restrict__ f0, Geo g, T tau, T shrink) {
+  EVR_GEO_INDEX
+  const T d = div_at(px[k], j > 0 ? px[k - 1] : T(0), py[k], gi > 0 ? py[k - W] : T(0), gi, j,
+                     g.Htot, W);
   T ubar;
   const T un = tv_primal_step(d, u[k], f0[k], tau, shrink, ubar);
   u[k] = un;
@@ -121,20 +138,20 @@ __global__ void k_tv_finish(const T* __restrict__ u, T* __restrict__ t, T t_scal
 // (solve.py:227-228).  `flat` gives flat_metric (surface.py:208-211).
 template <class T>
 __global__ void k_metric_setup(const T* __restrict__ t, const double* __restrict__ f, T* tx,
-                               T* ty, T* G, T* sg, CoefPlanes<T> c, T* beta, T* fb, int H,
-                               int W, T tl, int flat) {
-  EVR_2D_INDEX
+                               T* ty, T* G, T* sg, CoefPlanes<T> c, T* beta, T* fb, Geo g,
+                               T tl, int flat) {
+  EVR_GEO_INDEX
   T gx = T(0), gy = T(0);
   if (!flat) {
     gx = j < W - 1 ? t[k + 1] - t[k] : T(0);
-    gy = i < H - 1 ? t[k + W] - t[k] : T(0);
+    gy = gi < g.Htot - 1 ? t[k + W] - t[k] : T(0);
   }
-  const T g = metric_G(gx, gy);
-  const T s = Arith<T>::sqrt(g);
-  const Coef<T> a = coeffs_of(gx, gy, g);
+  const T det = metric_G(gx, gy);
+  const T s = Arith<T>::sqrt(det);
+  const Coef<T> a = coeffs_of(gx, gy, det);
   tx[k] = gx;
   ty[k] = gy;
-  G[k] = g;
+  G[k] = det;
   sg[k] = s;
   c.a11[k] = a.a11;
   c.a12[k] = a.a12;
@@ -179,15 +196,16 @@ __device__ __forceinline__ void q_at(const CoefPlanes<T>& c, const T* p1, const 
   q_of(c.at(k), p1[k], p2[k], p3[k], qx, qy);
 }
 
-// descent point div(A^T p) at (i, j) (solve.py:144-167, without *tau + u)
+// descent point div(A^T p) at global (gi, j) (solve.py:144-167, without
+// *tau + u); the row above is local k - W
 template <class T>
 __device__ __forceinline__ T div_q(const CoefPlanes<T>& c, const T* p1, const T* p2,
-                                   const T* p3, int i, int j, int H, int W, int64_t k) {
+                                   const T* p3, int gi, int j, int Htot, int W, int64_t k) {
   T qx, qy, qxl = T(0), qyu = T(0), dummy;
   q_at(c, p1, p2, p3, k, qx, qy);
   if (j > 0) q_at(c, p1, p2, p3, k - 1, qxl, dummy);
-  if (i > 0) q_at(c, p1, p2, p3, k - W, dummy, qyu);
-  return div_at(qx, qxl, qy, qyu, i, j, H, W);
+  if (gi > 0) q_at(c, p1, p2, p3, k - W, dummy, qyu);
+  return div_at(qx, qxl, qy, qyu, gi, j, Htot, W);
 }
 
 // KL primal half-step + over-relaxation (solve.py:234-252)
@@ -196,9 +214,9 @@ __global__ void k_pd_primal(const T* __restrict__ p1, const T* __restrict__ p2,
                             const T* __restrict__ p3, CoefPlanes<T> c,
                             const T* __restrict__ u, const T* __restrict__ beta,
                             const T* __restrict__ fb, T* __restrict__ un, T* __restrict__ v,
-                            int H, int W, T tau, T umin, T umax) {
-  EVR_2D_INDEX
-  const T d = div_q(c, p1, p2, p3, i, j, H, W, k);
+                            Geo g, T tau, T umin, T umax) {
+  EVR_GEO_INDEX
+  const T d = div_q(c, p1, p2, p3, gi, j, g.Htot, W, k);
   const T uk = u[k];
   const T nu = kl_primal(d, uk, beta[k], fb[k], tau, umin, umax);
   un[k] = nu;
@@ -212,9 +230,9 @@ __global__ void k_rof_primal(const T* __restrict__ p1, const T* __restrict__ p2,
                              const T* __restrict__ p3, CoefPlanes<T> c,
                              const T* __restrict__ u, const T* __restrict__ inv,
                              const T* __restrict__ wf, T* __restrict__ un, T* __restrict__ v,
-                             int H, int W, T tau) {
-  EVR_2D_INDEX
-  const T d = div_q(c, p1, p2, p3, i, j, H, W, k);
+                             Geo g, T tau) {
+  EVR_GEO_INDEX
+  const T d = div_q(c, p1, p2, p3, gi, j, g.Htot, W, k);
   const T uk = u[k];
   const T nu = rof_primal(d, uk, wf[k], inv[k], tau);
   un[k] = nu;
@@ -224,11 +242,11 @@ __global__ void k_rof_primal(const T* __restrict__ p1, const T* __restrict__ p2,
 // dual ascent + ball projection (solve.py:170-201)
 template <class T>
 __global__ void k_pd_dual(const T* __restrict__ v, T* __restrict__ p1, T* __restrict__ p2,
-                          T* __restrict__ p3, CoefPlanes<T> c, const T* __restrict__ sg, int H,
-                          int W, T sigma) {
-  EVR_2D_INDEX
+                          T* __restrict__ p3, CoefPlanes<T> c, const T* __restrict__ sg, Geo g,
+                          T sigma) {
+  EVR_GEO_INDEX
   const T gx = j < W - 1 ? v[k + 1] - v[k] : T(0);
-  const T gy = i < H - 1 ? v[k + W] - v[k] : T(0);
+  const T gy = gi < g.Htot - 1 ? v[k + W] - v[k] : T(0);
   T a = p1[k], b = p2[k], d = p3[k];
   dual_step(c.at(k), sigma, gx, gy, sg[k], a, b, d);
   p1[k] = a;
@@ -275,7 +293,7 @@ k_relchange_partial(const T* __restrict__ un, const T* __restrict__ u, int64_t N
 template <int NT>
 __global__ void __launch_bounds__(NT)
 k_relchange_final(const double* __restrict__ part, int nb, evr_solve_info* info,
-                  int iterations) {
+                  int iterations, double* sums) {
   __shared__ double sh[NT / 32];
   double d = 0.0, o = 0.0;
   for (int b = threadIdx.x; b < nb; b += NT) {
@@ -288,6 +306,8 @@ k_relchange_final(const double* __restrict__ part, int nb, evr_solve_info* info,
     const double den = sqrt(o);
     info->rel_change = sqrt(d) / (den > 1e-30 ? den : 1e-30);
     info->iterations = iterations;
+    sums[0] = d;  // evr_group folds the bands' sums
+    sums[1] = o;
   }
 }
 

@@ -1,0 +1,56 @@
+"""Row-band split (evr_group): bit-identical to the single
+context for any band count, including 1-row bands, uneven splits, flat
+metric and fixed windows.  Bands share GPU 0 here (the driver has one GPU);
+on a multi-GPU node the same copies go over NVLink peer access."""
+
+import numpy as np
+import pytest
+
+import paper_1607_06283_b200 as evr
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+def packets(H, W, n_packets, epp, seed, t_step=1):
+    rng = np.random.default_rng(seed)
+    n = n_packets * epp
+    ev = evr.make_event_array(rng.integers(0, W, n), rng.integers(0, H, n),
+                              rng.choice([-1, 1], n), np.arange(n, dtype=np.int64) * t_step)
+    return [ev[s:s + epp] for s in range(0, n, epp)]
+
+
+@pytest.mark.parametrize("H,W,bands,prec", [(64, 48, 1, 0), (64, 48, 2, 0), (37, 29, 4, 0),
+                                            (5, 17, 5, 0), (130, 96, 3, 0), (64, 48, 3, 1)])
+def test_banded_equals_single_context(H, W, bands, prec):
+    geom = evr.SensorGeometry(W, H)
+    sc = evr.SolverConfig(max_iterations=23)
+    mc = evr.ManifoldConfig(denoise_iterations=11)
+    grp = evr.BandedStream(geom, sc, mc, bands=bands, precision=prec)
+    st = evr.init_state(geom, sc, precision=prec, engine=1)
+    for pk in packets(H, W, 3, 300, seed=H * W + bands):
+        frame, res = grp.process_packet(pk)
+        _, ref, rres = evr.process_packet(st, pk, mc, sc, evr.Thresholds())
+        assert res.iterations == rres.iterations
+        assert np.array_equal(frame, ref)
+        assert res.rel_change == pytest.approx(rres.rel_change, rel=1e-9)
+    assert np.array_equal(grp.p, st.p)
+    assert np.array_equal(grp.raw_timestamps, st.raw_timestamps)
+    assert np.array_equal(grp.f, st.f)
+
+
+def test_banded_flat_and_fixed_window_vs_oracle():
+    H, W = 41, 33
+    geom = evr.SensorGeometry(W, H)
+    for mc, kw in ((evr.ManifoldConfig(enabled=False), dict(manifold_enabled=False)),
+                   (evr.ManifoldConfig(t_window=400.0, denoise_iterations=9),
+                    dict(denoise_iterations=9))):
+        sc = evr.SolverConfig(max_iterations=17)
+        grp = evr.BandedStream(geom, sc, mc, bands=3)
+        ref = O.OracleStream(H, W, O.make_config(max_iterations=17, **kw), t_window=mc.t_window)
+        for pk in packets(H, W, 3, 200, seed=5, t_step=3):
+            frame, res = grp.process_packet(pk)
+            it, _ = ref.process(np.ascontiguousarray(pk))
+            assert res.iterations == it
+            assert np.array_equal(frame, ref.u)
+        assert np.array_equal(grp.p, ref.p)
