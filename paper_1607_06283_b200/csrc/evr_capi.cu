@@ -462,9 +462,9 @@ int ensure_stage(evr_ctx* ctx, int64_t n) {
 
 int validate_events(evr_ctx* ctx, const evr_event* ev, int64_t n) {
   for (int64_t k = 0; k < n; ++k)
-    if (ev[k].x < 0 || ev[k].x >= ctx->W || ev[k].y < 0 || ev[k].y >= ctx->H)
+    if (ev[k].x < 0 || ev[k].x >= ctx->W || ev[k].y < 0 || ev[k].y >= ctx->Htot)
       return fail(ctx, EVR_ERR_RANGE, "event %lld at (%d, %d) outside the %dx%d sensor",
-                  (long long)k, (int)ev[k].x, (int)ev[k].y, ctx->W, ctx->H);
+                  (long long)k, (int)ev[k].x, (int)ev[k].y, ctx->W, ctx->Htot);
   return EVR_OK;
 }
 
