@@ -222,7 +222,7 @@ __global__ void __launch_bounds__(NT, 1) k_resident(const ResArgs<T> a) {
   auto mark = [&]() {
     if (a.trace && tid == 0 && tmark < 256) {
       unsigned long long t;
-      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t)::"memory");
       a.trace[(size_t)b * 256 + tmark] = t;
     }
     ++tmark;
@@ -548,6 +548,7 @@ __global__ void __launch_bounds__(NT, 1) k_resident(const ResArgs<T> a) {
         }
       }
     }
+    mark();  // primal issued (thread 0)
     __syncthreads();
     mark();  // primal done
     // dual ascent + ball projection (solve.py:170-201), own rows; refresh q;

@@ -35,10 +35,13 @@ for r in [rows[0], rows[len(rows) // 2], rows[-1]]:
     m = (tr[r] - t0) / 1e3
     k = 2 + tv  # marks 0, 1, tv x TV, metric, solve-start
     tvd = np.diff(m[1:2 + tv])
-    pdm = m[k + 1:k + 1 + 3 * pd].reshape(pd, 3)
-    fetch = pdm[1:, 0] - pdm[:-1, 2]
-    primal = pdm[:, 1] - pdm[:, 0]
-    dual = pdm[:, 2] - pdm[:, 1]
+    # per PD iteration: fetch done | primal issued (thread 0) | primal done | dual issued
+    pdm = m[k + 2:k + 2 + 4 * pd].reshape(pd, 4)
+    fetch = pdm[1:, 0] - pdm[:-1, 3]
+    primal0 = pdm[:, 1] - pdm[:, 0]
+    pbar = pdm[:, 2] - pdm[:, 1]
+    primal = pdm[:, 2] - pdm[:, 0]
+    dual = pdm[:, 3] - pdm[:, 2]
     print(f"{cfgname} f{'64' if prec == 0 else '32'} CTA {r:3d}: ingest {m[1]-m[0]:.2f} | TV/it {tvd.mean():.2f} "
           f"| metric {m[k] - m[k-1]:.2f} (+{m[k+1]-m[k]:.2f}) | PD/it {np.diff(pdm[:, 0]).mean():.2f} = "
-          f"fetch {fetch.mean():.2f} + primal {primal.mean():.2f} + dual {dual.mean():.2f} | end {m[k+1+3*pd]:.1f} us")
+          f"fetch {fetch.mean():.2f} + primal {primal.mean():.2f} (t0 {primal0.mean():.2f} bar {pbar.mean():.2f}) + dual {dual.mean():.2f} | end {m[k+2+4*pd]:.1f} us")
