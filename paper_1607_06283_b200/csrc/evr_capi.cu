@@ -13,11 +13,13 @@
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <type_traits>
 #include <vector>
 
 #include "../../include/evr.h"
 #include "evr_kernels.cuh"
 #include "evr_resident.cuh"
+#include "evr_resident_reg.cuh"
 
 using namespace evr;
 
@@ -288,8 +290,26 @@ template <class T> const ResidentKernel<T>* resident_pick(int W, int ms) {
   return nullptr;
 }
 
+// float32 register-state variant (evr_resident_reg.cuh): (NT, CS, RM)
+// shapes, a thread per CS columns of a W <= CS*NT sensor, bands <= RM rows
+struct ResidentRegKernel {
+  int nt, cs, rm;
+  void (*fn)(ResArgs<float>);
+};
+const ResidentRegKernel* resident_reg_pick(int W, int R) {
+  static const ResidentRegKernel table[] = {
+      {640, 1, 2, k_resident_reg<640, 1, 2>}, {640, 1, 4, k_resident_reg<640, 1, 4>},
+      {640, 2, 2, k_resident_reg<640, 2, 2>}, {640, 2, 5, k_resident_reg<640, 2, 5>},
+  };
+  for (const auto& k : table)
+    if (W <= k.cs * k.nt && (k.cs == 1 || W > (k.cs - 1) * k.nt) && R <= k.rm) return &k;
+  return nullptr;
+}
+
 // Band decomposition: one CTA per SM at most, equal band heights R.  The
-// frame goes to shared memory when it fits, else to global memory.
+// frame goes to shared memory when it fits; float32 sensors too large for
+// that keep the per-pixel state in registers (PLANES_REG); global-memory
+// frames only on request.
 template <class T> bool resident_plan(evr_ctx* ctx, bool allow_gmem, bool force_gmem = false) {
   int sms = 0, optin = 0;
   if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device) != cudaSuccess ||
@@ -303,15 +323,28 @@ template <class T> bool resident_plan(evr_ctx* ctx, bool allow_gmem, bool force_
   const int nt = W <= 128 ? 128 : W <= 384 ? 384 : 512;
   const size_t static_smem = sizeof(IngestShared<512>) + 64 * sizeof(double) + 64;
   int ms = PLANES_SMEM;
+  size_t smem = frame;
+  int nt_used = nt;
   if (force_gmem || frame + static_smem + 1024 > (size_t)optin) {
-    if (!allow_gmem) return false;
-    ms = PLANES_GMEM;
+    const ResidentRegKernel* rk =
+        std::is_same<T, float>::value && !force_gmem ? resident_reg_pick(W, R) : nullptr;
+    const size_t rframe = resident_reg_frame_bytes(R, W);
+    if (rk && rframe + sizeof(IngestShared<640>) + 64 * sizeof(double) + 1024 <= (size_t)optin) {
+      ms = PLANES_REG;
+      smem = rframe;
+      nt_used = rk->nt;
+    } else if (allow_gmem) {
+      ms = PLANES_GMEM;
+      smem = 0;
+    } else {
+      return false;
+    }
   }
   ctx->r_nb = nb;
   ctx->r_R = R;
-  ctx->r_nt = nt;
+  ctx->r_nt = nt_used;
   ctx->r_ms = ms;
-  ctx->r_smem = ms == PLANES_SMEM ? frame : 0;
+  ctx->r_smem = smem;
   ctx->r_frame = frame;
   return true;
 }
@@ -333,10 +366,16 @@ template <class T> int resident_alloc(evr_ctx* ctx) {
   CK(cudaMalloc(&ctx->d_ticket, sizeof(unsigned)));
   CK(cudaMemset(ctx->d_ticket, 0, sizeof(unsigned)));
   if (ctx->r_ms == PLANES_GMEM) CK(cudaMalloc(&ctx->d_frames, ctx->r_frame * ctx->r_nb));
-  const ResidentKernel<T>* k = resident_pick<T>(ctx->W, ctx->r_ms);
-  if (!k) return fail(ctx, EVR_ERR_UNSUPPORTED, "no resident kernel shape");
-  CK(cudaFuncSetAttribute((const void*)k->fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                          (int)ctx->r_smem));
+  const void* fn = nullptr;
+  if (ctx->r_ms == PLANES_REG) {
+    const ResidentRegKernel* rk = resident_reg_pick(ctx->W, ctx->r_R);
+    fn = rk ? (const void*)rk->fn : nullptr;
+  } else {
+    const ResidentKernel<T>* k = resident_pick<T>(ctx->W, ctx->r_ms);
+    fn = k ? (const void*)k->fn : nullptr;
+  }
+  if (!fn) return fail(ctx, EVR_ERR_UNSUPPORTED, "no resident kernel shape");
+  CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ctx->r_smem));
   return EVR_OK;
 }
 
@@ -396,8 +435,16 @@ template <class T> int resident_enqueue(evr_ctx* ctx, int which) {
   attr[0].val.cooperative = 1;
   lc.attrs = attr;
   lc.numAttrs = 1;
-  const ResidentKernel<T>* k = resident_pick<T>(ctx->W, ctx->r_ms);
-  cudaError_t e = cudaLaunchKernelEx(&lc, k->fn, a);
+  cudaError_t e;
+  if (ctx->r_ms == PLANES_REG) {
+    if constexpr (std::is_same<T, float>::value) {
+      e = cudaLaunchKernelEx(&lc, resident_reg_pick(ctx->W, ctx->r_R)->fn, a);
+    } else {
+      return fail(ctx, EVR_ERR_UNSUPPORTED, "register-state resident engine is float32 only");
+    }
+  } else {
+    e = cudaLaunchKernelEx(&lc, resident_pick<T>(ctx->W, ctx->r_ms)->fn, a);
+  }
   if (e != cudaSuccess) return fail(ctx, EVR_ERR_CUDA, "resident launch: %s", cudaGetErrorString(e));
   return 1;
 }
@@ -792,7 +839,9 @@ int evr_set_config(evr_ctx* ctx, const evr_config* cfg) {
     const bool ok = ctx->prec == EVR_PREC_F64 ? resident_plan<double>(ctx, gmem, gmem)
                                               : resident_plan<float>(ctx, gmem, gmem);
     if (ok) {
-      ctx->engine = ctx->r_ms == PLANES_SMEM ? EVR_ENGINE_RESIDENT : EVR_ENGINE_RESIDENT_GMEM;
+      ctx->engine = ctx->r_ms == PLANES_GMEM ? EVR_ENGINE_RESIDENT_GMEM
+                    : ctx->r_ms == PLANES_REG ? EVR_ENGINE_RESIDENT_REG
+                                              : EVR_ENGINE_RESIDENT;
       int rc = ctx->prec == EVR_PREC_F64 ? resident_alloc<double>(ctx) : resident_alloc<float>(ctx);
       if (rc) return rc;
     } else if (cfg->engine == EVR_ENGINE_RESIDENT) {

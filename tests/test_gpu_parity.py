@@ -264,3 +264,22 @@ def test_engines_agree_bitwise():
     for eng in ENGINES[1:]:
         assert np.array_equal(res["streaming"][0], res[eng][0]), eng
         assert np.array_equal(res["streaming"][1], res[eng][1]), eng
+
+
+def test_float32_register_engine_matches_streaming_bitwise():
+    """The float32 register-state resident kernel (sensors too large for
+    shared-memory frames) recomputes the metric matrix with the float
+    engine's own operations: bit-identical to the streaming float engine."""
+    H, W = 300, 1000
+    sc = evr.SolverConfig(max_iterations=20)
+    mc = evr.ManifoldConfig(denoise_iterations=10)
+    out = {}
+    for eng in ("streaming", "auto"):
+        st = evr.init_state(evr.SensorGeometry(W, H), sc, precision=1,
+                            engine={"streaming": 1, "auto": 0}[eng])
+        for pk in uniform_packets(H, W, 3, 1000, seed=21, t_step=1):
+            _, frame, _ = evr.process_packet(st, pk, mc, sc, evr.Thresholds())
+        out[eng] = (frame.copy(), st.p.copy(), st.engine())
+    assert out["auto"][2] == "resident_reg"
+    assert np.array_equal(out["auto"][0], out["streaming"][0])
+    assert np.array_equal(out["auto"][1], out["streaming"][1])
