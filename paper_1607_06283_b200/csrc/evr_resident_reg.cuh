@@ -130,6 +130,16 @@ __global__ void __launch_bounds__(NT, 1) k_resident_reg(const ResArgs<float> a) 
 #pragma unroll
       for (int f = 0; f < 3; ++f) out[s][f] = LLWords<T>::unpack(&w[s][f]);
   };
+  int tmark = 0;  // optional phase timeline, same marks as k_resident
+  auto mark = [&]() {
+    if (a.trace && tid == 0 && tmark < 256) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t)::"memory");
+      a.trace[(size_t)b * 256 + tmark] = t;
+    }
+    ++tmark;
+  };
+  mark();
   auto flag_publish = [&](int step) {
     __syncthreads();
     if (tid == 0) {
@@ -189,6 +199,7 @@ __global__ void __launch_bounds__(NT, 1) k_resident_reg(const ResArgs<float> a) 
           if (lr >= 1 && lr <= Rb) a.raw[(int64_t)(r0 - 1) * W + l] = t;
         });
   }
+  mark();
   // TV-L1 cold start u = u_bar = f0 = t (surface.py:161-165)
   EVR_CS(cs) {
     const int j = col(cs);
@@ -216,6 +227,7 @@ __global__ void __launch_bounds__(NT, 1) k_resident_reg(const ResArgs<float> a) 
         }
         __syncthreads();
       }
+      mark();
       // dual ascent + projection (surface.py:168-183), own rows + halo above
       EVR_CS(cs) {
         const int j = col(cs);
@@ -290,6 +302,7 @@ __global__ void __launch_bounds__(NT, 1) k_resident_reg(const ResArgs<float> a) 
   step = s_met;
   __syncthreads();
 
+  mark();
   // ------------------------------------------------------------ metric ---
   // surface slopes of pixel (r, j) from TD (row below the halo from L2)
   auto slopes = [&](int r, int j, T& gx, T& gy) {
@@ -364,6 +377,7 @@ __global__ void __launch_bounds__(NT, 1) k_resident_reg(const ResArgs<float> a) 
   __syncthreads();
 
   // ------------------------------------------------------- primal-dual ---
+  mark();
   double rd = 0.0, ro = 0.0;
   for (int it = 0; it < a.pd_iters; ++it) {
     const bool last = it == a.pd_iters - 1;
@@ -398,6 +412,7 @@ __global__ void __launch_bounds__(NT, 1) k_resident_reg(const ResArgs<float> a) 
       }
       __syncthreads();
     }
+    mark();
     // KL prox + over-relaxation (solve.py:234-252), own rows + halo below
     EVR_CS(cs) {
       const int j = col(cs);
@@ -429,7 +444,9 @@ __global__ void __launch_bounds__(NT, 1) k_resident_reg(const ResArgs<float> a) 
         }
       }
     }
+    mark();  // primal issued (thread 0)
     __syncthreads();
+    mark();  // primal done
     // dual ascent + ball projection (solve.py:170-201), own rows; refresh q
     EVR_CS(cs) {
       const int j = col(cs);
@@ -458,6 +475,7 @@ __global__ void __launch_bounds__(NT, 1) k_resident_reg(const ResArgs<float> a) 
         }
       }
     }
+    mark();  // dual issued (thread 0)
     if (!last) ++step;
   }
   if (a.pd_iters < 2) {
