@@ -18,6 +18,7 @@ from paper_1607_06283_b200 import _lib
 cfgname = sys.argv[1] if len(sys.argv) > 1 else "C2"
 prec = int(sys.argv[2]) if len(sys.argv) > 2 else 0
 H, W, epp, pd, tv, rate = bench.CONFIGS[cfgname]
+pd = min(pd, int(os.environ.get("PROBE_PD", "50")))  # 256 timeline slots per CTA
 sc = evr.SolverConfig(max_iterations=pd)
 mc = evr.ManifoldConfig(denoise_iterations=tv)
 st = evr.init_state(evr.SensorGeometry(W, H), sc, precision=prec, engine=2)
