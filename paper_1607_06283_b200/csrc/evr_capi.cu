@@ -10,6 +10,7 @@
 
 #include <algorithm>
 #include <cstdarg>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <string>
@@ -74,6 +75,7 @@ struct evr_ctx {
   int r_nb = 0, r_R = 0, r_nt = 0, r_ms = 0;
   size_t r_smem = 0, r_frame = 0;
   void* d_frames = nullptr;               // PLANES_GMEM per-CTA plane frames
+  void* d_pack = nullptr;                 // packed state of the fused streaming list
   unsigned long long* d_flags = nullptr;  // per-CTA progress words
   void* d_xchg = nullptr;                 // boundary-row ping-pong buffer
   unsigned* d_ticket = nullptr;
@@ -155,45 +157,126 @@ void launch_ingest(evr_ctx* ctx) {
 }
 
 // The per-packet sequence of the streaming engine as a list of steps, one
-// launch each (evr_group runs the same list on every band in lock step and
+// launch each (evr_group runs the split list on every band in lock step and
 // exchanges halo rows between steps).
 enum StepKind {
-  ST_INGEST, ST_NORM, ST_TVD, ST_TVP, ST_TVFIN, ST_METRIC, ST_PDP, ST_REL, ST_PDD, ST_EPI
+  ST_INGEST, ST_NORM, ST_TVD, ST_TVP, ST_TVFIN, ST_METRIC, ST_PDP, ST_REL, ST_PDD, ST_EPI,
+  // fused list (whole-sensor contexts): packed state, one launch per iteration
+  ST_NORMF, ST_TVF, ST_TVFINF, ST_PACK, ST_PDF, ST_RELF, ST_UNPACK
 };
 struct Step {
   int kind, it;
 };
 
-// which: 0 = surface (ingest .. metric), 1 = solve (primal-dual + epilogue), 2 = both
-std::vector<Step> packet_steps(const evr_config& g, int which) {
+// which: 0 = surface (ingest .. metric), 1 = solve (primal-dual + epilogue), 2 = both.
+// fused: one launch per TV-L1 / primal-dual iteration (k_tv_march,
+// k_pd_march) on the packed, ping-ponged state; band contexts (evr_group)
+// exchange halo rows between half-steps and use the split list.
+std::vector<Step> packet_steps(const evr_config& g, int which, bool fused) {
   std::vector<Step> v;
+  const int D = g.denoise_iterations, M = g.max_iterations;
   if (which != 1) {
     v.push_back({ST_INGEST, 0});
     if (g.manifold_enabled) {
-      v.push_back({ST_NORM, 0});
-      for (int k = 0; k < g.denoise_iterations; ++k) {
-        v.push_back({ST_TVD, k});
-        v.push_back({ST_TVP, k});
+      v.push_back({fused ? ST_NORMF : ST_NORM, 0});
+      for (int k = 0; k < D; ++k) {
+        if (fused) {
+          v.push_back({ST_TVF, k});
+        } else {
+          v.push_back({ST_TVD, k});
+          v.push_back({ST_TVP, k});
+        }
       }
-      v.push_back({ST_TVFIN, 0});
+      v.push_back({fused ? ST_TVFINF : ST_TVFIN, D});
     }
     v.push_back({ST_METRIC, 0});
   }
   if (which != 0) {
-    for (int k = 0; k < g.max_iterations; ++k) {
-      v.push_back({ST_PDP, k});
-      if (k == g.max_iterations - 1) v.push_back({ST_REL, k});
-      v.push_back({ST_PDD, k});
+    if (fused) v.push_back({ST_PACK, 0});
+    for (int k = 0; k < M; ++k) {
+      if (fused) {
+        v.push_back({ST_PDF, k});
+        if (k == M - 1) v.push_back({ST_RELF, k});
+      } else {
+        v.push_back({ST_PDP, k});
+        if (k == M - 1) v.push_back({ST_REL, k});
+        v.push_back({ST_PDD, k});
+      }
     }
-    v.push_back({ST_EPI, 0});
+    v.push_back({fused ? ST_UNPACK : ST_EPI, M});
   }
   return v;
 }
 
-template <class T> void relchange(evr_ctx* ctx, const T* un, const T* u, int iterations) {
+// fused iterations: rows per warp strip (RY), rows of loads in flight ahead
+// of the arithmetic (D, the register budget), threads per CTA; measured on
+// B200 at 640x480 .. 2048x2048 (tools/sweep_march.sh)
+#ifndef EVR_MARCH_RY
+#define EVR_MARCH_RY 4
+#endif
+#ifndef EVR_MARCH_D32
+#define EVR_MARCH_D32 4
+#endif
+#ifndef EVR_MARCH_D64
+#define EVR_MARCH_D64 1
+#endif
+constexpr int kMarchRY = EVR_MARCH_RY, kMarchNT = 128;
+template <class T> struct MarchDepth { static constexpr int tv = EVR_MARCH_D32, pd = EVR_MARCH_D32; };
+template <> struct MarchDepth<double> { static constexpr int tv = EVR_MARCH_D64, pd = EVR_MARCH_D64; };
+inline unsigned march_grid(const evr_ctx* c) {
+  const int64_t warps =
+      (int64_t)((c->W + kStrip - 1) / kStrip) * ((c->H + kMarchRY - 1) / kMarchRY);
+  return (unsigned)((warps + kMarchNT / 32 - 1) / (kMarchNT / 32));
+}
+
+// packed state of the fused list: TV {u, u_bar, px, py} x 2, solver
+// {p1, p2, p3, u} x 2, then the solver constants (1 quad per pixel for
+// float, 2 for double)
+template <class T> struct Packed {
+  Q4<T>* tv[2];
+  Q4<T>* pd[2];
+  Q4<T>* cst;
+};
+template <class T> Packed<T> packed(const evr_ctx* c) {
+  Q4<T>* b = reinterpret_cast<Q4<T>*>(c->d_pack);
+  const int64_t N = c->N;
+  return Packed<T>{{b, b + N}, {b + 2 * N, b + 3 * N}, b + 4 * N};
+}
+inline size_t packed_bytes(int64_t N, int prec) {
+  return prec == EVR_PREC_F64 ? (size_t)N * 6 * 32 : (size_t)N * 5 * 16;
+}
+
+template <class T> CoefPlanes<T> coefs(const evr_ctx* c);
+
+// iteration kernels go out with programmatic stream serialization (PDL,
+// see pdl_wait_and_release); EVR_PDL=0 turns it off for A/B timing
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("EVR_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+template <class... KArgs, class... Args>
+void launch_pdl(void (*k)(KArgs...), unsigned grid, unsigned block, cudaStream_t s,
+                Args&&... args) {
+  cudaLaunchConfig_t lc{};
+  lc.gridDim = dim3(grid);
+  lc.blockDim = dim3(block);
+  lc.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  lc.attrs = at;
+  lc.numAttrs = pdl_enabled() ? 1 : 0;
+  cudaLaunchKernelEx(&lc, k, std::forward<Args>(args)...);
+}
+
+template <class T>
+void relchange(evr_ctx* ctx, const T* un, const T* u, int iterations, int stride = 1) {
   const int nb = red_blocks(ctx->own_n());
-  k_relchange_partial<T, kNT><<<nb, kNT, 0, ctx->stream>>>(un + ctx->own_off(), u + ctx->own_off(),
-                                                          ctx->own_n(), ctx->part);
+  k_relchange_partial<T, kNT><<<nb, kNT, 0, ctx->stream>>>(
+      un + ctx->own_off() * stride, u + ctx->own_off() * stride, ctx->own_n(), ctx->part, stride);
   k_relchange_final<kNT><<<1, kNT, 0, ctx->stream>>>(ctx->part, nb, ctx->d_info, iterations,
                                                     ctx->d_scalar + 2);
 }
@@ -254,13 +337,62 @@ template <class T> int launch_step(evr_ctx* ctx, const Step& st) {
       k_epilogue<T><<<grid1d(n), kNT, 0, s>>>(last + off, ctx->fld<T>(F_U) + off, ctx->f + off, n);
       return 1;
     }
+    // ---- fused list (whole-sensor context: off = 0, n = N)
+    case ST_NORMF:
+      k_normalize_pack<T><<<grid1d(n), kNT, 0, s>>>(ctx->raw, ctx->hdr(), g.t_scale, t,
+                                                    packed<T>(ctx).tv[0], n);
+      return 1;
+    case ST_TVF: {  // iteration k reads set k & 1 and writes the other
+      const Packed<T> P = packed<T>(ctx);
+      const int a = st.it & 1;
+      launch_pdl(k_tv_march<T, kMarchRY, MarchDepth<T>::tv>, march_grid(ctx), kMarchNT, s,
+                 (const Q4<T>*)P.tv[a], (const T*)t, P.tv[a ^ 1], ctx->H, ctx->W, (T)step,
+                 (T)step, (T)(step * g.denoise_weight));
+      return 1;
+    }
+    case ST_TVFINF:  // st.it = the TV-L1 iteration count
+      k_tv_finish_packed<T><<<grid1d(n), kNT, 0, s>>>(packed<T>(ctx).tv[st.it & 1], t,
+                                                      (T)g.t_scale, n);
+      return 1;
+    case ST_PACK: {
+      const Packed<T> P = packed<T>(ctx);
+      k_pack_solver<T><<<grid1d(n), kNT, 0, s>>>(
+          ctx->fld<T>(F_P1), ctx->fld<T>(F_P2), ctx->fld<T>(F_P3), ctx->fld<T>(F_U),
+          ctx->fld<T>(F_TX), ctx->fld<T>(F_TY), coefs<T>(ctx), ctx->fld<T>(F_SG),
+          ctx->fld<T>(F_BETA), ctx->fld<T>(F_FB), P.pd[0], P.cst, n);
+      return 1;
+    }
+    case ST_PDF: {
+      const Packed<T> P = packed<T>(ctx);
+      const int a = st.it & 1;
+      using M = typename MetricPack<T>::type;
+      M m;
+      if constexpr (std::is_same<T, float>::value)
+        m = M{P.cst, (float)(g.tau * g.lam)};
+      else
+        m = M{P.cst};
+      launch_pdl(k_pd_march<T, kMarchRY, MarchDepth<T>::pd, M>, march_grid(ctx), kMarchNT, s,
+                 (const Q4<T>*)P.pd[a], m, P.pd[a ^ 1], ctx->H, ctx->W, (T)g.tau, (T)g.sigma,
+                 (T)g.u_min, (T)g.u_max);
+      return 1;
+    }
+    case ST_RELF: {  // u of the last two iterations, the w of the packed quads
+      const Packed<T> P = packed<T>(ctx);
+      relchange<T>(ctx, &P.pd[(st.it + 1) & 1]->w, &P.pd[st.it & 1]->w, st.it + 1, 4);
+      return 2;
+    }
+    case ST_UNPACK:  // st.it = the iteration count
+      k_unpack_solver<T><<<grid1d(n), kNT, 0, s>>>(packed<T>(ctx).pd[st.it & 1],
+                                                   ctx->fld<T>(F_P1), ctx->fld<T>(F_P2),
+                                                   ctx->fld<T>(F_P3), ctx->fld<T>(F_U), ctx->f, n);
+      return 1;
   }
   return 0;
 }
 
 template <class T> int enqueue_packet(evr_ctx* ctx, int which) {
   int n = 0;
-  for (const Step& st : packet_steps(ctx->cfg, which)) n += launch_step<T>(ctx, st);
+  for (const Step& st : packet_steps(ctx->cfg, which, !ctx->banded)) n += launch_step<T>(ctx, st);
   int rc = launch_err(ctx, "packet");
   return rc ? rc : n;
 }
@@ -767,6 +899,7 @@ int evr_create(evr_ctx** out, int device, int height, int width, int precision) 
     CK(cudaMalloc(&ctx->slab, ctx->field_stride * F_COUNT));
     CK(cudaMemsetAsync(ctx->slab, 0, ctx->field_stride * F_COUNT, ctx->stream));
     CK(cudaMalloc(&ctx->f, sizeof(double) * N));
+    CK(cudaMalloc(&ctx->d_pack, packed_bytes(N, precision)));
     CK(cudaMalloc(&ctx->raw, sizeof(int64_t) * N));
     CK(cudaMalloc(&ctx->aos_a, sizeof(double) * 3 * N));
     CK(cudaMalloc(&ctx->aos_b, sizeof(double) * 3 * N));
@@ -795,6 +928,7 @@ void evr_destroy(evr_ctx* ctx) {
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   drop_graphs(ctx);
   cudaFree(ctx->slab);
+  cudaFree(ctx->d_pack);
   cudaFree(ctx->f);
   cudaFree(ctx->raw);
   cudaFree(ctx->aos_a);
@@ -1441,7 +1575,7 @@ int exchange_after(evr_group* grp, int kind) {
 }
 
 template <class T> int group_packet(evr_group* grp) {
-  const std::vector<Step> steps = packet_steps(grp->cfg, 2);
+  const std::vector<Step> steps = packet_steps(grp->cfg, 2, false);
   const int n = grp->n;
   for (const Step& st : steps) {
     for (int b = 0; b < n; ++b) {

@@ -254,6 +254,254 @@ __global__ void k_pd_dual(const T* __restrict__ v, T* __restrict__ p1, T* __rest
   p3[k] = d;
 }
 
+// ------------------------------------------------- fused iterations --
+// One launch per iteration (streaming engine, whole-sensor contexts).  Each
+// warp owns a strip of kStrip = 30 columns x RY rows; its 32 lanes cover the
+// strip plus one column either side, and the warp marches down the rows
+// keeping the previous row in registers.  Horizontal neighbours come from
+// warp shuffles, vertical ones from the march, so the half-step a
+// neighbouring strip also needs (the TV-L1 dual on the left column / row
+// above; the KL primal on the right column / row
+// below) is recomputed, bit-identically, instead of exchanged.  Fields are
+// ping-ponged between iterations so neighbours read iteration k while
+// iteration k+1 is written.  No shared memory, no block barrier.
+constexpr int kStrip = 30;
+
+// Programmatic dependent launch: the iteration kernels are launched with
+// programmatic stream serialization, so the next iteration's CTAs are
+// resident and waiting while this one drains; griddepcontrol.wait blocks
+// until the previous grid has completed and its writes are visible (a
+// no-op for a normal launch).
+__device__ __forceinline__ void pdl_wait_and_release() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+struct Strip {
+  int j, i0, lane;
+  bool inb, own, live;
+};
+template <int RY>
+__device__ __forceinline__ Strip strip_of(int H, int W) {
+  Strip s;
+  s.lane = threadIdx.x & 31;
+  const int w = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int nsx = (W + kStrip - 1) / kStrip;
+  const int sx = w % nsx, sy = w / nsx;
+  s.live = sy * RY < H;
+  s.j = sx * kStrip - 1 + s.lane;
+  s.i0 = sy * RY;
+  s.inb = s.j >= 0 && s.j < W;
+  s.own = s.lane >= 1 && s.lane <= kStrip && s.j < W;
+  return s;
+}
+
+// The fused iterations keep their changing fields interleaved, one 16-byte
+// (float) / 32-byte (double) quad per pixel, so a warp row is one vector
+// load / store per field group instead of one access per plane:
+//   TV-L1:        TvQ = {u, u_bar, px, py}        (ping-pong), f0 = the t plane
+//   primal-dual:  PdQ = {p1, p2, p3, u}           (ping-pong)
+//                 constants: float  {tx, ty, fb, 0} (matrix recomputed)
+//                            double {a11, a12, a22, a31}, {a32, sqrtG, beta, fb}
+// k_pack_solver / k_unpack_solver convert to and from the planes the rest of
+// the engine (state I/O, operator API, host loop, bands) uses.
+template <class T> struct alignas(4 * sizeof(T)) Q4 {
+  T x, y, z, w;
+};
+
+// TV-L1 iteration (surface.py:167-193): dual ascent + projection on rows
+// i0-1 .. i0+RY-1, primal + L1 shrink + over-relaxation on the owned rows.
+// Loads go to the clamped pixel so they are unconditional and are issued D
+// rows ahead of the arithmetic (software pipeline over the unrolled march);
+// out-of-sensor lanes / rows compute values nobody reads and store nothing.
+template <class T, int RY, int D>
+__global__ void __launch_bounds__(128)
+k_tv_march(const Q4<T>* __restrict__ in, const T* __restrict__ f0, Q4<T>* __restrict__ out,
+           int H, int W, T sigma, T tau, T shrink) {
+  const Strip s = strip_of<RY>(H, W);
+  pdl_wait_and_release();
+  if (!s.live) return;  // whole warp
+  const int j = s.j;
+  const int jc = min(max(j, 0), W - 1);
+  auto at = [&](int rr) { return min(max(s.i0 - 1 + rr, 0), H - 1) * W + jc; };
+  constexpr int NR = RY + 2;  // rows i0-1 .. i0+RY (the last one: u_bar only)
+  Q4<T> q[NR];
+  T f[NR];
+  auto load = [&](int rr) {
+    const int kc = at(rr);
+    q[rr] = in[kc];
+    if (rr >= 1 && rr < NR - 1) f[rr] = f0[kc];
+  };
+#pragma unroll
+  for (int rr = 0; rr < D && rr < NR; ++rr) load(rr);
+  T pyn_up = T(0);
+#pragma unroll
+  for (int rr = 0; rr < NR - 1; ++rr) {
+    if (rr + D < NR) load(rr + D);
+    const int r = s.i0 - 1 + rr;
+    const T ub_c = q[rr].y, ub_n = q[rr + 1].y;
+    T pxn = q[rr].z, pyn = q[rr].w;
+    const T ub_r = __shfl_down_sync(0xffffffffu, ub_c, 1);
+    const T dx = j < W - 1 ? ub_r - ub_c : T(0);
+    const T dy = r < H - 1 ? ub_n - ub_c : T(0);
+    tv_dual_step(dx, dy, sigma, pxn, pyn);
+    const T pxl = __shfl_up_sync(0xffffffffu, pxn, 1);
+    if (rr >= 1 && r < H && s.own) {
+      const T d = div_at(pxn, j > 0 ? pxl : T(0), pyn, r > 0 ? pyn_up : T(0), r, j, H, W);
+      T ubar;
+      const T un = tv_primal_step(d, q[rr].x, f[rr], tau, shrink, ubar);
+      out[r * W + j] = Q4<T>{un, ubar, pxn, pyn};
+    }
+    pyn_up = pyn;
+  }
+}
+
+// metric inputs of the primal-dual iteration, from the packed constants
+struct MetricPackF32 {
+  const Q4<float>* __restrict__ c;  // {tx, ty, fb, 0}
+  float tl;                         // tau * lam (solve.py:227)
+  using Raw = Q4<float>;
+  __device__ __forceinline__ Raw load(int k) const { return c[k]; }
+  __device__ __forceinline__ void finish(const Raw& r, Coef<float>& cf, float& sg, float& beta,
+                                         float& fb) const {
+    const MetricPx m = metric_px(r.x, r.y);  // bit-identical to k_metric_setup's planes
+    cf = m.c;
+    sg = m.sg;
+    beta = tl * m.sg;
+    fb = r.z;
+  }
+};
+struct MetricPackF64 {
+  const Q4<double>* __restrict__ c;  // {a11, a12, a22, a31}, {a32, sqrtG, beta, fb}
+  struct Raw {
+    Q4<double> a, b;
+  };
+  __device__ __forceinline__ Raw load(int k) const { return Raw{c[2 * k], c[2 * k + 1]}; }
+  __device__ __forceinline__ void finish(const Raw& r, Coef<double>& cf, double& sg,
+                                         double& beta, double& fb) const {
+    cf = Coef<double>{r.a.x, r.a.y, r.a.z, r.a.w, r.b.x};
+    sg = r.b.y;
+    beta = r.b.z;
+    fb = r.b.w;
+  }
+};
+template <class T> struct MetricPack;
+template <> struct MetricPack<float> { using type = MetricPackF32; };
+template <> struct MetricPack<double> { using type = MetricPackF64; };
+
+// primal-dual iteration (solve.py:233-252): q = A^T p on rows i0-1 .. i0+RY,
+// KL prox + over-relaxation on rows i0 .. i0+RY, dual ascent + ball
+// projection on the owned rows one row behind the primal, then the row's
+// {p, u} quad is stored; loads pipelined D rows ahead as in k_tv_march.
+template <class T, int RY, int D, class M>
+__global__ void __launch_bounds__(128)
+k_pd_march(const Q4<T>* __restrict__ in, M m, Q4<T>* __restrict__ out, int H, int W, T tau,
+           T sigma, T umin, T umax) {
+  const Strip s = strip_of<RY>(H, W);
+  pdl_wait_and_release();
+  if (!s.live) return;  // whole warp
+  const int j = s.j;
+  const int jc = min(max(j, 0), W - 1);
+  auto at = [&](int rr) { return min(max(s.i0 - 1 + rr, 0), H - 1) * W + jc; };
+  constexpr int NR = RY + 2;  // rows i0-1 .. i0+RY
+  Q4<T> q[NR];
+  typename M::Raw c[NR];
+  auto load = [&](int rr) {
+    const int kc = at(rr);
+    q[rr] = in[kc];
+    c[rr] = m.load(kc);
+  };
+#pragma unroll
+  for (int rr = 0; rr < D && rr < NR; ++rr) load(rr);
+  T qy_up = T(0), v_up = T(0), sg_up = T(1), nu_up = T(0);
+  Coef<T> cf_up{T(0), T(0), T(0), T(0), T(0)};
+#pragma unroll
+  for (int rr = 0; rr < NR; ++rr) {
+    if (rr + D < NR) load(rr + D);
+    const int r = s.i0 - 1 + rr;
+    Coef<T> cf;
+    T sg, beta, fb, qx, qy, v = T(0), nu = T(0);
+    m.finish(c[rr], cf, sg, beta, fb);
+    q_of(cf, q[rr].x, q[rr].y, q[rr].z, qx, qy);
+    const T qxl = __shfl_up_sync(0xffffffffu, qx, 1);
+    if (rr >= 1) {
+      const T d = div_at(qx, j > 0 ? qxl : T(0), qy, r > 0 ? qy_up : T(0), r, j, H, W);
+      const T uk = q[rr].w;
+      nu = kl_primal(d, uk, beta, fb, tau, umin, umax);
+      v = nu * T(2) - uk;
+    }
+    const T vr = __shfl_down_sync(0xffffffffu, v_up, 1);
+    if (rr >= 2 && r - 1 < H && s.own) {
+      T a = q[rr - 1].x, b = q[rr - 1].y, cc = q[rr - 1].z;
+      const T gx = j < W - 1 ? vr - v_up : T(0);
+      const T gy = r - 1 < H - 1 ? v - v_up : T(0);
+      dual_step(cf_up, sigma, gx, gy, sg_up, a, b, cc);
+      out[(r - 1) * W + j] = Q4<T>{a, b, cc, nu_up};
+    }
+    qy_up = qy;
+    v_up = v;
+    nu_up = nu;
+    cf_up = cf;
+    sg_up = sg;
+  }
+}
+
+// normalize_timestamps (surface.py:130-143) + the TV-L1 cold start
+// (surface.py:161-165) into the packed state
+template <class T>
+__global__ void k_normalize_pack(const int64_t* __restrict__ raw,
+                                 const PacketHdr* __restrict__ hdr, double t_scale,
+                                 T* __restrict__ t, Q4<T>* __restrict__ q, int64_t N) {
+  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= N) return;
+  const T v = (T)normalize_at((double)raw[k], (double)hdr->now, t_scale, hdr->window);
+  t[k] = v;
+  q[k] = Q4<T>{v, v, T(0), T(0)};
+}
+
+// np.clip(u, 0, t_scale) from the packed TV-L1 state (surface.py:195)
+template <class T>
+__global__ void k_tv_finish_packed(const Q4<T>* __restrict__ q, T* __restrict__ t, T t_scale,
+                                   int64_t N) {
+  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= N) return;
+  t[k] = vclip(q[k].x, T(0), t_scale);
+}
+
+// planes -> packed solver state + constants (after k_metric_setup)
+template <class T>
+__global__ void k_pack_solver(const T* __restrict__ p1, const T* __restrict__ p2,
+                              const T* __restrict__ p3, const T* __restrict__ u,
+                              const T* __restrict__ tx, const T* __restrict__ ty,
+                              CoefPlanes<T> c, const T* __restrict__ sg,
+                              const T* __restrict__ beta, const T* __restrict__ fb,
+                              Q4<T>* __restrict__ st, Q4<T>* __restrict__ cst, int64_t N) {
+  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= N) return;
+  st[k] = Q4<T>{p1[k], p2[k], p3[k], u[k]};
+  if constexpr (sizeof(T) == 4) {
+    cst[k] = Q4<T>{tx[k], ty[k], fb[k], T(0)};
+  } else {
+    cst[2 * k] = Q4<T>{c.a11[k], c.a12[k], c.a22[k], c.a31[k]};
+    cst[2 * k + 1] = Q4<T>{c.a32[k], sg[k], beta[k], fb[k]};
+  }
+}
+
+// packed solver state -> p, u planes and f = u (pipeline.py:165)
+template <class T>
+__global__ void k_unpack_solver(const Q4<T>* __restrict__ st, T* __restrict__ p1,
+                                T* __restrict__ p2, T* __restrict__ p3, T* __restrict__ u,
+                                double* __restrict__ f, int64_t N) {
+  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= N) return;
+  const Q4<T> q = st[k];
+  p1[k] = q.x;
+  p2[k] = q.y;
+  p3[k] = q.z;
+  u[k] = q.w;
+  f[k] = (double)q.w;
+}
+
 // --------------------------------------------------------- reductions --
 // Deterministic two-pass reductions (fixed tree): pass 1 writes one partial
 // per block, pass 2 (one block) folds the partials in index order.
@@ -274,11 +522,11 @@ __device__ __forceinline__ double block_sum(double x, double* sh) {
 template <class T, int NT>
 __global__ void __launch_bounds__(NT)
 k_relchange_partial(const T* __restrict__ un, const T* __restrict__ u, int64_t N,
-                    double* __restrict__ part) {
+                    double* __restrict__ part, int stride = 1) {
   __shared__ double sh[NT / 32];
   double d = 0.0, o = 0.0;
   for (int64_t k = (int64_t)blockIdx.x * NT + threadIdx.x; k < N; k += (int64_t)gridDim.x * NT) {
-    const double a = (double)un[k], b = (double)u[k];
+    const double a = (double)un[k * stride], b = (double)u[k * stride];
     d += (a - b) * (a - b);
     o += b * b;
   }

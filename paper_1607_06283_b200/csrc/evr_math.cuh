@@ -57,6 +57,26 @@ template <class T> __device__ __forceinline__ T metric_G(T tx, T ty) {
   return T(1) + tx * tx + ty * ty;
 }
 
+// float32 metric matrix and sqrt(G) of one pixel from its surface slopes,
+// recomputed on the fly: G once, one MUFU.RCP shared by the five quotients
+// (__fdividef(a, G) == a * rcp(G)), bit-identical to k_metric_setup's planes
+struct MetricPx {
+  Coef<float> c;
+  float sg;
+};
+__device__ __forceinline__ MetricPx metric_px(float tx, float ty) {
+  const float G = metric_G(tx, ty);
+  const float r = Arith<float>::div(1.0f, G);  // MUFU.RCP(G)
+  MetricPx m;
+  m.c.a11 = (1.0f + ty * ty) * r;
+  m.c.a12 = -(tx * ty) * r;
+  m.c.a22 = (1.0f + tx * tx) * r;
+  m.c.a31 = tx * r;
+  m.c.a32 = ty * r;
+  m.sg = Arith<float>::sqrt(G);
+  return m;
+}
+
 // div_xy (surface.py:107-121) at (i, j): x part (qx here / qx left), then the
 // y part (qy here / qy above) added into it.  qx[:, W-1], qy[H-1, :] unused.
 template <class T>

@@ -33,24 +33,6 @@ __host__ __device__ inline size_t resident_reg_frame_bytes(int R, int W) {
   return (size_t)resident_plane_stride(R, W) * SR_COUNT * sizeof(float);
 }
 
-// metric matrix and sqrt(G) of one pixel from its surface slopes
-struct MetricPx {
-  Coef<float> c;
-  float sg;
-};
-__device__ __forceinline__ MetricPx metric_px(float tx, float ty) {
-  const float G = metric_G(tx, ty);
-  const float r = Arith<float>::div(1.0f, G);  // MUFU.RCP(G)
-  MetricPx m;
-  m.c.a11 = (1.0f + ty * ty) * r;
-  m.c.a12 = -(tx * ty) * r;
-  m.c.a22 = (1.0f + tx * tx) * r;
-  m.c.a31 = tx * r;
-  m.c.a32 = ty * r;
-  m.sg = Arith<float>::sqrt(G);
-  return m;
-}
-
 #define EVR_CS(cs) _Pragma("unroll") for (int cs = 0; cs < CS; ++cs)
 #define EVR_R(r) _Pragma("unroll") for (int r = 0; r < RM + 2; ++r)
 

@@ -182,6 +182,24 @@ def test_full_size_chained_vs_oracle(H, W, epp, iters, engine):
     assert np.array_equal(st.raw_timestamps, ref.raw)
 
 
+@pytest.mark.parametrize("H,W,tv,pd", [(45, 97, 13, 9), (17, 33, 1, 1), (9, 40, 2, 3)])
+def test_fused_streaming_odd_iterations_vs_oracle(H, W, tv, pd):
+    """The fused one-launch-per-iteration streaming kernels ping-pong their
+    fields; odd TV-L1 / primal-dual counts end on the second set, ragged
+    tiles at the right / bottom edges: bit-exact with the oracle, chained,
+    including the dual carried to the next packet."""
+    sc = evr.SolverConfig(max_iterations=pd)
+    mc = evr.ManifoldConfig(denoise_iterations=tv)
+    st = evr.init_state(evr.SensorGeometry(W, H), sc, precision=0, engine=1)
+    ref = O.OracleStream(H, W, O.make_config(max_iterations=pd, denoise_iterations=tv))
+    for pk in uniform_packets(H, W, 4, 300, seed=H * tv + pd, t_step=2):
+        _, frame, res = evr.process_packet(st, pk, mc, sc, evr.Thresholds())
+        it, rel = ref.process(np.ascontiguousarray(pk))
+        assert res.iterations == it
+        assert np.array_equal(frame, ref.u)
+        assert np.array_equal(st.p, ref.p)
+
+
 def test_float32_engine_within_log_tolerance():
     """float32 surface+solver: max |log u - log u_ref| <= 1e-4, teacher-forced
     per packet and chained over the DVS128 S-stream fixture."""
