@@ -238,7 +238,8 @@ def run_gpu(args):
     torch.cuda.set_device(local)
     H, W, epp, pd, tv, rate = CONFIGS[args.config]
     prec = {"f64": 0, "f32": 1}[args.precision]
-    engine = {"auto": 0, "streaming": 1, "resident": 2, "resident_gmem": 3}[args.engine]
+    engine = {"auto": 0, "streaming": 1, "resident": 2, "resident_gmem": 3,
+              "resident_reg": 4}[args.engine]
     mc = evr.ManifoldConfig(denoise_iterations=tv)
     sc = evr.SolverConfig(max_iterations=pd)
     th = evr.Thresholds()
@@ -383,7 +384,7 @@ def main():
     ap.add_argument("--config", default="C2", choices=sorted(CONFIGS))
     ap.add_argument("--precision", default="f64", choices=["f64", "f32"])
     ap.add_argument("--engine", default="auto",
-                    choices=["auto", "streaming", "resident", "resident_gmem"])
+                    choices=["auto", "streaming", "resident", "resident_gmem", "resident_reg"])
     ap.add_argument("--cpu-budget", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()

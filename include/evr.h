@@ -48,13 +48,14 @@ typedef enum { EVR_PREC_F64 = 0, EVR_PREC_F32 = 1 } evr_precision;
 
 /* Solver-engine selection for the per-packet path. */
 typedef enum {
-    EVR_ENGINE_AUTO = 0,      /* resident when it fits, else streaming */
+    EVR_ENGINE_AUTO = 0,      /* shared-memory resident for small sensors (<= 2 rows
+                                 per SM), else streaming */
     EVR_ENGINE_STREAMING = 1, /* one launch per half-step, fields in HBM/L2 */
     EVR_ENGINE_RESIDENT = 2,  /* persistent kernel, row bands in shared memory */
     EVR_ENGINE_RESIDENT_GMEM = 3, /* persistent kernel, band frames in L2/HBM
                                      (on request only) */
     EVR_ENGINE_RESIDENT_REG = 4   /* float32 persistent kernel, per-pixel state in
-                                     registers (reported; chosen by AUTO/RESIDENT) */
+                                     registers (on request; RESIDENT falls back to it) */
 } evr_engine;
 
 /* One camera event: events.py:35-43 Event(x, y, polarity, timestamp).

@@ -29,8 +29,9 @@ ENGINE_AUTO = 0
 ENGINE_STREAMING = 1
 ENGINE_RESIDENT = 2
 ENGINE_RESIDENT_GMEM = 3
+ENGINE_RESIDENT_REG = 4
 ENGINE_NAMES = {ENGINE_AUTO: "auto", ENGINE_STREAMING: "streaming", ENGINE_RESIDENT: "resident",
-                ENGINE_RESIDENT_GMEM: "resident_gmem", 4: "resident_reg"}
+                ENGINE_RESIDENT_GMEM: "resident_gmem", ENGINE_RESIDENT_REG: "resident_reg"}
 
 # evr_event (include/evr.h): 16-byte packed camera event
 EVENT_DTYPE = np.dtype([("t", "<i8"), ("x", "<i4"), ("y", "<i2"), ("polarity", "<i2")])

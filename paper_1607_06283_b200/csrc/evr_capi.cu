@@ -403,6 +403,7 @@ template <class T> int enqueue_packet(evr_ctx* ctx, int which) {
 // column when W <= NT), CH = 2 rows per register chunk, and where the CTA's
 // frame of planes lives (shared memory, else a global-memory slice).
 constexpr int kResidentCH = 2;
+constexpr int kAutoResidentRows = 2;  // AUTO: resident while rows per CTA <= this
 template <class T> struct ResidentKernel {
   int nt, ms;
   void (*fn)(ResArgs<T>);
@@ -442,7 +443,10 @@ const ResidentRegKernel* resident_reg_pick(int W, int R) {
 // frame goes to shared memory when it fits; float32 sensors too large for
 // that keep the per-pixel state in registers (PLANES_REG); global-memory
 // frames only on request.
-template <class T> bool resident_plan(evr_ctx* ctx, bool allow_gmem, bool force_gmem = false) {
+// where a plan may put the per-CTA frames
+enum PlanWant { WANT_SMEM, WANT_SMEM_OR_REG, WANT_REG, WANT_GMEM };
+
+template <class T> bool resident_plan(evr_ctx* ctx, PlanWant want) {
   int sms = 0, optin = 0;
   if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device) != cudaSuccess ||
       cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device) !=
@@ -454,23 +458,25 @@ template <class T> bool resident_plan(evr_ctx* ctx, bool allow_gmem, bool force_
   const size_t frame = resident_frame_bytes<T>(R, W);
   const int nt = W <= 128 ? 128 : W <= 384 ? 384 : 512;
   const size_t static_smem = sizeof(IngestShared<512>) + 64 * sizeof(double) + 64;
-  int ms = PLANES_SMEM;
-  size_t smem = frame;
-  int nt_used = nt;
-  if (force_gmem || frame + static_smem + 1024 > (size_t)optin) {
-    const ResidentRegKernel* rk =
-        std::is_same<T, float>::value && !force_gmem ? resident_reg_pick(W, R) : nullptr;
-    const size_t rframe = resident_reg_frame_bytes(R, W);
-    if (rk && rframe + sizeof(IngestShared<640>) + 64 * sizeof(double) + 1024 <= (size_t)optin) {
-      ms = PLANES_REG;
-      smem = rframe;
-      nt_used = rk->nt;
-    } else if (allow_gmem) {
-      ms = PLANES_GMEM;
-      smem = 0;
-    } else {
-      return false;
-    }
+  const bool smem_fits = frame + static_smem + 1024 <= (size_t)optin;
+  const ResidentRegKernel* rk = std::is_same<T, float>::value ? resident_reg_pick(W, R) : nullptr;
+  const size_t rframe = resident_reg_frame_bytes(R, W);
+  const bool reg_fits =
+      rk && rframe + sizeof(IngestShared<640>) + 64 * sizeof(double) + 1024 <= (size_t)optin;
+  int ms, nt_used = nt;
+  size_t smem;
+  if (want == WANT_GMEM) {
+    ms = PLANES_GMEM;
+    smem = 0;
+  } else if (want != WANT_REG && smem_fits) {
+    ms = PLANES_SMEM;
+    smem = frame;
+  } else if (want != WANT_SMEM && reg_fits) {
+    ms = PLANES_REG;
+    smem = rframe;
+    nt_used = rk->nt;
+  } else {
+    return false;
   }
   ctx->r_nb = nb;
   ctx->r_R = R;
@@ -966,21 +972,27 @@ int evr_set_config(evr_ctx* ctx, const evr_config* cfg) {
   ctx->engine = EVR_ENGINE_STREAMING;
   if (cfg->engine != EVR_ENGINE_STREAMING && cfg->convergence_tol <= 0 && ctx->H >= 2 &&
       ctx->W >= 2) {
-    // AUTO / RESIDENT: shared-memory frames or nothing (measured: for
-    // sensors beyond SMEM the streaming engine beats global frames, see
-    // profiles/r01_summary.md); RESIDENT_GMEM forces global frames.
-    const bool gmem = cfg->engine == EVR_ENGINE_RESIDENT_GMEM;
-    const bool ok = ctx->prec == EVR_PREC_F64 ? resident_plan<double>(ctx, gmem, gmem)
-                                              : resident_plan<float>(ctx, gmem, gmem);
+    // AUTO: the shared-memory resident kernel while each CTA owns at most
+    // kAutoResidentRows rows, else the fused streaming list (measured on
+    // B200, profiles/r01_summary.md: at 640x480 and beyond the streaming
+    // march beats every resident variant).  RESIDENT: shared-memory or
+    // (float32) register frames; the GMEM / REG engines on request only.
+    const PlanWant want = cfg->engine == EVR_ENGINE_RESIDENT_GMEM ? WANT_GMEM
+                          : cfg->engine == EVR_ENGINE_RESIDENT_REG ? WANT_REG
+                          : cfg->engine == EVR_ENGINE_RESIDENT    ? WANT_SMEM_OR_REG
+                                                                  : WANT_SMEM;
+    bool ok = ctx->prec == EVR_PREC_F64 ? resident_plan<double>(ctx, want)
+                                        : resident_plan<float>(ctx, want);
+    if (ok && cfg->engine == EVR_ENGINE_AUTO && ctx->r_R > kAutoResidentRows) ok = false;
     if (ok) {
       ctx->engine = ctx->r_ms == PLANES_GMEM ? EVR_ENGINE_RESIDENT_GMEM
                     : ctx->r_ms == PLANES_REG ? EVR_ENGINE_RESIDENT_REG
                                               : EVR_ENGINE_RESIDENT;
       int rc = ctx->prec == EVR_PREC_F64 ? resident_alloc<double>(ctx) : resident_alloc<float>(ctx);
       if (rc) return rc;
-    } else if (cfg->engine == EVR_ENGINE_RESIDENT) {
-      return fail(ctx, EVR_ERR_UNSUPPORTED, "resident engine does not fit a %dx%d sensor", ctx->W,
-                  ctx->H);
+    } else if (cfg->engine != EVR_ENGINE_AUTO) {
+      return fail(ctx, EVR_ERR_UNSUPPORTED, "engine %d does not fit a %dx%d sensor", cfg->engine,
+                  ctx->W, ctx->H);
     }
   }
   return EVR_OK;

@@ -220,7 +220,7 @@ __global__ void k_pd_primal(const T* __restrict__ p1, const T* __restrict__ p2,
   const T uk = u[k];
   const T nu = kl_primal(d, uk, beta[k], fb[k], tau, umin, umax);
   un[k] = nu;
-  v[k] = nu * T(2) - uk;
+  v[k] = Arith<T>::mad(nu, T(2), -uk);
 }
 
 // ROF primal half-step + over-relaxation (solve.py:283-291); beta holds
@@ -236,7 +236,7 @@ __global__ void k_rof_primal(const T* __restrict__ p1, const T* __restrict__ p2,
   const T uk = u[k];
   const T nu = rof_primal(d, uk, wf[k], inv[k], tau);
   un[k] = nu;
-  v[k] = nu * T(2) - uk;
+  v[k] = Arith<T>::mad(nu, T(2), -uk);
 }
 
 // dual ascent + ball projection (solve.py:170-201)
@@ -428,7 +428,7 @@ k_pd_march(const Q4<T>* __restrict__ in, M m, Q4<T>* __restrict__ out, int H, in
       const T d = div_at(qx, j > 0 ? qxl : T(0), qy, r > 0 ? qy_up : T(0), r, j, H, W);
       const T uk = q[rr].w;
       nu = kl_primal(d, uk, beta, fb, tau, umin, umax);
-      v = nu * T(2) - uk;
+      v = Arith<T>::mad(nu, T(2), -uk);
     }
     const T vr = __shfl_down_sync(0xffffffffu, v_up, 1);
     if (rr >= 2 && r - 1 < H && s.own) {

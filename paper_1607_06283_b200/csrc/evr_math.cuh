@@ -3,8 +3,9 @@
 //
 // Each function is one pixel's worth of a reference stage, written in the
 // reference's exact operation order.  The translation
-// unit is compiled with -fmad=false, so with T = double every result is
-// bit-identical to numpy float64: IEEE div.rn / sqrt.rn, no contraction.
+// unit is compiled with -fmad=false and every binary64 a*b+c is spelled
+// __dmul_rn + __dadd_rn, so with T = double every result is bit-identical to
+// numpy float64: IEEE div.rn / sqrt.rn, no contraction.
 // Scalars (tau, sigma, tau*lam, c+-, ...) come from the host already
 // rounded exactly as the reference computes them; none is re-derived here.
 #pragma once
@@ -25,12 +26,22 @@ template <class T> __device__ __forceinline__ T vclip(T x, T lo, T hi) {
 // (MUFU-based, ~2 ulp), which keep the float engine well inside its 1e-4
 // log-intensity tolerance at a fraction of the instruction count.
 template <class T> struct Arith;
+//
+// mad(a, b, c) is the reference's `a * b + c`: binary64 rounds the product
+// and the sum separately (numpy never fuses), binary32 issues one FFMA --
+// half the FP instructions of the iteration kernels, and more accurate.
 template <> struct Arith<double> {
   static __device__ __forceinline__ double div(double a, double b) { return a / b; }
   static __device__ __forceinline__ double sqrt(double x) { return ::sqrt(x); }
+  static __device__ __forceinline__ double mad(double a, double b, double c) {
+    return __dadd_rn(__dmul_rn(a, b), c);
+  }
 };
 template <> struct Arith<float> {
   static __device__ __forceinline__ float div(float a, float b) { return __fdividef(a, b); }
+  static __device__ __forceinline__ float mad(float a, float b, float c) {
+    return __fmaf_rn(a, b, c);
+  }
   static __device__ __forceinline__ float sqrt(float x) {
     float r;
     asm("sqrt.approx.f32 %0, %1;" : "=f"(r) : "f"(x));
@@ -44,9 +55,9 @@ template <class T> struct Coef { T a11, a12, a22, a31, a32; };
 template <class T>
 __device__ __forceinline__ Coef<T> coeffs_of(T tx, T ty, T G) {
   Coef<T> c;
-  c.a11 = Arith<T>::div(T(1) + ty * ty, G);
+  c.a11 = Arith<T>::div(Arith<T>::mad(ty, ty, T(1)), G);
   c.a12 = Arith<T>::div(-(tx * ty), G);
-  c.a22 = Arith<T>::div(T(1) + tx * tx, G);
+  c.a22 = Arith<T>::div(Arith<T>::mad(tx, tx, T(1)), G);
   c.a31 = Arith<T>::div(tx, G);
   c.a32 = Arith<T>::div(ty, G);
   return c;
@@ -54,7 +65,7 @@ __device__ __forceinline__ Coef<T> coeffs_of(T tx, T ty, T G) {
 
 // compute_metric (surface.py:202-205): G = 1 + tx*tx + ty*ty, left to right
 template <class T> __device__ __forceinline__ T metric_G(T tx, T ty) {
-  return T(1) + tx * tx + ty * ty;
+  return Arith<T>::mad(ty, ty, Arith<T>::mad(tx, tx, T(1)));
 }
 
 // float32 metric matrix and sqrt(G) of one pixel from its surface slopes,
@@ -68,9 +79,9 @@ __device__ __forceinline__ MetricPx metric_px(float tx, float ty) {
   const float G = metric_G(tx, ty);
   const float r = Arith<float>::div(1.0f, G);  // MUFU.RCP(G)
   MetricPx m;
-  m.c.a11 = (1.0f + ty * ty) * r;
+  m.c.a11 = Arith<float>::mad(ty, ty, 1.0f) * r;
   m.c.a12 = -(tx * ty) * r;
-  m.c.a22 = (1.0f + tx * tx) * r;
+  m.c.a22 = Arith<float>::mad(tx, tx, 1.0f) * r;
   m.c.a31 = tx * r;
   m.c.a32 = ty * r;
   m.sg = Arith<float>::sqrt(G);
@@ -101,24 +112,24 @@ __device__ __forceinline__ T div_at(T qx_c, T qx_l, T qy_c, T qy_u, int i, int j
 // _Loop.descent_point q = A^T p (solve.py:149-158)
 template <class T>
 __device__ __forceinline__ void q_of(const Coef<T>& c, T p1, T p2, T p3, T& qx, T& qy) {
-  qx = c.a11 * p1 + c.a12 * p2 + c.a31 * p3;
-  qy = c.a12 * p1 + c.a22 * p2 + c.a32 * p3;
+  qx = Arith<T>::mad(c.a31, p3, Arith<T>::mad(c.a12, p2, c.a11 * p1));
+  qy = Arith<T>::mad(c.a32, p3, Arith<T>::mad(c.a22, p2, c.a12 * p1));
 }
 
 // primal_dual_solve KL prox (solve.py:235-242): t1 = div*tau + u;
 // s = t1 - beta; clip((s + sqrt(s*s + 4 beta f)) * 0.5)
 template <class T>
 __device__ __forceinline__ T kl_primal(T divq, T u, T beta, T fb, T tau, T umin, T umax) {
-  const T t1 = divq * tau + u;
+  const T t1 = Arith<T>::mad(divq, tau, u);
   const T s = t1 - beta;
-  const T r = (s + Arith<T>::sqrt(s * s + fb)) * T(0.5);
+  const T r = (s + Arith<T>::sqrt(Arith<T>::mad(s, s, fb))) * T(0.5);
   return vclip(r, umin, umax);
 }
 
 // rof_manifold_solve primal (solve.py:285-287): ((div*tau + u) + wf) * inv
 template <class T>
 __device__ __forceinline__ T rof_primal(T divq, T u, T wf, T inv, T tau) {
-  return (divq * tau + u + wf) * inv;
+  return (Arith<T>::mad(divq, tau, u) + wf) * inv;
 }
 
 // _Loop.dual_ascent (solve.py:175-201) at one pixel; gx, gy are the forward
@@ -128,10 +139,10 @@ __device__ __forceinline__ void dual_step(const Coef<T>& c, T sigma, T gx, T gy,
                                           T& p1, T& p2, T& p3) {
   const T s11 = sigma * c.a11, s12 = sigma * c.a12, s22 = sigma * c.a22;
   const T s31 = sigma * c.a31, s32 = sigma * c.a32;
-  const T q1 = p1 + s11 * gx + s12 * gy;
-  const T q2 = p2 + s12 * gx + s22 * gy;
-  const T q3 = p3 + s31 * gx + s32 * gy;
-  T n = Arith<T>::sqrt(q1 * q1 + q2 * q2 + q3 * q3);
+  const T q1 = Arith<T>::mad(s12, gy, Arith<T>::mad(s11, gx, p1));
+  const T q2 = Arith<T>::mad(s22, gy, Arith<T>::mad(s12, gx, p2));
+  const T q3 = Arith<T>::mad(s32, gy, Arith<T>::mad(s31, gx, p3));
+  T n = Arith<T>::sqrt(Arith<T>::mad(q3, q3, Arith<T>::mad(q2, q2, q1 * q1)));
   if (sqrtG != T(1)) n = Arith<T>::div(n, sqrtG);  // x / 1 == x exactly
   n = vmax(n, T(1));
   if (n != T(1)) {  // interior point: p / 1 == p exactly
@@ -148,9 +159,9 @@ __device__ __forceinline__ void dual_step(const Coef<T>& c, T sigma, T gx, T gy,
 // denoise_timestamps dual ascent + unit-ball projection (surface.py:168-183)
 template <class T>
 __device__ __forceinline__ void tv_dual_step(T dx, T dy, T sigma, T& px, T& py) {
-  const T a = px + dx * sigma;
-  const T b = py + dy * sigma;
-  const T n = vmax(Arith<T>::sqrt(a * a + b * b), T(1));
+  const T a = Arith<T>::mad(dx, sigma, px);
+  const T b = Arith<T>::mad(dy, sigma, py);
+  const T n = vmax(Arith<T>::sqrt(Arith<T>::mad(b, b, a * a)), T(1));
   if (n != T(1)) {
     px = Arith<T>::div(a, n);
     py = Arith<T>::div(b, n);
@@ -164,10 +175,10 @@ __device__ __forceinline__ void tv_dual_step(T dx, T dy, T sigma, T& px, T& py) 
 // returns u+, writes the over-relaxed u_bar = u+ * 2 - u
 template <class T>
 __device__ __forceinline__ T tv_primal_step(T divp, T u, T f0, T tau, T shrink, T& ubar) {
-  const T t1 = divp * tau + u;
+  const T t1 = Arith<T>::mad(divp, tau, u);
   const T g = vclip(t1 - f0, -shrink, shrink);
   const T un = t1 - g;
-  ubar = un * T(2) - u;
+  ubar = Arith<T>::mad(un, T(2), -u);  // un * 2 is exact: same bits either way
   return un;
 }
 

@@ -538,7 +538,7 @@ __global__ void __launch_bounds__(NT, 1) k_resident(const ResArgs<T> a) {
           const T d = div_at(qxc[k], qxl[k], qyc[k + 1], gi > 0 ? qyc[k] : T(0), gi, j, H, W);
           const T uk = uu[k];
           const T nu = kl_primal(d, uk, a.tl * sgv[k], fbv[k], a.tau, a.uminT, a.umaxT);
-          V[r * W + j] = nu * T(2) - uk;
+          V[r * W + j] = Arith<T>::mad(nu, T(2), -uk);
           U[r * W + j] = nu;
           if (last && r <= Rb) {
             const double e = (double)nu - (double)uk;

@@ -417,7 +417,7 @@ __global__ void __launch_bounds__(NT, 1) k_resident_reg(const ResArgs<float> a) 
         const T sg = Arith<T>::sqrt(metric_G(TX[l], TY[l]));
         const T uk = u[cs][r];
         const T nu = kl_primal(d, uk, a.tl * sg, FB[l], a.tau, a.uminT, a.umaxT);
-        V[l] = nu * T(2) - uk;
+        V[l] = Arith<T>::mad(nu, T(2), -uk);
         u[cs][r] = nu;
         if (last && r <= Rb) {
           const double e = (double)nu - (double)uk;

@@ -43,6 +43,7 @@ _PRECISIONS = {"f64": _lib.PREC_F64, "fp64": _lib.PREC_F64, "float64": _lib.PREC
                "f32": _lib.PREC_F32, "fp32": _lib.PREC_F32, "float32": _lib.PREC_F32}
 _ENGINES = {"auto": _lib.ENGINE_AUTO, "streaming": _lib.ENGINE_STREAMING,
             "resident_gmem": _lib.ENGINE_RESIDENT_GMEM,
+            "resident_reg": _lib.ENGINE_RESIDENT_REG,
             "resident": _lib.ENGINE_RESIDENT}
 
 

@@ -231,6 +231,23 @@ def test_float32_chained_u_stream_tolerance():
     assert worst <= LOG_TOL, worst
 
 
+@pytest.mark.parametrize("engine", [0, 1])
+def test_float32_streaming_tolerance_vs_oracle(engine):
+    """float32 fused streaming list (packed state, FFMA, MUFU) at a sensor
+    AUTO sends to it: within the north_star log tolerance, chained."""
+    H, W = 300, 400
+    sc = evr.SolverConfig()
+    st = evr.init_state(evr.SensorGeometry(W, H), sc, precision=1, engine=engine)
+    ref = O.OracleStream(H, W, O.make_config())
+    worst = 0.0
+    for pk in uniform_packets(H, W, 4, 1000, seed=17, t_step=1):
+        _, frame, _ = evr.process_packet(st, pk, evr.ManifoldConfig(), sc, evr.Thresholds())
+        ref.process(np.ascontiguousarray(pk))
+        worst = max(worst, float(np.abs(np.log(frame) - np.log(ref.u)).max()))
+    assert st.engine() == "streaming"
+    assert worst <= LOG_TOL, worst
+
+
 def test_duplicates_and_clamp_order():
     """Multiply-then-clamp per event in stream order."""
     geom = evr.SensorGeometry(4, 3)
@@ -292,12 +309,12 @@ def test_float32_register_engine_matches_streaming_bitwise():
     sc = evr.SolverConfig(max_iterations=20)
     mc = evr.ManifoldConfig(denoise_iterations=10)
     out = {}
-    for eng in ("streaming", "auto"):
+    for eng in ("streaming", "reg"):
         st = evr.init_state(evr.SensorGeometry(W, H), sc, precision=1,
-                            engine={"streaming": 1, "auto": 0}[eng])
+                            engine={"streaming": 1, "reg": 4}[eng])
         for pk in uniform_packets(H, W, 3, 1000, seed=21, t_step=1):
             _, frame, _ = evr.process_packet(st, pk, mc, sc, evr.Thresholds())
         out[eng] = (frame.copy(), st.p.copy(), st.engine())
-    assert out["auto"][2] == "resident_reg"
-    assert np.array_equal(out["auto"][0], out["streaming"][0])
-    assert np.array_equal(out["auto"][1], out["streaming"][1])
+    assert out["reg"][2] == "resident_reg"
+    assert np.array_equal(out["reg"][0], out["streaming"][0])
+    assert np.array_equal(out["reg"][1], out["streaming"][1])
