@@ -21,6 +21,7 @@
 #include "evr_kernels.cuh"
 #include "evr_resident.cuh"
 #include "evr_resident_reg.cuh"
+#include "evr_resident_col.cuh"
 
 using namespace evr;
 
@@ -423,6 +424,28 @@ template <class T> const ResidentKernel<T>* resident_pick(int W, int ms) {
   return nullptr;
 }
 
+// column-per-thread variant (evr_resident_col.cuh): W <= NT, bands of RB rows
+template <class T> struct ResidentColKernel {
+  int nt, rb;
+  void (*fn)(ResArgs<T>);
+};
+template <class T> const ResidentColKernel<T>* resident_col_pick(int W, int R) {
+  static const ResidentColKernel<T> table[] = {
+      {128, 1, k_resident_col<T, 128, 1>}, {128, 2, k_resident_col<T, 128, 2>},
+      {256, 1, k_resident_col<T, 256, 1>}, {256, 2, k_resident_col<T, 256, 2>},
+      {384, 1, k_resident_col<T, 384, 1>}, {384, 2, k_resident_col<T, 384, 2>},
+      {512, 1, k_resident_col<T, 512, 1>}, {512, 2, k_resident_col<T, 512, 2>},
+  };
+  static const bool off = [] {
+    const char* e = getenv("EVR_RESIDENT_COL");
+    return e && e[0] == '0';
+  }();
+  if (off) return nullptr;
+  for (const auto& k : table)
+    if (W <= k.nt && R == k.rb) return &k;
+  return nullptr;
+}
+
 // float32 register-state variant (evr_resident_reg.cuh): (NT, CS, RM)
 // shapes, a thread per CS columns of a W <= CS*NT sensor, bands <= RM rows
 struct ResidentRegKernel {
@@ -463,9 +486,16 @@ template <class T> bool resident_plan(evr_ctx* ctx, PlanWant want) {
   const size_t rframe = resident_reg_frame_bytes(R, W);
   const bool reg_fits =
       rk && rframe + sizeof(IngestShared<640>) + 64 * sizeof(double) + 1024 <= (size_t)optin;
+  const ResidentColKernel<T>* ck = resident_col_pick<T>(W, R);
+  const size_t csmem = resident_col_smem<T>(R, W);
   int ms, nt_used = nt;
   size_t smem;
-  if (want == WANT_GMEM) {
+  if (want != WANT_GMEM && want != WANT_REG && ck &&
+      csmem + sizeof(IngestShared<512>) + 64 * sizeof(double) + 1024 <= (size_t)optin) {
+    ms = PLANES_COL;
+    smem = csmem;
+    nt_used = ck->nt;
+  } else if (want == WANT_GMEM) {
     ms = PLANES_GMEM;
     smem = 0;
   } else if (want != WANT_REG && smem_fits) {
@@ -508,6 +538,9 @@ template <class T> int resident_alloc(evr_ctx* ctx) {
   if (ctx->r_ms == PLANES_REG) {
     const ResidentRegKernel* rk = resident_reg_pick(ctx->W, ctx->r_R);
     fn = rk ? (const void*)rk->fn : nullptr;
+  } else if (ctx->r_ms == PLANES_COL) {
+    const ResidentColKernel<T>* ck = resident_col_pick<T>(ctx->W, ctx->r_R);
+    fn = ck ? (const void*)ck->fn : nullptr;
   } else {
     const ResidentKernel<T>* k = resident_pick<T>(ctx->W, ctx->r_ms);
     fn = k ? (const void*)k->fn : nullptr;
@@ -580,6 +613,8 @@ template <class T> int resident_enqueue(evr_ctx* ctx, int which) {
     } else {
       return fail(ctx, EVR_ERR_UNSUPPORTED, "register-state resident engine is float32 only");
     }
+  } else if (ctx->r_ms == PLANES_COL) {
+    e = cudaLaunchKernelEx(&lc, resident_col_pick<T>(ctx->W, ctx->r_R)->fn, a);
   } else {
     e = cudaLaunchKernelEx(&lc, resident_pick<T>(ctx->W, ctx->r_ms)->fn, a);
   }

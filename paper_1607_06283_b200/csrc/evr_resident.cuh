@@ -81,7 +81,7 @@ enum : int {
   RP_F64 = RP_V
 };
 
-enum : int { PLANES_SMEM = 0, PLANES_GMEM = 1, PLANES_REG = 2 };
+enum : int { PLANES_SMEM = 0, PLANES_GMEM = 1, PLANES_REG = 2, PLANES_COL = 3 };
 
 __host__ __device__ inline int resident_plane_stride(int R, int W) {
   return ((R + 2) * W + 3) / 4 * 4;
