@@ -22,6 +22,7 @@
 
 #include <cstdint>
 
+#include "evr_fastdp.cuh"
 #include "evr_ingest.cuh"
 #include "evr_kernels.cuh"
 #include "evr_math.cuh"
@@ -39,6 +40,11 @@ template <class T> __host__ __device__ inline size_t resident_col_smem(int RB, i
 template <class T, int NT, int RB>
 __global__ void __launch_bounds__(NT, 1) k_resident_col(const ResArgs<T> a) {
   constexpr int NR = RB + 2;  // local rows: 0 = halo above, 1..RB own, RB+1 = halo below
+  constexpr bool kFast = sizeof(T) == 8;  // float64: branch-free fast paths (evr_fastdp.cuh)
+#ifndef EVR_SKIP_UNIT
+#define EVR_SKIP_UNIT 1
+#endif
+  constexpr bool kSkipUnit = EVR_SKIP_UNIT;  // skip p / 1 when the whole warp is inside the ball
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ double red[64];
   const int tid = threadIdx.x;
@@ -214,14 +220,46 @@ __global__ void __launch_bounds__(NT, 1) k_resident_col(const ResArgs<T> a) {
         for (int r = 0; r <= RB; ++r) XB[r * W + j] = tub[r];
       }
       __syncthreads();
+      {
+        // every row branch-free (rows past the band compute unused values),
+        // so the rows' latency chains overlap; float64 fast paths with a
+        // rare IEEE redo (evr_fastdp.cuh)
+        T dx[RB + 1], dy[RB + 1], nx[RB + 1], ny[RB + 1], nn[RB + 1];
+        bool slow = false, proj = false;
 #pragma unroll
-      for (int r = 0; r <= RB; ++r) {
-        if (r > Rb) continue;
-        const T ubr = XB[r * W + jr];
-        const T dx = j < W - 1 ? ubr - tub[r] : T(0);
-        const T dy = r0 - 1 + r < H - 1 ? tub[r + 1] - tub[r] : T(0);
-        tv_dual_step(dx, dy, a.tv_step, px[r], py[r]);
-        if (col) XA[r * W + j] = px[r];
+        for (int r = 0; r <= RB; ++r) {
+          const T ubr = XB[r * W + jr];
+          dx[r] = j < W - 1 ? ubr - tub[r] : T(0);
+          dy[r] = r0 - 1 + r < H - 1 ? tub[r + 1] - tub[r] : T(0);
+          nx[r] = px[r];
+          ny[r] = py[r];
+          if constexpr (kFast) {
+            nn[r] = tv_dual_pre_fx(dx[r], dy[r], a.tv_step, nx[r], ny[r], slow);
+            proj |= nn[r] != T(1);
+          } else {
+            tv_dual_step(dx[r], dy[r], a.tv_step, nx[r], ny[r]);
+          }
+        }
+        if constexpr (kFast) {
+          if (!kSkipUnit || __any_sync(0xffffffffu, proj)) {  // warp-uniform: x / 1 == x otherwise
+#pragma unroll
+            for (int r = 0; r <= RB; ++r) fdp_div2(nx[r], ny[r], nn[r], slow);
+          }
+        }
+        if (kFast && slow) {
+#pragma unroll
+          for (int r = 0; r <= RB; ++r) {
+            nx[r] = px[r];
+            ny[r] = py[r];
+            tv_dual_step(dx[r], dy[r], a.tv_step, nx[r], ny[r]);
+          }
+        }
+#pragma unroll
+        for (int r = 0; r <= RB; ++r) {
+          px[r] = nx[r];
+          py[r] = ny[r];
+          if (col) XA[r * W + j] = px[r];
+        }
       }
       __syncthreads();
 #pragma unroll
@@ -330,41 +368,87 @@ __global__ void __launch_bounds__(NT, 1) k_resident_col(const ResArgs<T> a) {
       for (int r = 1; r < NR; ++r) XA[r * W + j] = qx[r];
     }
     __syncthreads();
-    // KL prox + over-relaxation (solve.py:234-252)
+    // KL prox + over-relaxation (solve.py:234-252), all rows branch-free
+    {
+      T d[NR], nu[NR];
+      bool slow = false;
 #pragma unroll
-    for (int r = 1; r < NR; ++r) {
-      if (r > hi) continue;
-      const int gi = r0 - 1 + r;
-      const T qxl = XA[r * W + jl];
-      const T d = div_at(qx[r], j > 0 ? qxl : T(0), qy[r], gi > 0 ? qy[r - 1] : T(0), gi, j, H, W);
-      const T uk = u[r];
-      const T nu = kl_primal(d, uk, a.tl * sg[r], fb[r], a.tau, a.uminT, a.umaxT);
-      v[r] = Arith<T>::mad(nu, T(2), -uk);
-      u[r] = nu;
-      if (last && r <= Rb && col) {
-        const double e = (double)nu - (double)uk;
-        rd += e * e;
-        ro += (double)uk * (double)uk;
+      for (int r = 1; r < NR; ++r) {
+        const int gi = r0 - 1 + r;
+        const T qxl = XA[r * W + jl];
+        d[r] = div_at(qx[r], j > 0 ? qxl : T(0), qy[r], gi > 0 ? qy[r - 1] : T(0), gi, j, H, W);
+        if constexpr (kFast)
+          nu[r] = kl_primal_fx(d[r], u[r], a.tl * sg[r], fb[r], a.tau, a.uminT, a.umaxT, slow);
+        else
+          nu[r] = kl_primal(d[r], u[r], a.tl * sg[r], fb[r], a.tau, a.uminT, a.umaxT);
       }
-      if (col) XB[r * W + j] = v[r];
+      if (kFast && slow) {
+#pragma unroll
+        for (int r = 1; r < NR; ++r)
+          nu[r] = kl_primal(d[r], u[r], a.tl * sg[r], fb[r], a.tau, a.uminT, a.umaxT);
+      }
+#pragma unroll
+      for (int r = 1; r < NR; ++r) {
+        const T uk = u[r];
+        v[r] = Arith<T>::mad(nu[r], T(2), -uk);
+        u[r] = nu[r];
+        if (last && r <= Rb && col) {
+          const double e = (double)nu[r] - (double)uk;
+          rd += e * e;
+          ro += (double)uk * (double)uk;
+        }
+        if (col) XB[r * W + j] = v[r];
+      }
     }
     mark();
     __syncthreads();
     mark();
     // dual ascent + ball projection (solve.py:170-201); boundary rows go out
     // to the neighbours as soon as they are computed
+    {
+      T gx[RB + 1], gy[RB + 1], n1[RB + 1], n2[RB + 1], n3[RB + 1], nn[RB + 1];
+      bool slow = false, proj = false;
 #pragma unroll
-    for (int r = 1; r <= RB; ++r) {
-      if (r > Rb) continue;
-      const T vr = XB[r * W + jr];
-      const T gx = j < W - 1 ? vr - v[r] : T(0);
-      const T gy = r0 - 1 + r < H - 1 ? v[r + 1] - v[r] : T(0);
-      dual_step(c[r], a.sigma, gx, gy, sg[r], p1[r], p2[r], p3[r]);
-      q_of(c[r], p1[r], p2[r], p3[r], qx[r], qy[r]);
-      if (!last && col) {
-        ll_put(step + 1, r, 0, p1[r]);
-        ll_put(step + 1, r, 1, p2[r]);
-        ll_put(step + 1, r, 2, p3[r]);
+      for (int r = 1; r <= RB; ++r) {
+        const T vr = XB[r * W + jr];
+        gx[r] = j < W - 1 ? vr - v[r] : T(0);
+        gy[r] = r0 - 1 + r < H - 1 ? v[r + 1] - v[r] : T(0);
+        n1[r] = p1[r];
+        n2[r] = p2[r];
+        n3[r] = p3[r];
+        if constexpr (kFast) {
+          nn[r] = dual_pre_fx(c[r], a.sigma, gx[r], gy[r], sg[r], n1[r], n2[r], n3[r], slow);
+          proj |= nn[r] != T(1);
+        } else {
+          dual_step(c[r], a.sigma, gx[r], gy[r], sg[r], n1[r], n2[r], n3[r]);
+        }
+      }
+      if constexpr (kFast) {
+        if (!kSkipUnit || __any_sync(0xffffffffu, proj)) {  // warp-uniform: q / 1 == q otherwise
+#pragma unroll
+          for (int r = 1; r <= RB; ++r) fdp_div3(n1[r], n2[r], n3[r], nn[r], slow);
+        }
+      }
+      if (kFast && slow) {
+#pragma unroll
+        for (int r = 1; r <= RB; ++r) {
+          n1[r] = p1[r];
+          n2[r] = p2[r];
+          n3[r] = p3[r];
+          dual_step(c[r], a.sigma, gx[r], gy[r], sg[r], n1[r], n2[r], n3[r]);
+        }
+      }
+#pragma unroll
+      for (int r = 1; r <= RB; ++r) {
+        p1[r] = n1[r];
+        p2[r] = n2[r];
+        p3[r] = n3[r];
+        q_of(c[r], p1[r], p2[r], p3[r], qx[r], qy[r]);
+        if (!last && col && r <= Rb) {
+          ll_put(step + 1, r, 0, p1[r]);
+          ll_put(step + 1, r, 1, p2[r]);
+          ll_put(step + 1, r, 2, p3[r]);
+        }
       }
     }
     mark();
