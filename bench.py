@@ -360,8 +360,9 @@ def run_gpu(args):
             "gpu_launches": int(launches),
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
                          "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": traffic,
-                         "kernel": "whole packet" if st.engine() != "resident" else
-                                   "evr::k_resident (one launch per packet)",
+                         "kernel": ctx.engine_detail() + (
+                             " (one launch per packet)" if st.engine().startswith("resident")
+                             else " (whole packet graph)"),
                          "algorithmic_bytes_per_launch": bpkt,
                          "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback"},
             "clocks": clocks.summary(),

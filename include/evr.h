@@ -101,6 +101,9 @@ const char *evr_last_error(const evr_ctx *ctx);
 int evr_set_config(evr_ctx *ctx, const evr_config *cfg);
 /* engine actually used by the per-packet path (after AUTO resolution) */
 int evr_active_engine(evr_ctx *ctx, int *engine);
+/* human-readable kernel shape of the per-packet path, e.g.
+ * "k_resident_col<f64,NT=384,RB=2> x130 CTAs" (NUL-terminated, truncated) */
+int evr_engine_detail(evr_ctx *ctx, char *buf, int len);
 
 /* ---- stream state: ReconstructionState (pipeline.py:87-111) ------------- */
 /* init_state (pipeline.py:102-111): u = f = (u_min+u_max)/2, raw = 0, p = 0 */
@@ -143,6 +146,12 @@ int evr_packet_solve(evr_ctx *ctx, evr_solve_info *info, double *energy_trace,
 int evr_synchronize(evr_ctx *ctx, evr_solve_info *info);
 /* Current frame u (the value process_packet returns), float64 (H, W). */
 int evr_get_frame(evr_ctx *ctx, double *u_out);
+/* evr_get_frame enqueued on the context stream without waiting (complete
+ * after evr_synchronize); asynchronous when u_out is pinned host memory */
+int evr_get_frame_async(evr_ctx *ctx, double *u_out);
+/* page-locked host buffers for frames / events (cudaHostAlloc) */
+int evr_host_alloc(size_t bytes, void **out);
+int evr_host_free(void *p);
 /* Last packet's denoised surface t and metric determinant G (the
  * debug_sink view, pipeline.py:162-163).  Either pointer may be NULL. */
 int evr_get_surface(evr_ctx *ctx, double *t_out, double *G_out);

@@ -83,6 +83,7 @@ _SIGNATURES = {
     "evr_last_error": ([_P], ctypes.c_char_p),
     "evr_set_config": ([_P, _P], _i32),
     "evr_active_engine": ([_P, _P], _i32),
+    "evr_engine_detail": ([_P, ctypes.c_char_p, _i32], _i32),
     "evr_init_state": ([_P], _i32),
     "evr_set_state": ([_P, _P, _P, _P, _P], _i32),
     "evr_get_state": ([_P, _P, _P, _P, _P], _i32),
@@ -94,6 +95,9 @@ _SIGNATURES = {
     "evr_packet_solve": ([_P, _P, _P, _P], _i32),
     "evr_synchronize": ([_P, _P], _i32),
     "evr_get_frame": ([_P, _P], _i32),
+    "evr_get_frame_async": ([_P, _P], _i32),
+    "evr_host_alloc": ([ctypes.c_size_t, _P], _i32),
+    "evr_host_free": ([_P], _i32),
     "evr_get_surface": ([_P, _P, _P], _i32),
     "evr_get_metric": ([_P, _P, _P, _P, _P], _i32),
     "evr_get_frame_u8": ([_P, _d, _d, _P], _i32),
@@ -187,6 +191,46 @@ def device_count():
     return n.value if rc == EVR_OK else 0
 
 
+class _PinnedBlock:
+    """A page-locked host block (evr_host_alloc); goes back to the pool when
+    the last array viewing it is collected."""
+
+    __slots__ = ("addr", "nbytes")
+
+    def __init__(self, addr, nbytes):
+        self.addr, self.nbytes = addr, nbytes
+
+    def __del__(self):
+        try:
+            with _pinned_lock:
+                _pinned_free.setdefault(self.nbytes, []).append(self.addr)
+        except Exception:  # interpreter shutdown
+            pass
+
+
+_pinned_free: dict = {}
+_pinned_lock = threading.Lock()
+
+
+def pinned_empty(shape, dtype=np.float64):
+    """np.empty in page-locked host memory, from a size-keyed pool, so frame
+    downloads run at full link speed without a staging copy."""
+    dtype = np.dtype(dtype)
+    nbytes = max(1, int(np.prod(shape)) * dtype.itemsize)
+    with _pinned_lock:
+        addrs = _pinned_free.get(nbytes)
+        addr = addrs.pop() if addrs else None
+    if addr is None:
+        out = ctypes.c_void_p()
+        rc = lib().evr_host_alloc(nbytes, ctypes.byref(out))
+        if rc != 0:
+            raise MemoryError(f"evr_host_alloc({nbytes}) failed ({rc})")
+        addr = out.value
+    buf = (ctypes.c_char * nbytes).from_address(addr)
+    buf._block = _PinnedBlock(addr, nbytes)  # lives as long as any view of buf
+    return np.frombuffer(buf, dtype=dtype, count=int(np.prod(shape))).reshape(shape)
+
+
 class Context:
     """Owns one evr_ctx (one sensor shape, one device, one precision)."""
 
@@ -235,6 +279,11 @@ class Context:
         e = ctypes.c_int(0)
         self.call("evr_active_engine", ctypes.byref(e))
         return ENGINE_NAMES.get(e.value, str(e.value))
+
+    def engine_detail(self):
+        buf = ctypes.create_string_buffer(256)
+        self.call("evr_engine_detail", buf, len(buf))
+        return buf.value.decode()
 
     def launch_count(self):
         return int(lib().evr_launch_count(self._h))

@@ -1033,6 +1033,27 @@ int evr_set_config(evr_ctx* ctx, const evr_config* cfg) {
   return EVR_OK;
 }
 
+int evr_engine_detail(evr_ctx* ctx, char* buf, int len) {
+  if (!ctx || !buf || len < 1) return EVR_ERR_INVALID;
+  const char* ty = ctx->prec == EVR_PREC_F64 ? "f64" : "f32";
+  if (ctx->engine == EVR_ENGINE_STREAMING) {
+    if (ctx->banded)
+      snprintf(buf, len, "streaming split half-steps (band rows %d..%d of %d)", ctx->row0,
+               ctx->row0 + ctx->H - 1, ctx->Htot);
+    else
+      snprintf(buf, len, "streaming k_tv_march/k_pd_march<%s,RY=%d> %u CTAs x %d", ty, kMarchRY,
+               march_grid(ctx), kMarchNT);
+  } else {
+    const char* k = ctx->r_ms == PLANES_COL    ? "k_resident_col"
+                    : ctx->r_ms == PLANES_REG  ? "k_resident_reg"
+                    : ctx->r_ms == PLANES_GMEM ? "k_resident(gmem frames)"
+                                               : "k_resident(smem frames)";
+    snprintf(buf, len, "%s<%s,NT=%d,RB=%d> x%d CTAs, %zu B smem", k, ty, ctx->r_nt, ctx->r_R,
+             ctx->r_nb, ctx->r_smem);
+  }
+  return EVR_OK;
+}
+
 int evr_active_engine(evr_ctx* ctx, int* engine) {
   if (!ctx || !engine) return EVR_ERR_INVALID;
   *engine = ctx->engine;
@@ -1173,6 +1194,36 @@ int evr_get_frame(evr_ctx* ctx, double* u_out) {
   if (!u_out) return fail(ctx, EVR_ERR_INVALID, "null output");
   return ctx->prec == EVR_PREC_F64 ? get_plane_t<double>(ctx, F_U, u_out)
                                    : get_plane_t<float>(ctx, F_U, u_out);
+}
+
+int evr_get_frame_async(evr_ctx* ctx, double* u_out) {
+  CHECK_CTX();
+  if (!u_out) return fail(ctx, EVR_ERR_INVALID, "null output");
+  const int64_t N = ctx->own_n(), o = ctx->own_off();
+  const double* src;
+  if (ctx->prec == EVR_PREC_F64) {
+    src = ctx->fld<double>(F_U) + o;
+  } else {
+    k_convert<float, double><<<grid1d(N), kNT, 0, ctx->stream>>>(ctx->fld<float>(F_U) + o,
+                                                                 ctx->aos_a, N);
+    int rc = launch_err(ctx, "get_frame_async");
+    if (rc) return rc;
+    src = ctx->aos_a;
+  }
+  CK(cudaMemcpyAsync(u_out, src, sizeof(double) * N, cudaMemcpyDeviceToHost, ctx->stream));
+  return EVR_OK;
+}
+
+int evr_host_alloc(size_t bytes, void** out) {
+  if (!out) return EVR_ERR_INVALID;
+  *out = nullptr;
+  const cudaError_t e = cudaHostAlloc(out, bytes > 0 ? bytes : 1, cudaHostAllocPortable);
+  return e == cudaSuccess ? EVR_OK : e == cudaErrorMemoryAllocation ? EVR_ERR_OOM : EVR_ERR_CUDA;
+}
+
+int evr_host_free(void* p) {
+  if (p && cudaFreeHost(p) != cudaSuccess) return EVR_ERR_CUDA;
+  return EVR_OK;
 }
 
 int evr_get_surface(evr_ctx* ctx, double* t_out, double* G_out) {

@@ -302,8 +302,15 @@ def process_packet_arrays(state, events, manifold_cfg, solver_cfg, thresholds, t
     window = _window(state, now, manifold_cfg) if manifold_cfg.enabled else 1.0
     info = _lib.SolveInfo()
     split = (debug_sink is not None or trace is not None or solver_cfg.convergence_tol > 0)
+    frame = None
     if not split:
-        ctx.call("evr_process_packet", _lib.ptr(events), n, float(window), ctypes.byref(info))
+        # one round trip: packet, solve and (pinned) frame download on the
+        # context stream, then a single synchronize
+        ctx.call("evr_process_packet_async", _lib.ptr(events), n, float(window))
+        if want_frame:
+            frame = _lib.pinned_empty(state.shape)
+            ctx.call("evr_get_frame_async", _lib.ptr(frame))
+        ctx.call("evr_synchronize", ctypes.byref(info))
     else:
         ctx.call("evr_packet_begin", _lib.ptr(events), n, float(window))
         if debug_sink is not None:
@@ -329,9 +336,9 @@ def process_packet_arrays(state, events, manifold_cfg, solver_cfg, thresholds, t
     if not want_frame:
         return state, None, SolveResult(u=None, p=None, iterations=int(info.iterations),
                                         rel_change=float(info.rel_change))
-    H, W = state.shape
-    frame = np.empty((H, W))
-    ctx.call("evr_get_frame", _lib.ptr(frame))
+    if frame is None:
+        frame = _lib.pinned_empty(state.shape)
+        ctx.call("evr_get_frame", _lib.ptr(frame))
     state._mirror["u"] = frame  # frame aliases state.u, like the reference
     return state, frame, _LazyResult(state, frame, info)
 
