@@ -19,7 +19,7 @@ for x in r[1:]:
 raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
                      text=True).stdout
 r = list(csv.reader(raw.splitlines()))
-for a, b in zip(r[0], r[2]):
+for a, u, b in zip(r[0], r[1], r[2]):
     if a in ("dram__bytes_read.sum", "dram__bytes_write.sum", "lts__t_bytes.sum",
              "smsp__inst_executed.sum", "launch__grid_size", "launch__registers_per_thread"):
-        print(f"{a:28s} {b}")
+        print(f"{a:28s} {b} {u}")
