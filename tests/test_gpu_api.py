@@ -218,3 +218,50 @@ def test_install_reroutes_reference_stream():
     finally:
         evr.uninstall()
     assert fake.process_packet is None
+
+
+def test_engine_detail_names_the_kernel():
+    st = evr.init_state(SensorGeometry(width=346, height=260), SolverConfig())
+    evr.process_packet(st, make_events(50, SensorGeometry(width=346, height=260)),
+                       ManifoldConfig(), SolverConfig(), Thresholds())
+    d = st.context().engine_detail()
+    assert d.startswith("k_resident_col<f64,NT=384,RB=2>") and "x130 CTAs" in d
+    st = evr.init_state(SensorGeometry(width=640, height=480), SolverConfig(), precision=1)
+    evr.process_packet(st, make_events(50, SensorGeometry(width=640, height=480)),
+                       ManifoldConfig(), SolverConfig(), Thresholds())
+    assert st.context().engine_detail().startswith("streaming k_tv_march/k_pd_march<f32")
+
+
+def test_frames_are_fresh_pinned_arrays():
+    """Each packet's frame is a new array (the reference's result.u), served
+    from the pinned pool; an old frame keeps its values after later packets
+    and after being dropped and reallocated."""
+    from paper_1607_06283_b200 import _lib
+
+    st = evr.init_state(GEOM, SolverConfig())
+    ev = make_events(90)
+    _, f1, _ = evr.process_packet(st, ev[:30], ManifoldConfig(), SolverConfig(), Thresholds())
+    keep = f1.copy()
+    _, f2, _ = evr.process_packet(st, ev[30:60], ManifoldConfig(), SolverConfig(), Thresholds())
+    assert f1 is not f2 and np.array_equal(f1, keep) and not np.array_equal(f1, f2)
+    assert f2.flags.writeable and f2.flags.c_contiguous and f2.dtype == np.float64
+    del f1
+    _, f3, _ = evr.process_packet(st, ev[60:], ManifoldConfig(), SolverConfig(), Thresholds())
+    assert np.array_equal(f3, st.u) and not np.array_equal(f2, f3)
+    a = _lib.pinned_empty((3, 5), np.int64)
+    a[:] = 7
+    assert a.sum() == 105
+
+
+def test_get_frame_async_matches_get_frame():
+    from paper_1607_06283_b200 import _lib
+
+    st = evr.init_state(GEOM, SolverConfig(), precision=1)
+    evr.process_packet(st, make_events(40), ManifoldConfig(), SolverConfig(), Thresholds())
+    ctx = st.context()
+    a = np.empty(GEOM.height * GEOM.width)
+    b = _lib.pinned_empty((GEOM.height, GEOM.width))
+    ctx.call("evr_get_frame", _lib.ptr(a))
+    ctx.call("evr_get_frame_async", _lib.ptr(b))
+    ctx.call("evr_synchronize", None)
+    assert np.array_equal(a.reshape(b.shape), b)
