@@ -276,6 +276,26 @@ int evr_op_rof_solve(evr_ctx *ctx, const double *f, const double *tx,
                      const double *ty, const double *G, const double *sqrtG,
                      double lam, int iterations, double *u_out);
 
+/* ---- event simulator: simulate.py:51-103 generate_events - */
+/* Events of a (n, H, W) stack of LOG intensities (the caller takes np.log,
+ * simulate.py:60) with strictly increasing integer frame timestamps, under
+ * thresholds dp, dn > 0; sorted by (t, y, x, polarity) like the reference's
+ * lexsort.  Limits of the packed sort key: H <= 32767, W <= 65535, frame time
+ * span < 2^30 ticks. */
+typedef struct evr_sim evr_sim;
+int evr_sim_create(evr_sim **out, int device);
+void evr_sim_destroy(evr_sim *sim);
+const char *evr_sim_last_error(const evr_sim *sim);
+int evr_sim_generate(evr_sim *sim, const double *log_frames,
+                     const int64_t *frame_timestamps, int n, int H, int W,
+                     double dp, double dn, int64_t *n_events);
+/* copy the generated events out (cap >= n_events) */
+int evr_sim_events(evr_sim *sim, evr_event *out, int64_t cap);
+/* device pointer of the generated events (valid until the next generate or
+ * destroy), for evr_process_packet_device */
+int evr_sim_device_events(evr_sim *sim, const evr_event **dev_events,
+                          int64_t *n);
+
 #ifdef __cplusplus
 }
 #endif

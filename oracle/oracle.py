@@ -285,3 +285,31 @@ class OracleStream:
         self.last_t, self.last_G = t_out, G_out
         self.frame_index += 1
         return it, rel.value
+
+
+def sim_generate(log_frames, frame_ts, dp, dn):
+    """generate_events (simulate.py:51-103) restated per pixel in numpy on a
+    (n, H, W) LOG-intensity stack; returns an (E, 4) int64 array of
+    [t, x, y, polarity] rows in the reference's (t, y, x, polarity) order."""
+    n, h, w = log_frames.shape
+    ref = log_frames[0].copy()
+    yy, xx = np.mgrid[0:h, 0:w]
+    rows = []
+    for k in range(n - 1):
+        l0, l1 = log_frames[k], log_frames[k + 1]
+        t0, t1 = int(frame_ts[k]), int(frame_ts[k + 1])
+        up = np.maximum(np.floor((l1 - ref) / dp + 1e-9).astype(np.int64), 0)
+        down = np.maximum(np.floor((ref - l1) / dn + 1e-9).astype(np.int64), 0)
+        for counts, sign, step in ((up, 1, dp), (down, -1, dn)):
+            for j in range(1, int(counts.max(initial=0)) + 1):
+                m = counts >= j
+                level = ref + j * step if sign > 0 else ref - j * step
+                frac = (level[m] - l0[m]) / (l1[m] - l0[m])
+                t = np.rint(t0 + frac * (t1 - t0)).astype(np.int64)
+                rows.append(np.stack([t, xx[m], yy[m], np.full(t.shape, sign)], axis=1))
+        ref += up * dp - down * dn
+    if not rows:
+        return np.zeros((0, 4), np.int64)
+    ev = np.concatenate(rows).astype(np.int64)
+    order = np.lexsort((ev[:, 3], ev[:, 1], ev[:, 2], ev[:, 0]))
+    return ev[order]

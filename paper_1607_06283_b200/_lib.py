@@ -98,6 +98,12 @@ _SIGNATURES = {
     "evr_get_frame_async": ([_P, _P], _i32),
     "evr_host_alloc": ([ctypes.c_size_t, _P], _i32),
     "evr_host_free": ([_P], _i32),
+    "evr_sim_create": ([_P, _i32], _i32),
+    "evr_sim_destroy": ([_P], None),
+    "evr_sim_last_error": ([_P], ctypes.c_char_p),
+    "evr_sim_generate": ([_P, _P, _P, _i32, _i32, _i32, _d, _d, _P], _i32),
+    "evr_sim_events": ([_P, _P, _i64], _i32),
+    "evr_sim_device_events": ([_P, _P, _P], _i32),
     "evr_get_surface": ([_P, _P, _P], _i32),
     "evr_get_metric": ([_P, _P, _P, _P, _P], _i32),
     "evr_get_frame_u8": ([_P, _d, _d, _P], _i32),
