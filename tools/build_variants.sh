@@ -8,6 +8,6 @@ for spec in "$@"; do
   name=${spec%%:*}; defs=${spec#*:}
   /usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -lineinfo \
     -fmad=false -Xcompiler -fPIC,-O2 --expt-relaxed-constexpr $defs -shared \
-    -o ../../build_variants/$name.so evr_capi.cu evr_events.cpp -lcudart 2>&1 | grep -iE "error" &
+    -o ../../build_variants/$name.so evr_capi.cu evr_simulate.cu evr_events.cpp -lcudart 2>&1 | grep -iE "error" &
 done
 wait
