@@ -124,21 +124,29 @@ __global__ void __launch_bounds__(NT, 1) k_resident_col(const ResArgs<T> a) {
     const bool on[2] = {has_up, has_dn};
     unsigned long long w[2][3][NWD];
     bool ready;
-    // Large grids exchanging the float64 dual: spin on one word per side
-    // (the last one the neighbour stores), then read and check them all --
-    // polling every word puts ~12 loads per thread per round on L2 and slows
-    // the very stores being waited for.  Light exchanges poll everything at
-    // once (one round trip fewer).  Measured on B200: C2 f64 0.299 -> 0.282
-    // ms with, C1 / float32 slower with.
     if (kSentinelPoll && nf * NWD >= 6 && a.nb * W >= 32768) {
+      // Large grids exchanging the float64 dual: spin on one word per side
+      // (the last one the neighbour stores), then read and check them all --
+      // polling every word puts ~12 loads per thread per round on L2 and
+      // slows the very stores being waited for.  Light exchanges poll
+      // everything at once (one round trip fewer).  Measured on B200: C2 f64
+      // 0.299 -> 0.282 ms with; C1 / float32 slower with, and slower still
+      // with one polling lane per warp.
       do {
         ready = true;
 #pragma unroll
         for (int s = 0; s < 2; ++s)
-          if (on[s])
+          if (on[s] && col)
             ready &= (unsigned)(ld_relaxed_u64(src[s] + ((size_t)(nf - 1) * W + j) * NWD +
                                                (NWD - 1)) >> 32) == want;
       } while (!ready);
+    }
+    if (!col) {
+#pragma unroll
+      for (int s = 0; s < 2; ++s)
+#pragma unroll
+        for (int f = 0; f < 3; ++f) v[s][f] = T(0);
+      return;
     }
     do {
       ready = true;
@@ -228,7 +236,7 @@ __global__ void __launch_bounds__(NT, 1) k_resident_col(const ResArgs<T> a) {
     }
     for (int it = 0; it < a.tv_iters; ++it) {
       const bool pub = it < a.tv_iters - 1;
-      if (it > 0 && col) {
+      if (it > 0) {
         T h[2][3];
         ll_fetch(step, 1, h);
         tub[0] = h[0][0];
@@ -370,7 +378,7 @@ __global__ void __launch_bounds__(NT, 1) k_resident_col(const ResArgs<T> a) {
   double rd = 0.0, ro = 0.0;
   for (int it = 0; it < a.pd_iters; ++it) {
     const bool last = it == a.pd_iters - 1;
-    if (it > 0 && col) {  // p of the previous step on the halo rows (+ their q)
+    if (it > 0) {  // p of the previous step on the halo rows (+ their q)
       T h[2][3];
       ll_fetch(step, 3, h);
       p1[0] = h[0][0];
