@@ -30,6 +30,28 @@
 
 namespace evr {
 
+// the NWD tagged words of one boundary value in one access (16 B for double)
+template <int NWD>
+__device__ __forceinline__ void st_words(unsigned long long* d, const unsigned long long* w) {
+  if constexpr (NWD == 2) {
+    asm volatile("st.relaxed.gpu.global.v2.u64 [%0], {%1, %2};" ::"l"(d), "l"(w[0]), "l"(w[1])
+                 : "memory");
+  } else {
+    st_relaxed_u64(d, w[0]);
+  }
+}
+template <int NWD>
+__device__ __forceinline__ void ld_words(const unsigned long long* s, unsigned long long* w) {
+  if constexpr (NWD == 2) {
+    asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];"
+                 : "=l"(w[0]), "=l"(w[1])
+                 : "l"(s)
+                 : "memory");
+  } else {
+    w[0] = ld_relaxed_u64(s);
+  }
+}
+
 // dynamic shared memory of k_resident_col: f (binary64), the normalised
 // surface, and two row-exchange planes, each (RB + 2) x W
 template <class T> __host__ __device__ inline size_t resident_col_smem(int RB, int W) {
@@ -45,6 +67,9 @@ __global__ void __launch_bounds__(NT, 1) k_resident_col(const ResArgs<T> a) {
 #define EVR_SKIP_UNIT 1
 #endif
   constexpr bool kSkipUnit = EVR_SKIP_UNIT;  // skip p / 1 when the whole warp is inside the ball
+#ifndef EVR_POLL_SLEEP
+#define EVR_POLL_SLEEP 0
+#endif
 #ifndef EVR_SENTINEL_POLL
 #define EVR_SENTINEL_POLL 1
 #endif
@@ -105,13 +130,11 @@ __global__ void __launch_bounds__(NT, 1) k_resident_col(const ResArgs<T> a) {
     unsigned long long* base = xw + (step & 1) * xslot + (size_t)b * 2 * xside;
     if (r == 1) {
       unsigned long long* d = base + ((size_t)field * W + j) * NWD;
-#pragma unroll
-      for (int k = 0; k < NWD; ++k) st_relaxed_u64(d + k, w[k]);
+      st_words<NWD>(d, w);
     }
     if (r == Rb) {
       unsigned long long* d = base + xside + ((size_t)field * W + j) * NWD;
-#pragma unroll
-      for (int k = 0; k < NWD; ++k) st_relaxed_u64(d + k, w[k]);
+      st_words<NWD>(d, w);
     }
   };
   // the neighbours' boundary values of `step` for this column: v[0][f] from
@@ -139,6 +162,7 @@ __global__ void __launch_bounds__(NT, 1) k_resident_col(const ResArgs<T> a) {
           if (on[s] && col)
             ready &= (unsigned)(ld_relaxed_u64(src[s] + ((size_t)(nf - 1) * W + j) * NWD +
                                                (NWD - 1)) >> 32) == want;
+        if (EVR_POLL_SLEEP > 0 && !ready) __nanosleep(EVR_POLL_SLEEP);
       } while (!ready);
     }
     if (!col) {
@@ -156,13 +180,12 @@ __global__ void __launch_bounds__(NT, 1) k_resident_col(const ResArgs<T> a) {
 #pragma unroll
         for (int f = 0; f < 3; ++f) {
           if (f >= nf) break;
+          ld_words<NWD>(src[s] + ((size_t)f * W + j) * NWD, w[s][f]);
 #pragma unroll
-          for (int q = 0; q < NWD; ++q) {
-            w[s][f][q] = ld_relaxed_u64(src[s] + ((size_t)f * W + j) * NWD + q);
-            ready &= (unsigned)(w[s][f][q] >> 32) == want;
-          }
+          for (int q = 0; q < NWD; ++q) ready &= (unsigned)(w[s][f][q] >> 32) == want;
         }
       }
+      if (EVR_POLL_SLEEP > 0 && !ready) __nanosleep(EVR_POLL_SLEEP);
     } while (!ready);
 #pragma unroll
     for (int s = 0; s < 2; ++s)

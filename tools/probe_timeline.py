@@ -46,3 +46,20 @@ for r in [rows[0], rows[len(rows) // 2], rows[-1]]:
     print(f"{cfgname} f{'64' if prec == 0 else '32'} CTA {r:3d}: ingest {m[1]-m[0]:.2f} | TV/it {tvd.mean():.2f} "
           f"| metric {m[k] - m[k-1]:.2f} (+{m[k+1]-m[k]:.2f}) | PD/it {np.diff(pdm[:, 0]).mean():.2f} = "
           f"fetch {fetch.mean():.2f} + primal {primal.mean():.2f} (t0 {primal0.mean():.2f} bar {pbar.mean():.2f}) + dual {dual.mean():.2f} | end {m[k+2+4*pd]:.1f} us")
+
+# neighbour handoff: fetch done (CTA r, iteration i) minus the later of the two
+# neighbours' "dual issued" marks of iteration i-1 (thread 0 = column 0 both)
+k = 2 + tv
+eff = []
+for r in rows[1:-1]:
+    a = (tr[r] - t0)[k + 2:k + 2 + 4 * pd].reshape(pd, 4) / 1e3
+    up = (tr[r - 1] - t0)[k + 2:k + 2 + 4 * pd].reshape(pd, 4) / 1e3
+    dn = (tr[r + 1] - t0)[k + 2:k + 2 + 4 * pd].reshape(pd, 4) / 1e3
+    own = a[:-1, 3]
+    nb = np.maximum(up[:-1, 3], dn[:-1, 3])
+    eff.append((a[1:, 0] - nb, a[1:, 0] - own, nb - own))
+L = np.concatenate([e[0] for e in eff])
+W8 = np.concatenate([e[1] for e in eff])
+S = np.concatenate([e[2] for e in eff])
+print(f"handoff after the later neighbour's put: median {np.median(L):.2f} us (p10 {np.percentile(L, 10):.2f}, p90 {np.percentile(L, 90):.2f}); "
+      f"own wait {np.median(W8):.2f} us; neighbour lag behind own put {np.median(S):.2f} us")
