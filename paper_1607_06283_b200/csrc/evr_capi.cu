@@ -528,7 +528,8 @@ template <class T> int resident_alloc(evr_ctx* ctx) {
   ctx->d_frames = nullptr;
   CK(cudaMalloc(&ctx->d_flags, sizeof(unsigned long long) * ctx->r_nb));
   CK(cudaMemset(ctx->d_flags, 0, sizeof(unsigned long long) * ctx->r_nb));
-  const size_t xbytes = sizeof(unsigned long long) * LLWords<T>::N * 2 * ctx->r_nb * 2 * 3 * (size_t)ctx->W;
+  // 4 slots per column: the plane-frame kernel uses 3, k_resident_col 4
+  const size_t xbytes = sizeof(unsigned long long) * LLWords<T>::N * 2 * ctx->r_nb * 2 * 4 * (size_t)ctx->W;
   CK(cudaMalloc(&ctx->d_xchg, xbytes));
   CK(cudaMemset(ctx->d_xchg, 0, xbytes));  // no stale tag can match a live one
   CK(cudaMalloc(&ctx->d_ticket, sizeof(unsigned)));

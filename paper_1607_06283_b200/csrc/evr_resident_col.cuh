@@ -30,25 +30,48 @@
 
 namespace evr {
 
-// the NWD tagged words of one boundary value in one access (16 B for double)
-template <int NWD>
-__device__ __forceinline__ void st_words(unsigned long long* d, const unsigned long long* w) {
-  if constexpr (NWD == 2) {
-    asm volatile("st.relaxed.gpu.global.v2.u64 [%0], {%1, %2};" ::"l"(d), "l"(w[0]), "l"(w[1])
-                 : "memory");
-  } else {
-    st_relaxed_u64(d, w[0]);
+// Halo words of one column and side: 4 slots (p1, p2, p3, spare) of NWD
+// tagged 64-bit words, contiguous, so a thread moves its column's whole dual
+// in 256-bit accesses (1 for float, 2 for double); the single TV-L1 value
+// per column is packed densely instead.
+__device__ __forceinline__ void st_v4(unsigned long long* d, const unsigned long long* w) {
+  asm volatile("st.relaxed.gpu.global.v4.u64 [%0], {%1, %2, %3, %4};" ::"l"(d), "l"(w[0]),
+               "l"(w[1]), "l"(w[2]), "l"(w[3])
+               : "memory");
+}
+__device__ __forceinline__ void ld_v4(const unsigned long long* s, unsigned long long* w) {
+  asm volatile("ld.relaxed.gpu.global.v4.u64 {%0, %1, %2, %3}, [%4];"
+               : "=l"(w[0]), "=l"(w[1]), "=l"(w[2]), "=l"(w[3])
+               : "l"(s)
+               : "memory");
+}
+__device__ __forceinline__ void st_v2(unsigned long long* d, const unsigned long long* w) {
+  asm volatile("st.relaxed.gpu.global.v2.u64 [%0], {%1, %2};" ::"l"(d), "l"(w[0]), "l"(w[1])
+               : "memory");
+}
+__device__ __forceinline__ void ld_v2(const unsigned long long* s, unsigned long long* w) {
+  asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];"
+               : "=l"(w[0]), "=l"(w[1])
+               : "l"(s)
+               : "memory");
+}
+// words [0, n) of a column's slots, n = NWD (one value) or 4 * NWD (all)
+template <int N> __device__ __forceinline__ void st_words(unsigned long long* d,
+                                                         const unsigned long long* w) {
+  if constexpr (N == 1) st_relaxed_u64(d, w[0]);
+  else if constexpr (N == 2) st_v2(d, w);
+  else {
+#pragma unroll
+    for (int k = 0; k < N; k += 4) st_v4(d + k, w + k);
   }
 }
-template <int NWD>
-__device__ __forceinline__ void ld_words(const unsigned long long* s, unsigned long long* w) {
-  if constexpr (NWD == 2) {
-    asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];"
-                 : "=l"(w[0]), "=l"(w[1])
-                 : "l"(s)
-                 : "memory");
-  } else {
-    w[0] = ld_relaxed_u64(s);
+template <int N> __device__ __forceinline__ void ld_words(const unsigned long long* s,
+                                                         unsigned long long* w) {
+  if constexpr (N == 1) w[0] = ld_relaxed_u64(s);
+  else if constexpr (N == 2) ld_v2(s, w);
+  else {
+#pragma unroll
+    for (int k = 0; k < N; k += 4) ld_v4(s + k, w + k);
   }
 }
 
@@ -67,9 +90,6 @@ __global__ void __launch_bounds__(NT, 1) k_resident_col(const ResArgs<T> a) {
 #define EVR_SKIP_UNIT 1
 #endif
   constexpr bool kSkipUnit = EVR_SKIP_UNIT;  // skip p / 1 when the whole warp is inside the ball
-#ifndef EVR_POLL_SLEEP
-#define EVR_POLL_SLEEP 0
-#endif
 #ifndef EVR_SENTINEL_POLL
 #define EVR_SENTINEL_POLL 1
 #endif
@@ -106,7 +126,8 @@ __global__ void __launch_bounds__(NT, 1) k_resident_col(const ResArgs<T> a) {
   const unsigned long long epoch = (unsigned long long)hdr->seq << 24;
   const unsigned tag_base = (unsigned)hdr->seq << 16;
   constexpr int NWD = LLWords<T>::N;
-  const size_t xside = (size_t)3 * W * NWD;
+  constexpr int NCW = 4 * NWD;                     // words of one column and side
+  const size_t xside = (size_t)W * NCW;             // words of one side of one CTA
   const size_t xslot = (size_t)a.nb * 2 * xside;
   unsigned long long* const xw = reinterpret_cast<unsigned long long*>(a.xchg);
   auto gk_of = [&](int r) { return (int64_t)(r0 - 1 + r) * W + j; };
@@ -122,47 +143,50 @@ __global__ void __launch_bounds__(NT, 1) k_resident_col(const ResArgs<T> a) {
   };
   mark();
 
-  // boundary value of local row r (1 = first own row -> the band above,
-  // Rb = last own row -> the band below) as tagged words
-  auto ll_put = [&](int step, int r, int field, T v) {
-    unsigned long long w[NWD];
-    LLWords<T>::pack(v, tag_base + (unsigned)step, w);
-    unsigned long long* base = xw + (step & 1) * xslot + (size_t)b * 2 * xside;
-    if (r == 1) {
-      unsigned long long* d = base + ((size_t)field * W + j) * NWD;
-      st_words<NWD>(d, w);
+  // boundary values of local row r (1 = first own row -> the band above,
+  // Rb = last own row -> the band below) as tagged words: nv = 1 (u_bar) or
+  // 3 (p1, p2, p3) values in the column's slots
+  auto ll_put = [&](int step, int r, int nv, T v0, T v1, T v2) {
+    unsigned long long w[NCW];
+    const unsigned tag = tag_base + (unsigned)step;
+    LLWords<T>::pack(v0, tag, w);
+    unsigned long long* side = xw + (step & 1) * xslot + (size_t)b * 2 * xside;
+    if (nv == 1) {  // one value per column, densely packed (TV-L1)
+      if (r == 1) st_words<NWD>(side + (size_t)j * NWD, w);
+      if (r == Rb) st_words<NWD>(side + xside + (size_t)j * NWD, w);
+      return;
     }
-    if (r == Rb) {
-      unsigned long long* d = base + xside + ((size_t)field * W + j) * NWD;
-      st_words<NWD>(d, w);
-    }
+    unsigned long long* base = side + (size_t)j * NCW;
+    LLWords<T>::pack(v1, tag, w + NWD);
+    LLWords<T>::pack(v2, tag, w + 2 * NWD);
+    LLWords<T>::pack(v2, tag, w + 3 * NWD);  // spare slot: keeps the access 256-bit
+    if (r == 1) st_words<NCW>(base, w);
+    if (r == Rb) st_words<NCW>(base + xside, w);
   };
   // the neighbours' boundary values of `step` for this column: v[0][f] from
   // the band above (-> local row 0), v[1][f] from the band below (-> RB+1)
   auto ll_fetch = [&](int step, int nf, T (&v)[2][3]) {
     const unsigned want = tag_base + (unsigned)step;
     const unsigned long long* slot = xw + (step & 1) * xslot;
-    const unsigned long long* src[2] = {slot + (size_t)(b - 1) * 2 * xside + xside,
-                                        slot + (size_t)(b + 1) * 2 * xside};
+    const size_t jw = (size_t)j * (nf == 1 ? NWD : NCW);  // dense for one value
+    const unsigned long long* src[2] = {slot + (size_t)(b - 1) * 2 * xside + xside + jw,
+                                        slot + (size_t)(b + 1) * 2 * xside + jw};
     const bool on[2] = {has_up, has_dn};
-    unsigned long long w[2][3][NWD];
+    unsigned long long w[2][NCW];
     bool ready;
-    if (kSentinelPoll && nf * NWD >= 6 && a.nb * W >= 32768) {
+    if (kSentinelPoll && nf * NWD >= 6 && a.nb * W >= 32768 && col) {
       // Large grids exchanging the float64 dual: spin on one word per side
-      // (the last one the neighbour stores), then read and check them all --
-      // polling every word puts ~12 loads per thread per round on L2 and
-      // slows the very stores being waited for.  Light exchanges poll
-      // everything at once (one round trip fewer).  Measured on B200: C2 f64
-      // 0.299 -> 0.282 ms with; C1 / float32 slower with, and slower still
-      // with one polling lane per warp.
+      // (p3's high word, in the last 256-bit block the neighbour stores),
+      // then read and check them all -- polling every word keeps ~6 loads
+      // per thread per round on L2 and slows the very stores being waited
+      // for.  Light exchanges poll everything at once (one round trip
+      // fewer).  Measured on B200: C2 f64 0.299 -> 0.282 ms with; C1 /
+      // float32 slower with, and slower still with one polling lane per warp.
       do {
         ready = true;
 #pragma unroll
         for (int s = 0; s < 2; ++s)
-          if (on[s] && col)
-            ready &= (unsigned)(ld_relaxed_u64(src[s] + ((size_t)(nf - 1) * W + j) * NWD +
-                                               (NWD - 1)) >> 32) == want;
-        if (EVR_POLL_SLEEP > 0 && !ready) __nanosleep(EVR_POLL_SLEEP);
+          if (on[s]) ready &= (unsigned)(ld_relaxed_u64(src[s] + 3 * NWD - 1) >> 32) == want;
       } while (!ready);
     }
     if (!col) {
@@ -177,21 +201,22 @@ __global__ void __launch_bounds__(NT, 1) k_resident_col(const ResArgs<T> a) {
 #pragma unroll
       for (int s = 0; s < 2; ++s) {
         if (!on[s]) continue;
+        if (nf == 1) {
+          ld_words<NWD>(src[s], w[s]);
 #pragma unroll
-        for (int f = 0; f < 3; ++f) {
-          if (f >= nf) break;
-          ld_words<NWD>(src[s] + ((size_t)f * W + j) * NWD, w[s][f]);
+          for (int q = 0; q < NWD; ++q) ready &= (unsigned)(w[s][q] >> 32) == want;
+        } else {
+          ld_words<NCW>(src[s], w[s]);
 #pragma unroll
-          for (int q = 0; q < NWD; ++q) ready &= (unsigned)(w[s][f][q] >> 32) == want;
+          for (int q = 0; q < 3 * NWD; ++q) ready &= (unsigned)(w[s][q] >> 32) == want;
         }
       }
-      if (EVR_POLL_SLEEP > 0 && !ready) __nanosleep(EVR_POLL_SLEEP);
     } while (!ready);
 #pragma unroll
     for (int s = 0; s < 2; ++s)
 #pragma unroll
       for (int f = 0; f < 3; ++f)
-        if (f < nf) v[s][f] = on[s] ? LLWords<T>::unpack(w[s][f]) : T(0);
+        if (f < nf) v[s][f] = on[s] ? LLWords<T>::unpack(w[s] + f * NWD) : T(0);
   };
   auto flag_publish = [&](int step) {
     __syncthreads();
@@ -322,7 +347,7 @@ __global__ void __launch_bounds__(NT, 1) k_resident_col(const ResArgs<T> a) {
         T ub;
         tu[r] = tv_primal_step(d, tu[r], t0[r], a.tv_step, a.shrink, ub);
         tub[r] = ub;
-        if (pub && col) ll_put(step + 1, r, 0, ub);
+        if (pub && col) ll_put(step + 1, r, 1, ub, ub, ub);
       }
       if (pub) ++step;
     }
@@ -496,9 +521,7 @@ __global__ void __launch_bounds__(NT, 1) k_resident_col(const ResArgs<T> a) {
         p3[r] = n3[r];
         q_of(c[r], p1[r], p2[r], p3[r], qx[r], qy[r]);
         if (!last && col && r <= Rb) {
-          ll_put(step + 1, r, 0, p1[r]);
-          ll_put(step + 1, r, 1, p2[r]);
-          ll_put(step + 1, r, 2, p3[r]);
+          ll_put(step + 1, r, 3, p1[r], p2[r], p3[r]);
         }
       }
     }
