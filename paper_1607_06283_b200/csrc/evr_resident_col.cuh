@@ -90,10 +90,6 @@ __global__ void __launch_bounds__(NT, 1) k_resident_col(const ResArgs<T> a) {
 #define EVR_SKIP_UNIT 1
 #endif
   constexpr bool kSkipUnit = EVR_SKIP_UNIT;  // skip p / 1 when the whole warp is inside the ball
-#ifndef EVR_SENTINEL_POLL
-#define EVR_SENTINEL_POLL 1
-#endif
-  constexpr bool kSentinelPoll = EVR_SENTINEL_POLL;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ double red[64];
   const int tid = threadIdx.x;
@@ -174,21 +170,6 @@ __global__ void __launch_bounds__(NT, 1) k_resident_col(const ResArgs<T> a) {
     const bool on[2] = {has_up, has_dn};
     unsigned long long w[2][NCW];
     bool ready;
-    if (kSentinelPoll && nf * NWD >= 6 && a.nb * W >= 32768 && col) {
-      // Large grids exchanging the float64 dual: spin on one word per side
-      // (p3's high word, in the last 256-bit block the neighbour stores),
-      // then read and check them all -- polling every word keeps ~6 loads
-      // per thread per round on L2 and slows the very stores being waited
-      // for.  Light exchanges poll everything at once (one round trip
-      // fewer).  Measured on B200: C2 f64 0.299 -> 0.282 ms with; C1 /
-      // float32 slower with, and slower still with one polling lane per warp.
-      do {
-        ready = true;
-#pragma unroll
-        for (int s = 0; s < 2; ++s)
-          if (on[s]) ready &= (unsigned)(ld_relaxed_u64(src[s] + 3 * NWD - 1) >> 32) == want;
-      } while (!ready);
-    }
     if (!col) {
 #pragma unroll
       for (int s = 0; s < 2; ++s)
@@ -196,6 +177,9 @@ __global__ void __launch_bounds__(NT, 1) k_resident_col(const ResArgs<T> a) {
         for (int f = 0; f < 3; ++f) v[s][f] = T(0);
       return;
     }
+    // poll the whole column (1-2 256-bit loads per side) until every tag
+    // matches; measured faster on B200 than spinning on one sentinel word
+    // first (one L2 round trip fewer), and than any backoff
     do {
       ready = true;
 #pragma unroll
