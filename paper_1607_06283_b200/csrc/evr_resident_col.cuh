@@ -129,13 +129,16 @@ __global__ void __launch_bounds__(NT, 1) k_resident_col(const ResArgs<T> a) {
   auto gk_of = [&](int r) { return (int64_t)(r0 - 1 + r) * W + j; };
 
   int tmark = 0;
+  const bool tracing = a.trace != nullptr && tid == 0;
   auto mark = [&]() {
-    if (a.trace && tid == 0 && tmark < 256) {
-      unsigned long long t;
-      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t)::"memory");
-      a.trace[(size_t)b * 256 + tmark] = t;
+    if (tracing) {
+      if (tmark < 256) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t)::"memory");
+        a.trace[(size_t)b * 256 + tmark] = t;
+      }
+      ++tmark;
     }
-    ++tmark;
   };
   mark();
 
