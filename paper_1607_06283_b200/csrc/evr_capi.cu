@@ -433,6 +433,7 @@ template <class T> const ResidentColKernel<T>* resident_col_pick(int W, int R) {
   static const ResidentColKernel<T> table[] = {
       {128, 1, k_resident_col<T, 128, 1>}, {128, 2, k_resident_col<T, 128, 2>},
       {256, 1, k_resident_col<T, 256, 1>}, {256, 2, k_resident_col<T, 256, 2>},
+      {352, 1, k_resident_col<T, 352, 1>}, {352, 2, k_resident_col<T, 352, 2>},  // 346 wide
       {384, 1, k_resident_col<T, 384, 1>}, {384, 2, k_resident_col<T, 384, 2>},
       {512, 1, k_resident_col<T, 512, 1>}, {512, 2, k_resident_col<T, 512, 2>},
   };

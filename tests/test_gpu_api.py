@@ -225,7 +225,7 @@ def test_engine_detail_names_the_kernel():
     evr.process_packet(st, make_events(50, SensorGeometry(width=346, height=260)),
                        ManifoldConfig(), SolverConfig(), Thresholds())
     d = st.context().engine_detail()
-    assert d.startswith("k_resident_col<f64,NT=384,RB=2>") and "x130 CTAs" in d
+    assert d.startswith("k_resident_col<f64,NT=352,RB=2>") and "x130 CTAs" in d
     st = evr.init_state(SensorGeometry(width=640, height=480), SolverConfig(), precision=1)
     evr.process_packet(st, make_events(50, SensorGeometry(width=640, height=480)),
                        ManifoldConfig(), SolverConfig(), Thresholds())
