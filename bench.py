@@ -215,7 +215,9 @@ def run_reference(args):
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "frames_per_s": round(len(timed) / sec, 4),
         "config": {"workload": DESCR[args.config], "sensor": f"{W}x{H}",
-                   "events_per_packet": epp, "pd_iterations": pd, "tv_iterations": tv},
+                   "events_per_packet": epp, "pd_iterations": pd, "tv_iterations": tv,
+                   "engine": "cpu (C port of the reference)", "precision": "f64",
+                   "streams": "1 (rank 0 only)", "generator": "U(seed, W, H, 1 Mev/s)"},
         "cpu_baseline": {"value": round(value, 3), "unit": "events/s", "cores": threads,
                          "kind": "port",
                          "sample": f"{len(timed)} packets of the same workload, C port of "
