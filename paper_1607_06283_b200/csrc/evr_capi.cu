@@ -85,6 +85,10 @@ struct evr_ctx {
   // own rows [own_lo, own_hi]; a whole-sensor context owns all its rows
   int row0 = 0, Htot = 0, own_lo = 0, own_hi = -1;
   bool banded = false;
+  // bands: the contexts of the bands above / below (their packed state is
+  // read in place by the fused iteration kernels; peer memory across GPUs)
+  const evr_ctx* nb_up = nullptr;
+  const evr_ctx* nb_dn = nullptr;
   std::string err;
 
   template <class T> T* fld(int k) const { return reinterpret_cast<T*>(slab + field_stride * k); }
@@ -225,8 +229,8 @@ constexpr int kMarchRY = EVR_MARCH_RY, kMarchNT = 128;
 template <class T> struct MarchDepth { static constexpr int tv = EVR_MARCH_D32, pd = EVR_MARCH_D32; };
 template <> struct MarchDepth<double> { static constexpr int tv = EVR_MARCH_D64, pd = EVR_MARCH_D64; };
 inline unsigned march_grid(const evr_ctx* c) {
-  const int64_t warps =
-      (int64_t)((c->W + kStrip - 1) / kStrip) * ((c->H + kMarchRY - 1) / kMarchRY);
+  const int rows = c->own_hi - c->own_lo + 1;
+  const int64_t warps = (int64_t)((c->W + kStrip - 1) / kStrip) * ((rows + kMarchRY - 1) / kMarchRY);
   return (unsigned)((warps + kMarchNT / 32 - 1) / (kMarchNT / 32));
 }
 
@@ -245,6 +249,21 @@ template <class T> Packed<T> packed(const evr_ctx* c) {
 }
 inline size_t packed_bytes(int64_t N, int prec) {
   return prec == EVR_PREC_F64 ? (size_t)N * 6 * 32 : (size_t)N * 5 * 16;
+}
+
+// row sources of a fused iteration: `buf` maps a context to the packed
+// buffer read (the same one in the neighbours), E quads per pixel
+template <class Q, class Buf>
+MarchRows<Q> march_rows(const evr_ctx* c, Buf buf, int E) {
+  MarchRows<Q> r;
+  r.own = buf(c);
+  r.y0 = c->row0 + c->own_lo;
+  r.y1 = c->row0 + c->own_hi + 1;
+  r.olo = c->own_lo;
+  r.E = E;
+  r.up = c->nb_up ? buf(c->nb_up) + (int64_t)c->nb_up->own_hi * c->W * E : nullptr;
+  r.dn = c->nb_dn ? buf(c->nb_dn) + (int64_t)c->nb_dn->own_lo * c->W * E : nullptr;
+  return r;
 }
 
 template <class T> CoefPlanes<T> coefs(const evr_ctx* c);
@@ -339,42 +358,60 @@ template <class T> int launch_step(evr_ctx* ctx, const Step& st) {
       return 1;
     }
     // ---- fused list (whole-sensor context: off = 0, n = N)
-    case ST_NORMF:
-      k_normalize_pack<T><<<grid1d(n), kNT, 0, s>>>(ctx->raw, ctx->hdr(), g.t_scale, t,
-                                                    packed<T>(ctx).tv[0], n);
+    case ST_NORMF:  // own rows; a band's halo rows come from its neighbours
+      k_normalize_pack<T><<<grid1d(n), kNT, 0, s>>>(ctx->raw + off, ctx->hdr(), g.t_scale, t + off,
+                                                    packed<T>(ctx).tv[0] + off, n);
       return 1;
     case ST_TVF: {  // iteration k reads set k & 1 and writes the other
-      const Packed<T> P = packed<T>(ctx);
       const int a = st.it & 1;
-      launch_pdl(k_tv_march<T, kMarchRY, MarchDepth<T>::tv>, march_grid(ctx), kMarchNT, s,
-                 (const Q4<T>*)P.tv[a], (const T*)t, P.tv[a ^ 1], ctx->H, ctx->W, (T)step,
-                 (T)step, (T)(step * g.denoise_weight));
+      const auto in = march_rows<Q4<T>>(ctx, [a](const evr_ctx* c) { return packed<T>(c).tv[a]; }, 1);
+      Q4<T>* out = packed<T>(ctx).tv[a ^ 1];
+      const T sh = (T)(step * g.denoise_weight);
+      if (ctx->banded)
+        launch_pdl(k_tv_march<T, kMarchRY, MarchDepth<T>::tv, true>, march_grid(ctx), kMarchNT, s,
+                   in.own, in, (const T*)t, out, ctx->Htot, ctx->W, (T)step, (T)step, sh);
+      else
+        launch_pdl(k_tv_march<T, kMarchRY, MarchDepth<T>::tv, false>, march_grid(ctx), kMarchNT, s,
+                   in.own, in, (const T*)t, out, ctx->Htot, ctx->W, (T)step, (T)step, sh);
       return 1;
     }
     case ST_TVFINF:  // st.it = the TV-L1 iteration count
-      k_tv_finish_packed<T><<<grid1d(n), kNT, 0, s>>>(packed<T>(ctx).tv[st.it & 1], t,
+      k_tv_finish_packed<T><<<grid1d(n), kNT, 0, s>>>(packed<T>(ctx).tv[st.it & 1] + off, t + off,
                                                       (T)g.t_scale, n);
       return 1;
     case ST_PACK: {
       const Packed<T> P = packed<T>(ctx);
+      constexpr int E = sizeof(T) == 8 ? 2 : 1;
       k_pack_solver<T><<<grid1d(n), kNT, 0, s>>>(
-          ctx->fld<T>(F_P1), ctx->fld<T>(F_P2), ctx->fld<T>(F_P3), ctx->fld<T>(F_U),
-          ctx->fld<T>(F_TX), ctx->fld<T>(F_TY), coefs<T>(ctx), ctx->fld<T>(F_SG),
-          ctx->fld<T>(F_BETA), ctx->fld<T>(F_FB), P.pd[0], P.cst, n);
+          ctx->fld<T>(F_P1) + off, ctx->fld<T>(F_P2) + off, ctx->fld<T>(F_P3) + off,
+          ctx->fld<T>(F_U) + off, ctx->fld<T>(F_TX) + off, ctx->fld<T>(F_TY) + off,
+          CoefPlanes<T>{ctx->fld<T>(F_A11) + off, ctx->fld<T>(F_A12) + off,
+                        ctx->fld<T>(F_A22) + off, ctx->fld<T>(F_A31) + off,
+                        ctx->fld<T>(F_A32) + off},
+          ctx->fld<T>(F_SG) + off, ctx->fld<T>(F_BETA) + off, ctx->fld<T>(F_FB) + off,
+          P.pd[0] + off, P.cst + off * E, n);
       return 1;
     }
     case ST_PDF: {
-      const Packed<T> P = packed<T>(ctx);
       const int a = st.it & 1;
+      constexpr int E = sizeof(T) == 8 ? 2 : 1;
       using M = typename MetricPack<T>::type;
+      const auto in = march_rows<Q4<T>>(ctx, [a](const evr_ctx* c) { return packed<T>(c).pd[a]; }, 1);
+      const auto cr = march_rows<Q4<T>>(ctx, [](const evr_ctx* c) { return packed<T>(c).cst; }, E);
       M m;
       if constexpr (std::is_same<T, float>::value)
-        m = M{P.cst, (float)(g.tau * g.lam)};
+        m = M{cr.own, cr, (float)(g.tau * g.lam)};
       else
-        m = M{P.cst};
-      launch_pdl(k_pd_march<T, kMarchRY, MarchDepth<T>::pd, M>, march_grid(ctx), kMarchNT, s,
-                 (const Q4<T>*)P.pd[a], m, P.pd[a ^ 1], ctx->H, ctx->W, (T)g.tau, (T)g.sigma,
-                 (T)g.u_min, (T)g.u_max);
+        m = M{cr.own, cr};
+      Q4<T>* out = packed<T>(ctx).pd[a ^ 1];
+      if (ctx->banded)
+        launch_pdl(k_pd_march<T, kMarchRY, MarchDepth<T>::pd, M, true>, march_grid(ctx), kMarchNT,
+                   s, in.own, in, m, out, ctx->Htot, ctx->W, (T)g.tau, (T)g.sigma, (T)g.u_min,
+                   (T)g.u_max);
+      else
+        launch_pdl(k_pd_march<T, kMarchRY, MarchDepth<T>::pd, M, false>, march_grid(ctx), kMarchNT,
+                   s, in.own, in, m, out, ctx->Htot, ctx->W, (T)g.tau, (T)g.sigma, (T)g.u_min,
+                   (T)g.u_max);
       return 1;
     }
     case ST_RELF: {  // u of the last two iterations, the w of the packed quads
@@ -383,9 +420,10 @@ template <class T> int launch_step(evr_ctx* ctx, const Step& st) {
       return 2;
     }
     case ST_UNPACK:  // st.it = the iteration count
-      k_unpack_solver<T><<<grid1d(n), kNT, 0, s>>>(packed<T>(ctx).pd[st.it & 1],
-                                                   ctx->fld<T>(F_P1), ctx->fld<T>(F_P2),
-                                                   ctx->fld<T>(F_P3), ctx->fld<T>(F_U), ctx->f, n);
+      k_unpack_solver<T><<<grid1d(n), kNT, 0, s>>>(packed<T>(ctx).pd[st.it & 1] + off,
+                                                   ctx->fld<T>(F_P1) + off, ctx->fld<T>(F_P2) + off,
+                                                   ctx->fld<T>(F_P3) + off, ctx->fld<T>(F_U) + off,
+                                                   ctx->f + off, n);
       return 1;
   }
   return 0;
@@ -1584,6 +1622,9 @@ int evr_op_rof_solve(evr_ctx* ctx, const double* f, const double* tx, const doub
 // =========================================================================
 struct evr_group {
   int n = 0, H = 0, W = 0, prec = EVR_PREC_F64;
+  // fused list: the iteration kernels read the neighbours' halo rows in place
+  // (needs peer access between neighbouring GPUs); else split list + copies
+  bool fused = true;
   std::vector<evr_ctx*> band;
   std::vector<int> y0;
   std::vector<cudaEvent_t> done, copied;
@@ -1658,6 +1699,7 @@ int exchange_after(evr_group* grp, int kind) {
       rc = from_above(F_TPY);
       break;
     case ST_TVFIN:
+    case ST_TVFINF:  // the metric's slopes read the neighbours' denoised rows
       if (!(rc = from_above(F_T))) rc = from_below(F_T);
       break;
     case ST_METRIC:
@@ -1675,7 +1717,7 @@ int exchange_after(evr_group* grp, int kind) {
 }
 
 template <class T> int group_packet(evr_group* grp) {
-  const std::vector<Step> steps = packet_steps(grp->cfg, 2, false);
+  const std::vector<Step> steps = packet_steps(grp->cfg, 2, grp->fused);
   const int n = grp->n;
   for (const Step& st : steps) {
     for (int b = 0; b < n; ++b) {
@@ -1748,8 +1790,17 @@ int evr_group_create(evr_group** out, int n_bands, const int* devices, int heigh
       cudaSetDevice(d1);
       cudaDeviceEnablePeerAccess(d0, 0);
       cudaGetLastError();  // already-enabled is fine
+    } else {
+      grp->fused = false;  // no peer loads: halo rows travel as copies
     }
   }
+  if (const char* e = getenv("EVR_GROUP_SPLIT"))  // A/B and test hook: split list + copies
+    if (e[0] == '1') grp->fused = false;
+  if (grp->fused)
+    for (int b = 0; b < n_bands; ++b) {
+      grp->band[b]->nb_up = b > 0 ? grp->band[b - 1] : nullptr;
+      grp->band[b]->nb_dn = b + 1 < n_bands ? grp->band[b + 1] : nullptr;
+    }
   *out = grp;
   return EVR_OK;
 }

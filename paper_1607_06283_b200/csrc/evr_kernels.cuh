@@ -277,25 +277,6 @@ __device__ __forceinline__ void pdl_wait_and_release() {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
 
-struct Strip {
-  int j, i0, lane;
-  bool inb, own, live;
-};
-template <int RY>
-__device__ __forceinline__ Strip strip_of(int H, int W) {
-  Strip s;
-  s.lane = threadIdx.x & 31;
-  const int w = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  const int nsx = (W + kStrip - 1) / kStrip;
-  const int sx = w % nsx, sy = w / nsx;
-  s.live = sy * RY < H;
-  s.j = sx * kStrip - 1 + s.lane;
-  s.i0 = sy * RY;
-  s.inb = s.j >= 0 && s.j < W;
-  s.own = s.lane >= 1 && s.lane <= kStrip && s.j < W;
-  return s;
-}
-
 // The fused iterations keep their changing fields interleaved, one 16-byte
 // (float) / 32-byte (double) quad per pixel, so a warp row is one vector
 // load / store per field group instead of one access per plane:
@@ -304,33 +285,84 @@ __device__ __forceinline__ Strip strip_of(int H, int W) {
 //                 constants: float  {tx, ty, fb, 0} (matrix recomputed)
 //                            double {a11, a12, a22, a31}, {a32, sqrtG, beta, fb}
 // k_pack_solver / k_unpack_solver convert to and from the planes the rest of
-// the engine (state I/O, operator API, host loop, bands) uses.
+// the engine (state I/O, operator API, host loop) uses.
 template <class T> struct alignas(4 * sizeof(T)) Q4 {
   T x, y, z, w;
 };
+
+// Row sources of a march kernel.  A context owns global sensor rows
+// [y0, y1), global row gr living at local row gr - y0 + olo of `own` (E
+// elements per pixel).  A whole-sensor context is y0 = 0, y1 = H, olo = 0.
+// A band (evr_group) reads the one row on each side its recomputed halo
+// half-steps need -- the last row of the band above (y0 - 1) and the first
+// row of the band below (y1) -- in place from the neighbours' buffers: peer
+// memory over NVLink when the bands sit on different GPUs, so the halo
+// exchange is part of the iteration kernel itself.
+template <class Q> struct MarchRows {
+  const Q* own;
+  const Q* up;  // row y0 - 1 of the band above (BANDED only)
+  const Q* dn;  // row y1 of the band below (BANDED only)
+  int y0, y1, olo, E;
+};
+
+struct Strip {
+  int j, i0, lane;
+  bool inb, own, live;
+};
+// warp strips over the context's own rows [y0, y1)
+template <int RY>
+__device__ __forceinline__ Strip strip_of(int y0, int y1, int W) {
+  Strip s;
+  s.lane = threadIdx.x & 31;
+  const int w = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int nsx = (W + kStrip - 1) / kStrip;
+  const int sx = w % nsx, sy = w / nsx;
+  s.i0 = y0 + sy * RY;
+  s.live = s.i0 < y1;
+  s.j = sx * kStrip - 1 + s.lane;
+  s.inb = s.j >= 0 && s.j < W;
+  s.own = s.lane >= 1 && s.lane <= kStrip && s.j < W;
+  return s;
+}
 
 // TV-L1 iteration (surface.py:167-193): dual ascent + projection on rows
 // i0-1 .. i0+RY-1, primal + L1 shrink + over-relaxation on the owned rows.
 // Loads go to the clamped pixel so they are unconditional and are issued D
 // rows ahead of the arithmetic (software pipeline over the unrolled march);
 // out-of-sensor lanes / rows compute values nobody reads and store nothing.
-template <class T, int RY, int D>
+// H is the sensor height (boundary rules by global row); f0 and out are
+// indexed like in.own.
+template <class T, int RY, int D, bool BANDED>
 __global__ void __launch_bounds__(128)
-k_tv_march(const Q4<T>* __restrict__ in, const T* __restrict__ f0, Q4<T>* __restrict__ out,
-           int H, int W, T sigma, T tau, T shrink) {
-  const Strip s = strip_of<RY>(H, W);
+k_tv_march(const Q4<T>* __restrict__ own, const MarchRows<Q4<T>> in, const T* __restrict__ f0,
+           Q4<T>* __restrict__ out, int H, int W, T sigma, T tau, T shrink) {
+  const int y1 = BANDED ? in.y1 : H;  // end of the own rows (global)
+  const Strip s = strip_of<RY>(BANDED ? in.y0 : 0, y1, W);
   pdl_wait_and_release();
   if (!s.live) return;  // whole warp
   const int j = s.j;
   const int jc = min(max(j, 0), W - 1);
-  auto at = [&](int rr) { return min(max(s.i0 - 1 + rr, 0), H - 1) * W + jc; };
+  const int rlo = BANDED ? max(in.y0 - 1, 0) : 0, rhi = BANDED ? min(y1, H - 1) : H - 1;
+  auto grow = [&](int rr) { return min(max(s.i0 - 1 + rr, rlo), rhi); };
+  // offset of global row gr in the context's own buffers (32-bit for a
+  // whole sensor, the hot case)
+  auto local = [&](int gr) {
+    if constexpr (BANDED) return (int64_t)(gr - in.y0 + in.olo) * W;
+    else return gr * W;
+  };
   constexpr int NR = RY + 2;  // rows i0-1 .. i0+RY (the last one: u_bar only)
   Q4<T> q[NR];
   T f[NR];
   auto load = [&](int rr) {
-    const int kc = at(rr);
-    q[rr] = in[kc];
-    if (rr >= 1 && rr < NR - 1) f[rr] = f0[kc];
+    const int gr = grow(rr);
+    if constexpr (BANDED) {
+      q[rr] = gr < in.y0 ? in.up[jc] : gr >= y1 ? in.dn[jc] : own[local(gr) + jc];
+      if (rr >= 1 && rr < NR - 1) f[rr] = f0[local(min(gr, y1 - 1)) + jc];
+    } else {
+      const int kc = gr * W + jc;
+      q[rr] = own[kc];
+      if (rr >= 1 && rr < NR - 1) f[rr] = f0[kc];
+    }
   };
 #pragma unroll
   for (int rr = 0; rr < D && rr < NR; ++rr) load(rr);
@@ -346,11 +378,11 @@ k_tv_march(const Q4<T>* __restrict__ in, const T* __restrict__ f0, Q4<T>* __rest
     const T dy = r < H - 1 ? ub_n - ub_c : T(0);
     tv_dual_step(dx, dy, sigma, pxn, pyn);
     const T pxl = __shfl_up_sync(0xffffffffu, pxn, 1);
-    if (rr >= 1 && r < H && s.own) {
+    if (rr >= 1 && r < y1 && s.own) {
       const T d = div_at(pxn, j > 0 ? pxl : T(0), pyn, r > 0 ? pyn_up : T(0), r, j, H, W);
       T ubar;
       const T un = tv_primal_step(d, q[rr].x, f[rr], tau, shrink, ubar);
-      out[r * W + j] = Q4<T>{un, ubar, pxn, pyn};
+      out[local(r) + j] = Q4<T>{un, ubar, pxn, pyn};
     }
     pyn_up = pyn;
   }
@@ -358,10 +390,19 @@ k_tv_march(const Q4<T>* __restrict__ in, const T* __restrict__ f0, Q4<T>* __rest
 
 // metric inputs of the primal-dual iteration, from the packed constants
 struct MetricPackF32 {
-  const Q4<float>* __restrict__ c;  // {tx, ty, fb, 0}
+  const Q4<float>* __restrict__ c;  // {tx, ty, fb, 0}, the context's own rows
+  MarchRows<Q4<float>> rows;        // a band's neighbour rows
   float tl;                         // tau * lam (solve.py:227)
   using Raw = Q4<float>;
-  __device__ __forceinline__ Raw load(int k) const { return c[k]; }
+  template <bool BANDED>
+  __device__ __forceinline__ Raw load(int gr, int y1, int jc, int W) const {
+    if constexpr (BANDED)
+      return gr < rows.y0 ? rows.up[jc]
+             : gr >= y1   ? rows.dn[jc]
+                          : c[(int64_t)(gr - rows.y0 + rows.olo) * W + jc];
+    else
+      return c[gr * W + jc];
+  }
   __device__ __forceinline__ void finish(const Raw& r, Coef<float>& cf, float& sg, float& beta,
                                          float& fb) const {
     const MetricPx m = metric_px(r.x, r.y);  // bit-identical to k_metric_setup's planes
@@ -373,10 +414,22 @@ struct MetricPackF32 {
 };
 struct MetricPackF64 {
   const Q4<double>* __restrict__ c;  // {a11, a12, a22, a31}, {a32, sqrtG, beta, fb}
+  MarchRows<Q4<double>> rows;        // a band's neighbour rows (E = 2)
   struct Raw {
     Q4<double> a, b;
   };
-  __device__ __forceinline__ Raw load(int k) const { return Raw{c[2 * k], c[2 * k + 1]}; }
+  template <bool BANDED>
+  __device__ __forceinline__ Raw load(int gr, int y1, int jc, int W) const {
+    if constexpr (BANDED) {
+      const Q4<double>* p = gr < rows.y0 ? rows.up + 2 * jc
+                            : gr >= y1   ? rows.dn + 2 * jc
+                                         : c + 2 * ((int64_t)(gr - rows.y0 + rows.olo) * W + jc);
+      return Raw{p[0], p[1]};
+    } else {
+      const int k = gr * W + jc;
+      return Raw{c[2 * k], c[2 * k + 1]};
+    }
+  }
   __device__ __forceinline__ void finish(const Raw& r, Coef<double>& cf, double& sg,
                                          double& beta, double& fb) const {
     cf = Coef<double>{r.a.x, r.a.y, r.a.z, r.a.w, r.b.x};
@@ -393,23 +446,33 @@ template <> struct MetricPack<double> { using type = MetricPackF64; };
 // KL prox + over-relaxation on rows i0 .. i0+RY, dual ascent + ball
 // projection on the owned rows one row behind the primal, then the row's
 // {p, u} quad is stored; loads pipelined D rows ahead as in k_tv_march.
-template <class T, int RY, int D, class M>
+template <class T, int RY, int D, class M, bool BANDED>
 __global__ void __launch_bounds__(128)
-k_pd_march(const Q4<T>* __restrict__ in, M m, Q4<T>* __restrict__ out, int H, int W, T tau,
-           T sigma, T umin, T umax) {
-  const Strip s = strip_of<RY>(H, W);
+k_pd_march(const Q4<T>* __restrict__ own, const MarchRows<Q4<T>> in, M m,
+           Q4<T>* __restrict__ out, int H, int W, T tau, T sigma, T umin, T umax) {
+  const int y1 = BANDED ? in.y1 : H;  // end of the own rows (global)
+  const Strip s = strip_of<RY>(BANDED ? in.y0 : 0, y1, W);
   pdl_wait_and_release();
   if (!s.live) return;  // whole warp
   const int j = s.j;
   const int jc = min(max(j, 0), W - 1);
-  auto at = [&](int rr) { return min(max(s.i0 - 1 + rr, 0), H - 1) * W + jc; };
+  const int rlo = BANDED ? max(in.y0 - 1, 0) : 0, rhi = BANDED ? min(y1, H - 1) : H - 1;
+  auto grow = [&](int rr) { return min(max(s.i0 - 1 + rr, rlo), rhi); };
+  auto local = [&](int gr) {
+    if constexpr (BANDED) return (int64_t)(gr - in.y0 + in.olo) * W;
+    else return gr * W;
+  };
   constexpr int NR = RY + 2;  // rows i0-1 .. i0+RY
   Q4<T> q[NR];
   typename M::Raw c[NR];
   auto load = [&](int rr) {
-    const int kc = at(rr);
-    q[rr] = in[kc];
-    c[rr] = m.load(kc);
+    const int gr = grow(rr);
+    if constexpr (BANDED) {
+      q[rr] = gr < in.y0 ? in.up[jc] : gr >= y1 ? in.dn[jc] : own[local(gr) + jc];
+    } else {
+      q[rr] = own[gr * W + jc];
+    }
+    c[rr] = m.template load<BANDED>(gr, y1, jc, W);
   };
 #pragma unroll
   for (int rr = 0; rr < D && rr < NR; ++rr) load(rr);
@@ -431,12 +494,12 @@ k_pd_march(const Q4<T>* __restrict__ in, M m, Q4<T>* __restrict__ out, int H, in
       v = Arith<T>::mad(nu, T(2), -uk);
     }
     const T vr = __shfl_down_sync(0xffffffffu, v_up, 1);
-    if (rr >= 2 && r - 1 < H && s.own) {
+    if (rr >= 2 && r - 1 < y1 && s.own) {
       T a = q[rr - 1].x, b = q[rr - 1].y, cc = q[rr - 1].z;
       const T gx = j < W - 1 ? vr - v_up : T(0);
       const T gy = r - 1 < H - 1 ? v - v_up : T(0);
       dual_step(cf_up, sigma, gx, gy, sg_up, a, b, cc);
-      out[(r - 1) * W + j] = Q4<T>{a, b, cc, nu_up};
+      out[local(r - 1) + j] = Q4<T>{a, b, cc, nu_up};
     }
     qy_up = qy;
     v_up = v;
