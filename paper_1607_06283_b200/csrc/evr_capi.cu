@@ -1625,6 +1625,12 @@ struct evr_group {
   // fused list: the iteration kernels read the neighbours' halo rows in place
   // (needs peer access between neighbouring GPUs); else split list + copies
   bool fused = true;
+  // the whole per-packet step list of all bands as one CUDA graph (launched
+  // on band 0's stream; cross-band / cross-device order from captured events)
+  cudaGraphExec_t graph = nullptr;
+  bool graph_failed = false;
+  std::vector<int64_t> graph_launches, graph_cap;
+  std::vector<cudaEvent_t> fork;  // per band: graph fork / join / host-order events
   std::vector<evr_ctx*> band;
   std::vector<int> y0;
   std::vector<cudaEvent_t> done, copied;
@@ -1634,6 +1640,14 @@ struct evr_group {
 };
 
 namespace {
+
+void drop_group_graph(evr_group* g) {
+  if (g && g->graph) {
+    cudaSetDevice(g->band[0]->device);
+    cudaGraphExecDestroy(g->graph);
+    g->graph = nullptr;
+  }
+}
 
 int gfail(evr_group* g, int code, const char* fmt, ...) {
   char buf[512];
@@ -1668,7 +1682,9 @@ int copy_row(evr_group* grp, int dst, int rd, int src, int rs, int field) {
   const char* sp = S->slab + S->field_stride * field + (size_t)rs * grp->W * es;
   GCK(cudaSetDevice(D->device));
   GCK(cudaStreamWaitEvent(D->stream, grp->done[src], 0));
-  GCK(cudaMemcpyPeerAsync(dp, D->device, sp, S->device, grp->W * es, D->stream));
+  // unified addressing: a peer (NVLink) copy across GPUs, a D2D copy on one;
+  // unlike cudaMemcpyPeerAsync it can be captured into the group's graph
+  GCK(cudaMemcpyAsync(dp, sp, grp->W * es, cudaMemcpyDefault, D->stream));
   return EVR_OK;
 }
 
@@ -1740,6 +1756,86 @@ template <class T> int group_packet(evr_group* grp) {
   return EVR_OK;
 }
 
+// host order: every band stream (staging copies) before `dst`
+int group_order(evr_group* grp, cudaStream_t dst, int dst_dev) {
+  for (int b = 0; b < grp->n; ++b) {
+    evr_ctx* c = grp->band[b];
+    if (c->stream == dst) continue;
+    GCK(cudaSetDevice(c->device));
+    GCK(cudaEventRecord(grp->fork[b], c->stream));
+    GCK(cudaSetDevice(dst_dev));
+    GCK(cudaStreamWaitEvent(dst, grp->fork[b], 0));
+  }
+  return EVR_OK;
+}
+
+// Capture the step list of all bands once (fork from band 0's stream, join
+// back into it) and replay it per packet; the eager loop is the fallback
+// when capture is refused (e.g. a driver without multi-device capture).
+int group_run(evr_group* grp) {
+  evr_ctx* c0 = grp->band[0];
+  for (int b = 0; b < grp->n; ++b)  // staging buffers baked into the graph
+    if (grp->graph && grp->graph_cap[b] != grp->band[b]->ev_cap) drop_group_graph(grp);
+  if (!grp->graph && !grp->graph_failed) {
+    std::vector<int64_t> before(grp->n);
+    for (int b = 0; b < grp->n; ++b) before[b] = grp->band[b]->launches;
+    GCK(cudaSetDevice(c0->device));
+    cudaGraph_t g = nullptr;
+    bool ok = cudaStreamBeginCapture(c0->stream, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
+    int rc = EVR_OK;
+    if (ok) {
+      GCK(cudaEventRecord(grp->fork[0], c0->stream));
+      for (int b = 0; b < grp->n; ++b) {
+        evr_ctx* c = grp->band[b];
+        cudaSetDevice(c->device);
+        if (b > 0) ok &= cudaStreamWaitEvent(c->stream, grp->fork[0], 0) == cudaSuccess;
+        ok &= cudaEventRecord(grp->copied[b], c->stream) == cudaSuccess;
+      }
+      if (ok)
+        rc = grp->prec == EVR_PREC_F64 ? group_packet<double>(grp) : group_packet<float>(grp);
+      for (int b = 1; b < grp->n && ok && !rc; ++b) {
+        evr_ctx* c = grp->band[b];
+        cudaSetDevice(c->device);
+        ok &= cudaEventRecord(grp->done[b], c->stream) == cudaSuccess;
+        cudaSetDevice(c0->device);
+        ok &= cudaStreamWaitEvent(c0->stream, grp->done[b], 0) == cudaSuccess;
+      }
+      cudaSetDevice(c0->device);
+      ok &= cudaStreamEndCapture(c0->stream, &g) == cudaSuccess;
+      ok = ok && !rc && cudaGraphInstantiate(&grp->graph, g, 0) == cudaSuccess;
+      if (g) cudaGraphDestroy(g);
+    }
+    cudaGetLastError();
+    grp->graph_launches.assign(grp->n, 0);
+    grp->graph_cap.assign(grp->n, 0);
+    for (int b = 0; b < grp->n; ++b) {
+      grp->graph_launches[b] = grp->band[b]->launches - before[b];
+      grp->band[b]->launches = before[b];
+      grp->graph_cap[b] = grp->band[b]->ev_cap;
+    }
+    if (!ok || rc) {  // capture refused: run (and keep running) the eager loop
+      if (grp->graph) cudaGraphExecDestroy(grp->graph);
+      grp->graph = nullptr;
+      grp->graph_failed = true;
+    }
+  }
+  if (!grp->graph)
+    return grp->prec == EVR_PREC_F64 ? group_packet<double>(grp) : group_packet<float>(grp);
+  int rc = group_order(grp, c0->stream, c0->device);  // staging copies first
+  if (rc) return rc;
+  GCK(cudaSetDevice(c0->device));
+  GCK(cudaGraphLaunch(grp->graph, c0->stream));
+  GCK(cudaEventRecord(grp->fork[0], c0->stream));
+  for (int b = 0; b < grp->n; ++b) {  // later per-band work after the graph
+    evr_ctx* c = grp->band[b];
+    c->launches += grp->graph_launches[b];
+    if (b == 0) continue;
+    GCK(cudaSetDevice(c->device));
+    GCK(cudaStreamWaitEvent(c->stream, grp->fork[0], 0));
+  }
+  return EVR_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -1777,6 +1873,9 @@ int evr_group_create(evr_group** out, int n_bands, const int* devices, int heigh
     cudaEventRecord(e2, ctx->stream);
     grp->done.push_back(e1);
     grp->copied.push_back(e2);
+    cudaEvent_t e3;
+    cudaEventCreateWithFlags(&e3, cudaEventDisableTiming);
+    grp->fork.push_back(e3);
   }
   // peer access between neighbouring GPUs (NVLink); same-device bands need none
   for (int b = 0; b + 1 < n_bands; ++b) {
@@ -1807,10 +1906,12 @@ int evr_group_create(evr_group** out, int n_bands, const int* devices, int heigh
 
 void evr_group_destroy(evr_group* grp) {
   if (!grp) return;
+  drop_group_graph(grp);
   for (size_t b = 0; b < grp->band.size(); ++b) {
     cudaSetDevice(grp->band[b]->device);
     if (b < grp->done.size()) cudaEventDestroy(grp->done[b]);
     if (b < grp->copied.size()) cudaEventDestroy(grp->copied[b]);
+    if (b < grp->fork.size()) cudaEventDestroy(grp->fork[b]);
     evr_destroy(grp->band[b]);
   }
   delete grp;
@@ -1837,6 +1938,7 @@ int evr_group_set_config(evr_group* grp, const evr_config* cfg) {
   for (int b = 0; b < grp->n; ++b) GBAND(b, evr_set_config(grp->band[b], &c));
   grp->cfg = c;
   grp->cfg_set = true;
+  drop_group_graph(grp);
   return EVR_OK;
 }
 
@@ -1878,7 +1980,7 @@ int evr_group_process_packet(evr_group* grp, const evr_event* events, int64_t n,
     cudaSetDevice(ctx->device);
     GBAND(b, stage_host_packet(ctx, events, n, window));
   }
-  int rc = grp->prec == EVR_PREC_F64 ? group_packet<double>(grp) : group_packet<float>(grp);
+  int rc = group_run(grp);
   if (rc) return rc;
   double d = 0.0, o = 0.0;
   int iters = 0;
