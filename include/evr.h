@@ -149,6 +149,16 @@ int evr_get_frame(evr_ctx *ctx, double *u_out);
 /* evr_get_frame enqueued on the context stream without waiting (complete
  * after evr_synchronize); asynchronous when u_out is pinned host memory */
 int evr_get_frame_async(evr_ctx *ctx, double *u_out);
+/* Pipelined read-back for streams (run_stream, pipeline.py:206-276, with
+ * packet k+1 computing while frame k travels to the host).  Submit, right
+ * after evr_process_packet_async, snapshots this packet's frame u (float64
+ * (H, W) into u_out, pinned host memory, or NULL for the record only) and
+ * its SolveResult record; the copy runs on a second stream, so the caller
+ * may enqueue the next packet at once.  Wait blocks until ticket's frame and
+ * record are on the host.  At most 4 tickets in flight; waits in any order.
+ * An event outside the sensor is reported by the wait of that packet. */
+int evr_frame_submit(evr_ctx *ctx, double *u_out, int64_t *ticket);
+int evr_frame_wait(evr_ctx *ctx, int64_t ticket, evr_solve_info *info);
 /* page-locked host buffers for frames / events (cudaHostAlloc) */
 int evr_host_alloc(size_t bytes, void **out);
 int evr_host_free(void *p);

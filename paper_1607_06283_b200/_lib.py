@@ -96,6 +96,8 @@ _SIGNATURES = {
     "evr_synchronize": ([_P, _P], _i32),
     "evr_get_frame": ([_P, _P], _i32),
     "evr_get_frame_async": ([_P, _P], _i32),
+    "evr_frame_submit": ([_P, _P, _P], _i32),
+    "evr_frame_wait": ([_P, _i64, _P], _i32),
     "evr_host_alloc": ([ctypes.c_size_t, _P], _i32),
     "evr_host_free": ([_P], _i32),
     "evr_sim_create": ([_P, _i32], _i32),

@@ -40,6 +40,13 @@ enum Field {
 
 }  // namespace
 
+constexpr int kFrameSlots = 4;
+struct FrameRec {
+  evr_solve_info info;
+  int err;
+  int pad;
+};
+
 struct evr_ctx {
   int device = 0;
   int H = 0, W = 0;
@@ -89,6 +96,19 @@ struct evr_ctx {
   // read in place by the fused iteration kernels; peer memory across GPUs)
   const evr_ctx* nb_up = nullptr;
   const evr_ctx* nb_dn = nullptr;
+  // pipelined frame read-back (evr_frame_submit / evr_frame_wait): per slot a
+  // device snapshot of u (float64) + the packet record, copied to the host on
+  // a second stream while the next packet runs
+  cudaStream_t cstream = nullptr;
+  double* d_fr[kFrameSlots] = {};
+  FrameRec* d_rec = nullptr;
+  FrameRec* h_rec = nullptr;
+  double* fr_host[kFrameSlots] = {};
+  cudaEvent_t fr_ready[kFrameSlots] = {};
+  cudaEvent_t fr_done[kFrameSlots] = {};
+  int64_t fr_ticket[kFrameSlots] = {-1, -1, -1, -1};
+  int64_t fr_next = 0;
+  int* h_err = nullptr;  // pinned error-flag read-back of evr_synchronize
   std::string err;
 
   template <class T> T* fld(int k) const { return reinterpret_cast<T*>(slab + field_stride * k); }
@@ -933,6 +953,40 @@ int d2h_sync(evr_ctx* ctx, void* dst, const void* src, size_t bytes) {
 }  // namespace
 
 // =========================================================================
+namespace {
+
+// Snapshot of one packet's result on the context stream: the frame u (as
+// float64) into a per-slot device buffer, plus the solve record and the
+// device error flag (then cleared), so the next packet may run while the
+// copy stream reads the slot back.
+template <class T>
+__global__ void k_frame_snapshot(const T* __restrict__ u, double* __restrict__ out, int64_t n,
+                                 const evr_solve_info* info, int* err, FrameRec* rec) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += stride)
+    out[k] = (double)u[k];
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    rec->info = *info;
+    rec->err = *err;
+    *err = 0;
+  }
+}
+
+int ensure_frame_slots(evr_ctx* ctx) {
+  if (ctx->cstream) return EVR_OK;
+  CK(cudaStreamCreateWithFlags(&ctx->cstream, cudaStreamNonBlocking));
+  for (int i = 0; i < kFrameSlots; ++i) {
+    CK(cudaMalloc(&ctx->d_fr[i], sizeof(double) * std::max<int64_t>(ctx->own_n(), 1)));
+    CK(cudaEventCreateWithFlags(&ctx->fr_ready[i], cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&ctx->fr_done[i], cudaEventDisableTiming));
+  }
+  CK(cudaMalloc(&ctx->d_rec, sizeof(FrameRec) * kFrameSlots));
+  CK(cudaMallocHost(&ctx->h_rec, sizeof(FrameRec) * kFrameSlots));
+  return EVR_OK;
+}
+
+}  // namespace
+
 extern "C" {
 
 const char* evr_version(void) { return "evr-b200 0.1.0 (sm_100a)"; }
@@ -991,6 +1045,8 @@ int evr_create(evr_ctx** out, int device, int height, int width, int precision) 
     CK(cudaMalloc(&ctx->d_info, sizeof(evr_solve_info)));
     CK(cudaMemsetAsync(ctx->d_info, 0, sizeof(evr_solve_info), ctx->stream));
     CK(cudaMallocHost(&ctx->h_info, sizeof(evr_solve_info)));
+    CK(cudaMallocHost(&ctx->h_err, sizeof(int)));
+    *ctx->h_err = 0;
     for (int i = 0; i < 2; ++i) {
       CK(cudaEventCreateWithFlags(&ctx->stage_done[i], cudaEventDisableTiming));
       CK(cudaEventRecord(ctx->stage_done[i], ctx->stream));
@@ -1029,6 +1085,16 @@ void evr_destroy(evr_ctx* ctx) {
     if (ctx->stage_done[i]) cudaEventDestroy(ctx->stage_done[i]);
   }
   if (ctx->h_info) cudaFreeHost(ctx->h_info);
+  if (ctx->h_err) cudaFreeHost(ctx->h_err);
+  if (ctx->cstream) cudaStreamSynchronize(ctx->cstream);
+  for (int i = 0; i < kFrameSlots; ++i) {
+    cudaFree(ctx->d_fr[i]);
+    if (ctx->fr_ready[i]) cudaEventDestroy(ctx->fr_ready[i]);
+    if (ctx->fr_done[i]) cudaEventDestroy(ctx->fr_done[i]);
+  }
+  cudaFree(ctx->d_rec);
+  if (ctx->h_rec) cudaFreeHost(ctx->h_rec);
+  if (ctx->cstream) cudaStreamDestroy(ctx->cstream);
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
 }
@@ -1224,9 +1290,69 @@ int evr_synchronize(evr_ctx* ctx, evr_solve_info* info) {
     CK(cudaMemcpyAsync(ctx->h_info, ctx->d_info, sizeof(evr_solve_info), cudaMemcpyDeviceToHost,
                        ctx->stream));
   }
+  // the device error flag rides the same stream (no extra blocking copy)
+  CK(cudaMemcpyAsync(ctx->h_err, ctx->d_err, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
   if (info) *info = *ctx->h_info;
-  return check_err_flag(ctx);
+  if (*ctx->h_err) {
+    *ctx->h_err = 0;
+    CK(cudaMemset(ctx->d_err, 0, sizeof(int)));
+    return fail(ctx, EVR_ERR_RANGE, "a device-side event lay outside the %dx%d sensor", ctx->W,
+                ctx->H);
+  }
+  return EVR_OK;
+}
+
+
+int evr_frame_submit(evr_ctx* ctx, double* u_out, int64_t* ticket) {
+  CHECK_CTX();
+  if (!ticket) return fail(ctx, EVR_ERR_INVALID, "null ticket");
+  int rc;
+  if ((rc = ensure_frame_slots(ctx))) return rc;
+  const int64_t t = ctx->fr_next;
+  const int s = (int)(t % kFrameSlots);
+  if (ctx->fr_ticket[s] >= 0)
+    return fail(ctx, EVR_ERR_INVALID, "all %d frame slots are in flight: wait ticket %lld first",
+                kFrameSlots, (long long)ctx->fr_ticket[s]);
+  const int64_t N = ctx->own_n(), o = ctx->own_off();
+  const int grid = (int)std::min<int64_t>((N + kNT - 1) / kNT, 4 * 148);
+  if (ctx->prec == EVR_PREC_F64)
+    k_frame_snapshot<double><<<std::max(grid, 1), kNT, 0, ctx->stream>>>(
+        ctx->fld<double>(F_U) + o, ctx->d_fr[s], N, ctx->d_info, ctx->d_err, ctx->d_rec + s);
+  else
+    k_frame_snapshot<float><<<std::max(grid, 1), kNT, 0, ctx->stream>>>(
+        ctx->fld<float>(F_U) + o, ctx->d_fr[s], N, ctx->d_info, ctx->d_err, ctx->d_rec + s);
+  ctx->launches += 1;
+  if ((rc = launch_err(ctx, "frame_snapshot"))) return rc;
+  CK(cudaEventRecord(ctx->fr_ready[s], ctx->stream));
+  CK(cudaStreamWaitEvent(ctx->cstream, ctx->fr_ready[s], 0));
+  if (u_out)
+    CK(cudaMemcpyAsync(u_out, ctx->d_fr[s], sizeof(double) * N, cudaMemcpyDeviceToHost,
+                       ctx->cstream));
+  CK(cudaMemcpyAsync(ctx->h_rec + s, ctx->d_rec + s, sizeof(FrameRec), cudaMemcpyDeviceToHost,
+                     ctx->cstream));
+  CK(cudaEventRecord(ctx->fr_done[s], ctx->cstream));
+  ctx->fr_ticket[s] = t;
+  ctx->fr_host[s] = u_out;
+  ctx->fr_next = t + 1;
+  *ticket = t;
+  return EVR_OK;
+}
+
+int evr_frame_wait(evr_ctx* ctx, int64_t ticket, evr_solve_info* info) {
+  CHECK_CTX();
+  const int s = (int)(((ticket % kFrameSlots) + kFrameSlots) % kFrameSlots);
+  if (ticket < 0 || !ctx->cstream || ctx->fr_ticket[s] != ticket)
+    return fail(ctx, EVR_ERR_INVALID, "unknown frame ticket %lld", (long long)ticket);
+  CK(cudaEventSynchronize(ctx->fr_done[s]));
+  ctx->fr_ticket[s] = -1;
+  ctx->fr_host[s] = nullptr;
+  const FrameRec r = ctx->h_rec[s];
+  if (info) *info = r.info;
+  if (r.err)
+    return fail(ctx, EVR_ERR_RANGE, "a device-side event lay outside the %dx%d sensor", ctx->W,
+                ctx->H);
+  return EVR_OK;
 }
 
 int evr_get_frame(evr_ctx* ctx, double* u_out) {

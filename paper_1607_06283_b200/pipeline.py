@@ -349,10 +349,10 @@ class _LazyResult(SolveResult):
     In the reference result.p is state.p; it is served from the state while
     the state still holds this packet's solution."""
 
-    def __new__(cls, state, frame, info):
+    def __new__(cls, state, frame, info, frame_index=None):
         self = super().__new__(cls, frame, None, int(info.iterations), float(info.rel_change))
         self._state = state
-        self._frame_index = state.frame_index
+        self._frame_index = state.frame_index if frame_index is None else frame_index
         return self
 
     @property
@@ -360,6 +360,78 @@ class _LazyResult(SolveResult):
         if self._state.frame_index != self._frame_index:
             raise RuntimeError("result.p is only available until the next packet is processed")
         return self._state.p
+
+
+def stream_packets(state, packets, manifold_cfg, solver_cfg, thresholds, depth=2,
+                   want_frames=True):
+    """Pipelined process_packet over a sequence of packets (the run_stream
+    loop, pipeline.py:228-256): yields ``(frame, SolveResult)`` per packet in
+    stream order, with up to ``depth`` packets in flight on the device --
+    packet k+1's events go up and its solve runs while frame k is copied to
+    the host on a second stream (evr_frame_submit / evr_frame_wait).
+
+    The state advances exactly as with one process_packet call per packet
+    (the device executes the packets in order; frames are bit-identical).
+    ``want_frames`` may be a bool or a callable ``(frame_index) -> bool``
+    (decimation: frames not wanted come back as None).  A result's ``p`` is
+    readable only while the state still holds that packet's solution (the
+    last packet of the stream).  Packets that need the host-driven solve
+    (``convergence_tol > 0``) run one at a time.
+    """
+    if not 1 <= depth <= 4:
+        raise ValueError(f"depth must be in [1, 4], got {depth}")
+    if solver_cfg.convergence_tol > 0:
+        for pk in packets:
+            idx = state.frame_index
+            want = want_frames(idx) if callable(want_frames) else want_frames
+            _, frame, res = process_packet_arrays(state, events_to_array(pk), manifold_cfg,
+                                                  solver_cfg, thresholds, want_frame=bool(want))
+            yield frame, res
+        return
+    ctx = _prepare(state, manifold_cfg, solver_cfg, thresholds)
+    pending = deque()
+
+    def finish():
+        ticket, frame, idx = pending.popleft()
+        info = _lib.SolveInfo()
+        ctx.call("evr_frame_wait", ticket, ctypes.byref(info))
+        if frame is not None and not pending and idx == state.frame_index:
+            state._mirror["u"] = frame  # frame aliases state.u, like the reference
+        return frame, _LazyResult(state, frame, info, frame_index=idx)
+
+    try:
+        for pk in packets:
+            events = events_to_array(pk)
+            n = len(events)
+            if n == 0:  # pipeline.py:151-153, after the packets before it
+                while pending:
+                    yield finish()
+                yield state.u.copy(), None
+                continue
+            state._flush()
+            state.packet_starts.append(int(events["t"][0]))  # pipeline.py:155
+            state.events_in_packet = n
+            now = int(events["t"][-1])
+            window = _window(state, now, manifold_cfg) if manifold_cfg.enabled else 1.0
+            want = want_frames(state.frame_index) if callable(want_frames) else want_frames
+            ctx.call("evr_process_packet_async", _lib.ptr(events), n, float(window))
+            frame = _lib.pinned_empty(state.shape) if want else None
+            ticket = ctypes.c_int64(0)
+            ctx.call("evr_frame_submit", _lib.ptr(frame), ctypes.byref(ticket))
+            state.frame_index += 1
+            state._after_device_write(replaced=("u", "f", "p"), in_place=("raw_timestamps",))
+            pending.append((ticket.value, frame, state.frame_index))
+            if len(pending) >= depth:
+                yield finish()
+        while pending:
+            yield finish()
+    finally:
+        while pending:  # generator closed early: release the slots
+            try:
+                finish()
+            except Exception:
+                pending.clear()
+                raise
 
 
 def process_packet(state, events, manifold_cfg, solver_cfg, thresholds, trace=None,
@@ -439,6 +511,11 @@ def run_stream(events, geometry, policy, manifold_cfg, solver_cfg, thresholds, s
     t0 = time.perf_counter()
     if trace is not None:
         trace.write("packet,iteration,energy,rel_change\n")
+    if trace is None and debug_sink is None:
+        _run_pipelined(events, state, policy, manifold_cfg, solver_cfg, thresholds, sink,
+                       stats, stride, stats_every, log, t0)
+        stats.wall_seconds = time.perf_counter() - t0
+        return state, stats
     for packet, n in _packets(events, policy.events_per_packet):
         stats.events_consumed += n
         rows = [] if trace is not None else None
@@ -467,3 +544,39 @@ def run_stream(events, geometry, policy, manifold_cfg, solver_cfg, thresholds, s
                   f"{result.iterations} iterations, {rate:.0f} events/s", file=log)
     stats.wall_seconds = time.perf_counter() - t0
     return state, stats
+
+
+def _run_pipelined(events, state, policy, manifold_cfg, solver_cfg, thresholds, sink, stats,
+                   stride, stats_every, log, t0):
+    """run_stream's packet loop over stream_packets: the device works on
+    packet k+1 while frame k is read back and handed to the sink."""
+    sizes = deque()
+
+    def packets():
+        for packet, n in _packets(events, policy.events_per_packet):
+            sizes.append(n)
+            yield events_to_array(packet)
+
+    want = (lambda idx: idx % stride == 0) if sink is not None else False
+    first_index = state.frame_index - stats.packets
+    t_last = time.perf_counter()
+    for frame, result in stream_packets(state, packets(), manifold_cfg, solver_cfg, thresholds,
+                                        want_frames=want):
+        n = sizes.popleft()
+        stats.events_consumed += n
+        now = time.perf_counter()
+        ms = (now - t_last) * 1e3  # per-packet share of the pipelined wall time
+        t_last = now
+        stats.packets += 1
+        stats.solve_ms.append(ms)
+        stats.iterations.append(result.iterations)
+        # decimation phase carried in the state (frame_index after the packet)
+        if (first_index + stats.packets - 1) % stride == 0:
+            if sink is not None:
+                sink(stats.frames_emitted, frame)
+            stats.frames_emitted += 1
+        if stats_every and stats.packets % stats_every == 0:
+            elapsed = now - t0
+            rate = stats.events_consumed / elapsed if elapsed > 0 else 0.0
+            print(f"packet {stats.packets}: {ms:.2f} ms/solve, "
+                  f"{result.iterations} iterations, {rate:.0f} events/s", file=log)

@@ -265,3 +265,49 @@ def test_get_frame_async_matches_get_frame():
     ctx.call("evr_get_frame_async", _lib.ptr(b))
     ctx.call("evr_synchronize", None)
     assert np.array_equal(a.reshape(b.shape), b)
+
+
+@pytest.mark.parametrize("precision,engine,depth", [(0, 0, 2), (0, 1, 3), (1, 0, 4), (1, 1, 1)])
+def test_stream_packets_matches_process_packet(precision, engine, depth):
+    """The pipelined stream (packet k+1 in flight while frame k is read back)
+    yields exactly the frames and results of one process_packet per packet
+    and leaves the same state behind."""
+    geom = SensorGeometry(width=37, height=23)
+    ev = evr.events_to_array(make_events(700, geom, seed=3))
+    pk = [ev[s:s + 100] for s in range(0, len(ev), 100)]
+    mc, sc, th = ManifoldConfig(), SolverConfig(max_iterations=20), Thresholds()
+    a = evr.init_state(geom, sc, precision=precision, engine=engine)
+    ref = [evr.process_packet_arrays(a, p, mc, sc, th) for p in pk]
+    b = evr.init_state(geom, sc, precision=precision, engine=engine)
+    got = list(evr.stream_packets(b, pk, mc, sc, th, depth=depth))
+    assert len(got) == len(ref)
+    for (_, fr, rr), (fg, rg) in zip(ref, got):
+        assert np.array_equal(fr, fg)
+        assert rr.iterations == rg.iterations and rr.rel_change == rg.rel_change
+    assert np.array_equal(a.u, b.u) and np.array_equal(a.p, b.p)
+    assert np.array_equal(a.f, b.f) and np.array_equal(a.raw_timestamps, b.raw_timestamps)
+    assert a.frame_index == b.frame_index == len(pk)
+    assert list(a.packet_starts) == list(b.packet_starts)
+    assert np.array_equal(got[-1][1].p, a.p)  # last result still holds the state's dual
+
+
+def test_stream_packets_decimation_and_errors():
+    geom = SensorGeometry(width=16, height=16)
+    ev = evr.events_to_array(make_events(600))
+    pk = [ev[s:s + 100] for s in range(0, 600, 100)]
+    mc, sc, th = ManifoldConfig(), SolverConfig(max_iterations=10), Thresholds()
+    st = evr.init_state(geom, sc)
+    got = list(evr.stream_packets(st, pk, mc, sc, th, want_frames=lambda i: i % 3 == 0))
+    assert [f is not None for f, _ in got] == [True, False, False, True, False, False]
+    with pytest.raises(ValueError):
+        list(evr.stream_packets(st, pk, mc, sc, th, depth=5))
+    with pytest.raises(ValueError, match="ticket"):
+        st.context().call("evr_frame_wait", 12345, None)
+    # an event outside the sensor is reported by its packet's wait
+    bad = evr.make_event_array([3, 99], [2, 2], [1, 1], [10_000, 10_010])
+    with pytest.raises((ValueError, IndexError)):
+        list(evr.stream_packets(st, [bad], mc, sc, th))
+    # an empty packet yields the current frame after the ones before it
+    st2 = evr.init_state(geom, sc)
+    out = list(evr.stream_packets(st2, [pk[0], pk[0][:0]], mc, sc, th))
+    assert out[1][1] is None and np.array_equal(out[0][0], out[1][0])
