@@ -149,6 +149,11 @@ int evr_get_frame(evr_ctx *ctx, double *u_out);
 /* evr_get_frame enqueued on the context stream without waiting (complete
  * after evr_synchronize); asynchronous when u_out is pinned host memory */
 int evr_get_frame_async(evr_ctx *ctx, double *u_out);
+/* Streaming engine, whole-sensor contexts: primal-dual / TV-L1 iterations
+ * fused per launch by the temporally blocked tile kernels (1 = one march
+ * launch per iteration, 2..4 = tiles, 0 = the EVR_TILE_K default).
+ * Results are bit-identical for every k; this is a performance knob. */
+int evr_set_tile_k(evr_ctx *ctx, int k);
 /* Pipelined read-back for streams (run_stream, pipeline.py:206-276, with
  * packet k+1 computing while frame k travels to the host).  Submit, right
  * after evr_process_packet_async, snapshots this packet's frame u (float64

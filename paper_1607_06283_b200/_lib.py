@@ -97,6 +97,7 @@ _SIGNATURES = {
     "evr_get_frame": ([_P, _P], _i32),
     "evr_get_frame_async": ([_P, _P], _i32),
     "evr_frame_submit": ([_P, _P, _P], _i32),
+    "evr_set_tile_k": ([_P, _i32], _i32),
     "evr_frame_wait": ([_P, _i64, _P], _i32),
     "evr_host_alloc": ([ctypes.c_size_t, _P], _i32),
     "evr_host_free": ([_P], _i32),
@@ -218,6 +219,20 @@ class _PinnedBlock:
 
 _pinned_free: dict = {}
 _pinned_lock = threading.Lock()
+
+
+def pinned_reserve(shape, count, dtype=np.float64):
+    """Grow the pinned pool to at least `count` free blocks of this size
+    (cudaHostAlloc is milliseconds: keep it out of a stream's hot loop)."""
+    nbytes = max(1, int(np.prod(shape)) * np.dtype(dtype).itemsize)
+    with _pinned_lock:
+        have = len(_pinned_free.get(nbytes, ()))
+    for _ in range(count - have):
+        out = ctypes.c_void_p()
+        if lib().evr_host_alloc(nbytes, ctypes.byref(out)) != 0:
+            raise MemoryError(f"evr_host_alloc({nbytes}) failed")
+        with _pinned_lock:
+            _pinned_free.setdefault(nbytes, []).append(out.value)
 
 
 def pinned_empty(shape, dtype=np.float64):

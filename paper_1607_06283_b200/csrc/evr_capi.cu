@@ -19,6 +19,7 @@
 
 #include "../../include/evr.h"
 #include "evr_kernels.cuh"
+#include "evr_tile.cuh"
 #include "evr_resident.cuh"
 #include "evr_resident_reg.cuh"
 #include "evr_resident_col.cuh"
@@ -79,6 +80,7 @@ struct evr_ctx {
   int64_t graph_launches[3] = {0, 0, 0};
   int64_t launches = 0;
   int engine = EVR_ENGINE_STREAMING;  // resolved
+  int tile_k = 0;                     // fused iterations per tile launch (0 = EVR_TILE_K default)
   // resident engine plan + buffers
   int r_nb = 0, r_R = 0, r_nt = 0, r_ms = 0;
   size_t r_smem = 0, r_frame = 0;
@@ -191,46 +193,78 @@ enum StepKind {
 };
 struct Step {
   int kind, it;
+  int buf = 0;  // fused list: packed set read (TVF, PDF, RELF) / holding the result (TVFINF, UNPACK)
+  int k = 1;    // fused list: iterations per launch (1 = march kernel, > 1 = tile kernel)
 };
 
 // which: 0 = surface (ingest .. metric), 1 = solve (primal-dual + epilogue), 2 = both.
 // fused: one launch per TV-L1 / primal-dual iteration (k_tv_march,
-// k_pd_march) on the packed, ping-ponged state; band contexts (evr_group)
-// exchange halo rows between half-steps and use the split list.
-std::vector<Step> packet_steps(const evr_config& g, int which, bool fused) {
+// k_pd_march) on the packed, ping-ponged state, or -- tk > 1, whole-sensor
+// contexts -- tk iterations per launch (k_tv_tile, k_pd_tile); the last
+// primal-dual iteration always runs alone, so rel_change sees the u of the
+// two last iterations.  Split list (bands with EVR_GROUP_SPLIT): one launch
+// per half-step with halo rows exchanged between half-steps.
+std::vector<Step> packet_steps(const evr_config& g, int which, bool fused, int tk = 1) {
   std::vector<Step> v;
   const int D = g.denoise_iterations, M = g.max_iterations;
+  tk = std::max(tk, 1);
   if (which != 1) {
     v.push_back({ST_INGEST, 0});
     if (g.manifold_enabled) {
       v.push_back({fused ? ST_NORMF : ST_NORM, 0});
-      for (int k = 0; k < D; ++k) {
+      int b = 0;
+      for (int k = 0; k < D;) {
         if (fused) {
-          v.push_back({ST_TVF, k});
+          const int kk = D - k >= tk ? tk : 1;
+          v.push_back({ST_TVF, k, b, kk});
+          b ^= 1;
+          k += kk;
         } else {
           v.push_back({ST_TVD, k});
           v.push_back({ST_TVP, k});
+          ++k;
         }
       }
-      v.push_back({fused ? ST_TVFINF : ST_TVFIN, D});
+      v.push_back({fused ? ST_TVFINF : ST_TVFIN, D, b});
     }
     v.push_back({ST_METRIC, 0});
   }
   if (which != 0) {
     if (fused) v.push_back({ST_PACK, 0});
-    for (int k = 0; k < M; ++k) {
+    int b = 0;
+    for (int k = 0; k < M;) {
       if (fused) {
-        v.push_back({ST_PDF, k});
-        if (k == M - 1) v.push_back({ST_RELF, k});
+        const int kk = M - 1 - k >= tk ? tk : 1;
+        v.push_back({ST_PDF, k, b, kk});
+        if (k == M - 1) v.push_back({ST_RELF, k, b});
+        b ^= 1;
+        k += kk;
       } else {
         v.push_back({ST_PDP, k});
         if (k == M - 1) v.push_back({ST_REL, k});
         v.push_back({ST_PDD, k});
+        ++k;
       }
     }
-    v.push_back({fused ? ST_UNPACK : ST_EPI, M});
+    v.push_back({fused ? ST_UNPACK : ST_EPI, M, b});
   }
   return v;
+}
+
+// temporal blocking of the whole-sensor fused list: iterations per tile
+// launch (EVR_TILE_K overrides; 1 = one march launch per iteration).
+// Measured on B200 (tools/tilerun.sh): float32 K=4 (C3 0.94 -> 0.74 ms,
+// C4 0.38 -> 0.24, C5 3.2 -> 2.0); float64 tiles are register-bound (one
+// CTA per SM) and not faster than the march yet.
+int tile_k(int prec) {
+  static const int env = [] {
+    const char* e = getenv("EVR_TILE_K");
+    if (!e) return 0;
+    const int v = atoi(e);
+    return v >= 1 && v <= 4 ? v : 1;
+  }();
+  if (env) return env;
+  return prec == EVR_PREC_F32 ? 4 : 1;
 }
 
 // fused iterations: rows per warp strip (RY), rows of loads in flight ahead
@@ -321,6 +355,64 @@ void relchange(evr_ctx* ctx, const T* un, const T* u, int iterations, int stride
                                                     ctx->d_scalar + 2);
 }
 
+// temporally blocked tiles (evr_tile.cuh): a CTA of G warps covers 32 x
+// G*RPT region pixels and keeps the (32 - 2K) x (G*RPT - 2K) interior
+template <class T> struct TileShape;
+template <> struct TileShape<float> { static constexpr int RPT = 8, G = 8; };
+template <> struct TileShape<double> { static constexpr int RPT = 4, G = 8; };
+template <class T, int K> dim3 tile_grid(const evr_ctx* c) {
+  constexpr int TIW = 32 - 2 * K, TIH = TileShape<T>::G * TileShape<T>::RPT - 2 * K;
+  return dim3((c->W + TIW - 1) / TIW, (c->H + TIH - 1) / TIH);
+}
+template <class... KArgs, class... Args>
+void launch_pdl2(void (*k)(KArgs...), dim3 grid, unsigned block, cudaStream_t s, Args&&... args) {
+  cudaLaunchConfig_t lc{};
+  lc.gridDim = grid;
+  lc.blockDim = dim3(block);
+  lc.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  lc.attrs = at;
+  lc.numAttrs = pdl_enabled() ? 1 : 0;
+  cudaLaunchKernelEx(&lc, k, std::forward<Args>(args)...);
+}
+template <class T>
+int launch_tv_tile(evr_ctx* ctx, int K, const Q4<T>* in, const T* f0, Q4<T>* out, T sigma,
+                   T tau, T shrink) {
+  constexpr int RPT = TileShape<T>::RPT, G = TileShape<T>::G;
+  const int H = ctx->H, W = ctx->W;
+  cudaStream_t s = ctx->stream;
+  if (K == 2)
+    launch_pdl2(k_tv_tile<T, 2, RPT, G>, tile_grid<T, 2>(ctx), 32 * G, s, in, f0, out, H, W,
+                sigma, tau, shrink);
+  else if (K == 3)
+    launch_pdl2(k_tv_tile<T, 3, RPT, G>, tile_grid<T, 3>(ctx), 32 * G, s, in, f0, out, H, W,
+                sigma, tau, shrink);
+  else
+    launch_pdl2(k_tv_tile<T, 4, RPT, G>, tile_grid<T, 4>(ctx), 32 * G, s, in, f0, out, H, W,
+                sigma, tau, shrink);
+  return 1;
+}
+template <class T, class M>
+int launch_pd_tile(evr_ctx* ctx, int K, const Q4<T>* in, const M& m, Q4<T>* out) {
+  constexpr int RPT = TileShape<T>::RPT, G = TileShape<T>::G;
+  const evr_config& g = ctx->cfg;
+  const int H = ctx->H, W = ctx->W;
+  cudaStream_t s = ctx->stream;
+  const T tau = (T)g.tau, sigma = (T)g.sigma, lo = (T)g.u_min, hi = (T)g.u_max;
+  if (K == 2)
+    launch_pdl2(k_pd_tile<T, 2, RPT, G, M>, tile_grid<T, 2>(ctx), 32 * G, s, in, m, out, H, W,
+                tau, sigma, lo, hi);
+  else if (K == 3)
+    launch_pdl2(k_pd_tile<T, 3, RPT, G, M>, tile_grid<T, 3>(ctx), 32 * G, s, in, m, out, H, W,
+                tau, sigma, lo, hi);
+  else
+    launch_pdl2(k_pd_tile<T, 4, RPT, G, M>, tile_grid<T, 4>(ctx), 32 * G, s, in, m, out, H, W,
+                tau, sigma, lo, hi);
+  return 1;
+}
+
 // launches of one step (returns the kernel count)
 template <class T> int launch_step(evr_ctx* ctx, const Step& st) {
   const evr_config& g = ctx->cfg;
@@ -382,11 +474,13 @@ template <class T> int launch_step(evr_ctx* ctx, const Step& st) {
       k_normalize_pack<T><<<grid1d(n), kNT, 0, s>>>(ctx->raw + off, ctx->hdr(), g.t_scale, t + off,
                                                     packed<T>(ctx).tv[0] + off, n);
       return 1;
-    case ST_TVF: {  // iteration k reads set k & 1 and writes the other
-      const int a = st.it & 1;
+    case ST_TVF: {  // reads set st.buf, writes the other
+      const int a = st.buf;
       const auto in = march_rows<Q4<T>>(ctx, [a](const evr_ctx* c) { return packed<T>(c).tv[a]; }, 1);
       Q4<T>* out = packed<T>(ctx).tv[a ^ 1];
       const T sh = (T)(step * g.denoise_weight);
+      if (st.k > 1)
+        return launch_tv_tile<T>(ctx, st.k, in.own, (const T*)t, out, (T)step, (T)step, sh);
       if (ctx->banded)
         launch_pdl(k_tv_march<T, kMarchRY, MarchDepth<T>::tv, true>, march_grid(ctx), kMarchNT, s,
                    in.own, in, (const T*)t, out, ctx->Htot, ctx->W, (T)step, (T)step, sh);
@@ -395,8 +489,8 @@ template <class T> int launch_step(evr_ctx* ctx, const Step& st) {
                    in.own, in, (const T*)t, out, ctx->Htot, ctx->W, (T)step, (T)step, sh);
       return 1;
     }
-    case ST_TVFINF:  // st.it = the TV-L1 iteration count
-      k_tv_finish_packed<T><<<grid1d(n), kNT, 0, s>>>(packed<T>(ctx).tv[st.it & 1] + off, t + off,
+    case ST_TVFINF:  // st.buf = the set holding the last iteration
+      k_tv_finish_packed<T><<<grid1d(n), kNT, 0, s>>>(packed<T>(ctx).tv[st.buf] + off, t + off,
                                                       (T)g.t_scale, n);
       return 1;
     case ST_PACK: {
@@ -413,7 +507,7 @@ template <class T> int launch_step(evr_ctx* ctx, const Step& st) {
       return 1;
     }
     case ST_PDF: {
-      const int a = st.it & 1;
+      const int a = st.buf;
       constexpr int E = sizeof(T) == 8 ? 2 : 1;
       using M = typename MetricPack<T>::type;
       const auto in = march_rows<Q4<T>>(ctx, [a](const evr_ctx* c) { return packed<T>(c).pd[a]; }, 1);
@@ -424,6 +518,7 @@ template <class T> int launch_step(evr_ctx* ctx, const Step& st) {
       else
         m = M{cr.own, cr};
       Q4<T>* out = packed<T>(ctx).pd[a ^ 1];
+      if (st.k > 1) return launch_pd_tile<T>(ctx, st.k, in.own, m, out);
       if (ctx->banded)
         launch_pdl(k_pd_march<T, kMarchRY, MarchDepth<T>::pd, M, true>, march_grid(ctx), kMarchNT,
                    s, in.own, in, m, out, ctx->Htot, ctx->W, (T)g.tau, (T)g.sigma, (T)g.u_min,
@@ -436,11 +531,11 @@ template <class T> int launch_step(evr_ctx* ctx, const Step& st) {
     }
     case ST_RELF: {  // u of the last two iterations, the w of the packed quads
       const Packed<T> P = packed<T>(ctx);
-      relchange<T>(ctx, &P.pd[(st.it + 1) & 1]->w, &P.pd[st.it & 1]->w, st.it + 1, 4);
+      relchange<T>(ctx, &P.pd[st.buf ^ 1]->w, &P.pd[st.buf]->w, st.it + 1, 4);
       return 2;
     }
-    case ST_UNPACK:  // st.it = the iteration count
-      k_unpack_solver<T><<<grid1d(n), kNT, 0, s>>>(packed<T>(ctx).pd[st.it & 1] + off,
+    case ST_UNPACK:  // st.buf = the set holding the last iteration
+      k_unpack_solver<T><<<grid1d(n), kNT, 0, s>>>(packed<T>(ctx).pd[st.buf] + off,
                                                    ctx->fld<T>(F_P1) + off, ctx->fld<T>(F_P2) + off,
                                                    ctx->fld<T>(F_P3) + off, ctx->fld<T>(F_U) + off,
                                                    ctx->f + off, n);
@@ -451,7 +546,9 @@ template <class T> int launch_step(evr_ctx* ctx, const Step& st) {
 
 template <class T> int enqueue_packet(evr_ctx* ctx, int which) {
   int n = 0;
-  for (const Step& st : packet_steps(ctx->cfg, which, !ctx->banded)) n += launch_step<T>(ctx, st);
+  const int tk = ctx->banded ? 1 : ctx->tile_k > 0 ? ctx->tile_k : tile_k(ctx->prec);
+  for (const Step& st : packet_steps(ctx->cfg, which, !ctx->banded, tk))
+    n += launch_step<T>(ctx, st);
   int rc = launch_err(ctx, "packet");
   return rc ? rc : n;
 }
@@ -1146,9 +1243,23 @@ int evr_engine_detail(evr_ctx* ctx, char* buf, int len) {
     if (ctx->banded)
       snprintf(buf, len, "streaming split half-steps (band rows %d..%d of %d)", ctx->row0,
                ctx->row0 + ctx->H - 1, ctx->Htot);
-    else
-      snprintf(buf, len, "streaming k_tv_march/k_pd_march<%s,RY=%d> %u CTAs x %d", ty, kMarchRY,
-               march_grid(ctx), kMarchNT);
+    else {
+      const int tk = ctx->tile_k > 0 ? ctx->tile_k : tile_k(ctx->prec);
+      if (tk > 1) {
+        const bool d = ctx->prec == EVR_PREC_F64;
+        const int rpt = d ? TileShape<double>::RPT : TileShape<float>::RPT;
+        const int G = d ? TileShape<double>::G : TileShape<float>::G;
+        const int tiw = 32 - 2 * tk, tih = G * rpt - 2 * tk;
+        snprintf(buf, len,
+                 "streaming k_tv_tile/k_pd_tile<%s,K=%d> %d iterations per launch, %dx%d tiles, "
+                 "%d CTAs x %d (+ k_pd_march<RY=%d> for the last iteration)",
+                 ty, tk, tk, tiw, tih, ((ctx->W + tiw - 1) / tiw) * ((ctx->H + tih - 1) / tih),
+                 32 * G, kMarchRY);
+      } else {
+        snprintf(buf, len, "streaming k_tv_march/k_pd_march<%s,RY=%d> %u CTAs x %d", ty,
+                 kMarchRY, march_grid(ctx), kMarchNT);
+      }
+    }
   } else {
     const char* k = ctx->r_ms == PLANES_COL    ? "k_resident_col"
                     : ctx->r_ms == PLANES_REG  ? "k_resident_reg"
@@ -1303,6 +1414,15 @@ int evr_synchronize(evr_ctx* ctx, evr_solve_info* info) {
   return EVR_OK;
 }
 
+
+int evr_set_tile_k(evr_ctx* ctx, int k) {
+  CHECK_CTX();
+  if (k < 0 || k > 4) return fail(ctx, EVR_ERR_INVALID, "tile iterations must be in [0, 4]");
+  CK(cudaStreamSynchronize(ctx->stream));
+  ctx->tile_k = k;
+  drop_graphs(ctx);
+  return EVR_OK;
+}
 
 int evr_frame_submit(evr_ctx* ctx, double* u_out, int64_t* ticket) {
   CHECK_CTX();

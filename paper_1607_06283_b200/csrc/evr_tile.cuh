@@ -1,0 +1,165 @@
+// evr_tile.cuh -- temporally blocked iteration kernels of the streaming
+// engine: K TV-L1 or K primal-dual iterations per launch.
+//
+// One iteration of either solver reads each pixel's neighbours at distance
+// one (TV-L1: u_bar right / below for the dual, px left and py above for the
+// primal; primal-dual: q = A^T p left / above for the primal, v right /
+// below for the dual), so K iterations over a tile need K halo pixels on
+// every side.  A CTA loads a region of 32 columns x G*RPT rows of the packed
+// state (+ constants) into registers, runs K iterations on chip and stores
+// the (32 - 2K) x (G*RPT - 2K) interior; the halo pixels it computes on the
+// way are the neighbours' (recomputed bit-identically, never stored).
+//
+// Layout on chip: warp g owns region rows [g*RPT, (g+1)*RPT), lane l region
+// column l; a thread keeps its RPT pixels' state and constants in registers.
+// Horizontal neighbours come from warp shuffles (lane 0 / 31 are halo
+// columns, so their missing neighbour only spoils values nobody keeps);
+// vertical ones from the thread's own rows, and at a warp's first / last row
+// from the adjacent warp through one shared-memory row (2 CTA barriers per
+// iteration).  Global traffic per pixel and iteration falls from one state
+// read + constants read + state write per iteration (k_pd_march) to that
+// once per K iterations, x the halo overhead.
+//
+// Boundary rules (div_at, the last-row / last-column zero differences) go by
+// global pixel coordinates, so a pixel inside the sensor never reads a value
+// from outside it: region pixels beyond the sensor load the clamped pixel
+// and compute values nobody reads.  Every pixel runs exactly the reference
+// operation sequence of k_tv_march / k_pd_march, so results are bit-identical
+// to the one-iteration-per-launch kernels.
+#pragma once
+
+#include "evr_kernels.cuh"
+
+namespace evr {
+
+// TV-L1 (surface.py:167-193), K iterations: dual ascent + projection, then
+// divergence + L1 shrink + over-relaxation.  f0 is the t plane.
+template <class T, int K, int RPT, int G>
+__global__ void __launch_bounds__(32 * G)
+k_tv_tile(const Q4<T>* __restrict__ in, const T* __restrict__ f0, Q4<T>* __restrict__ out,
+          int H, int W, T sigma, T tau, T shrink) {
+  constexpr int RH = G * RPT, TIW = 32 - 2 * K, TIH = RH - 2 * K;
+  __shared__ T ub_top[G][32];  // u_bar of each warp's first row
+  __shared__ T py_bot[G][32];  // py of each warp's last row
+  const int l = threadIdx.x & 31, g = threadIdx.x >> 5;
+  const int gj = (int)blockIdx.x * TIW - K + l;
+  const int gi0 = (int)blockIdx.y * TIH - K + g * RPT;
+  const int jc = min(max(gj, 0), W - 1);
+  pdl_wait_and_release();
+  T u[RPT], ub[RPT], px[RPT], py[RPT], f[RPT];
+#pragma unroll
+  for (int r = 0; r < RPT; ++r) {
+    const int k = min(max(gi0 + r, 0), H - 1) * W + jc;
+    const Q4<T> q = in[k];
+    u[r] = q.x;
+    ub[r] = q.y;
+    px[r] = q.z;
+    py[r] = q.w;
+    f[r] = f0[k];
+  }
+#pragma unroll 1
+  for (int it = 0; it < K; ++it) {
+    ub_top[g][l] = ub[0];
+    __syncthreads();
+    const T ub_below = ub_top[g < G - 1 ? g + 1 : g][l];
+#pragma unroll
+    for (int r = 0; r < RPT; ++r) {  // dual (surface.py:168-183)
+      const int gi = gi0 + r;
+      const T ub_r = __shfl_down_sync(0xffffffffu, ub[r], 1);
+      const T ub_n = r < RPT - 1 ? ub[r + 1] : ub_below;
+      const T dx = gj < W - 1 ? ub_r - ub[r] : T(0);
+      const T dy = gi < H - 1 ? ub_n - ub[r] : T(0);
+      tv_dual_step(dx, dy, sigma, px[r], py[r]);
+    }
+    py_bot[g][l] = py[RPT - 1];
+    __syncthreads();
+    const T py_above = py_bot[g > 0 ? g - 1 : g][l];
+#pragma unroll
+    for (int r = 0; r < RPT; ++r) {  // primal (surface.py:185-193)
+      const int gi = gi0 + r;
+      const T pxl = __shfl_up_sync(0xffffffffu, px[r], 1);
+      const T pyu = r > 0 ? py[r - 1] : py_above;
+      const T d = div_at(px[r], gj > 0 ? pxl : T(0), py[r], gi > 0 ? pyu : T(0), gi, gj, H, W);
+      T ubar;
+      u[r] = tv_primal_step(d, u[r], f[r], tau, shrink, ubar);
+      ub[r] = ubar;
+    }
+  }
+  if (l < K || l >= 32 - K || gj >= W) return;
+#pragma unroll
+  for (int r = 0; r < RPT; ++r) {
+    const int R = g * RPT + r, gi = gi0 + r;
+    if (R >= K && R < RH - K && gi < H) out[gi * W + gj] = Q4<T>{u[r], ub[r], px[r], py[r]};
+  }
+}
+
+// Manifold-TV + KL primal-dual (solve.py:233-252), K iterations: q = A^T p,
+// divergence, KL prox + over-relaxation, dual ascent + ball projection.
+// The metric constants of the region are loaded once (M: MetricPackF32
+// recomputes the matrix from the slopes, MetricPackF64 reads it) and stay
+// in registers for the K iterations.
+template <class T, int K, int RPT, int G, class M>
+__global__ void __launch_bounds__(32 * G)
+k_pd_tile(const Q4<T>* __restrict__ in, M m, Q4<T>* __restrict__ out, int H, int W, T tau,
+          T sigma, T umin, T umax) {
+  constexpr int RH = G * RPT, TIW = 32 - 2 * K, TIH = RH - 2 * K;
+  __shared__ T qy_bot[G][32];  // qy of each warp's last row
+  __shared__ T v_top[G][32];   // v of each warp's first row
+  const int l = threadIdx.x & 31, g = threadIdx.x >> 5;
+  const int gj = (int)blockIdx.x * TIW - K + l;
+  const int gi0 = (int)blockIdx.y * TIH - K + g * RPT;
+  const int jc = min(max(gj, 0), W - 1);
+  pdl_wait_and_release();
+  T p1[RPT], p2[RPT], p3[RPT], u[RPT];
+  Coef<T> cf[RPT];
+  T sg[RPT], beta[RPT], fb[RPT];
+#pragma unroll
+  for (int r = 0; r < RPT; ++r) {
+    const int gr = min(max(gi0 + r, 0), H - 1);
+    const Q4<T> q = in[gr * W + jc];
+    p1[r] = q.x;
+    p2[r] = q.y;
+    p3[r] = q.z;
+    u[r] = q.w;
+    m.finish(m.template load<false>(gr, H, jc, W), cf[r], sg[r], beta[r], fb[r]);
+  }
+#pragma unroll 1
+  for (int it = 0; it < K; ++it) {
+    T qx[RPT], qy[RPT], v[RPT];
+#pragma unroll
+    for (int r = 0; r < RPT; ++r) q_of(cf[r], p1[r], p2[r], p3[r], qx[r], qy[r]);
+    qy_bot[g][l] = qy[RPT - 1];
+    __syncthreads();
+    const T qy_above = qy_bot[g > 0 ? g - 1 : g][l];
+#pragma unroll
+    for (int r = 0; r < RPT; ++r) {  // primal (solve.py:233-245)
+      const int gi = gi0 + r;
+      const T qxl = __shfl_up_sync(0xffffffffu, qx[r], 1);
+      const T qyu = r > 0 ? qy[r - 1] : qy_above;
+      const T d = div_at(qx[r], gj > 0 ? qxl : T(0), qy[r], gi > 0 ? qyu : T(0), gi, gj, H, W);
+      const T nu = kl_primal(d, u[r], beta[r], fb[r], tau, umin, umax);
+      v[r] = Arith<T>::mad(nu, T(2), -u[r]);
+      u[r] = nu;
+    }
+    v_top[g][l] = v[0];
+    __syncthreads();
+    const T v_below = v_top[g < G - 1 ? g + 1 : g][l];
+#pragma unroll
+    for (int r = 0; r < RPT; ++r) {  // dual (solve.py:246-252)
+      const int gi = gi0 + r;
+      const T vr = __shfl_down_sync(0xffffffffu, v[r], 1);
+      const T vd = r < RPT - 1 ? v[r + 1] : v_below;
+      const T gx = gj < W - 1 ? vr - v[r] : T(0);
+      const T gy = gi < H - 1 ? vd - v[r] : T(0);
+      dual_step(cf[r], sigma, gx, gy, sg[r], p1[r], p2[r], p3[r]);
+    }
+  }
+  if (l < K || l >= 32 - K || gj >= W) return;
+#pragma unroll
+  for (int r = 0; r < RPT; ++r) {
+    const int R = g * RPT + r, gi = gi0 + r;
+    if (R >= K && R < RH - K && gi < H) out[gi * W + gj] = Q4<T>{p1[r], p2[r], p3[r], u[r]};
+  }
+}
+
+}  // namespace evr

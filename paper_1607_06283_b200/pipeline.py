@@ -390,6 +390,8 @@ def stream_packets(state, packets, manifold_cfg, solver_cfg, thresholds, depth=2
         return
     ctx = _prepare(state, manifold_cfg, solver_cfg, thresholds)
     pending = deque()
+    if want_frames:  # frames in flight + the one the caller holds
+        _lib.pinned_reserve(state.shape, depth + 2)
 
     def finish():
         ticket, frame, idx = pending.popleft()

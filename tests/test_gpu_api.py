@@ -229,7 +229,7 @@ def test_engine_detail_names_the_kernel():
     st = evr.init_state(SensorGeometry(width=640, height=480), SolverConfig(), precision=1)
     evr.process_packet(st, make_events(50, SensorGeometry(width=640, height=480)),
                        ManifoldConfig(), SolverConfig(), Thresholds())
-    assert st.context().engine_detail().startswith("streaming k_tv_march/k_pd_march<f32")
+    assert st.context().engine_detail().startswith("streaming k_tv_tile/k_pd_tile<f32,K=4>")
 
 
 def test_frames_are_fresh_pinned_arrays():

@@ -321,3 +321,39 @@ def test_float32_register_engine_matches_streaming_bitwise():
     assert out["reg"][2] == "resident_reg"
     assert np.array_equal(out["reg"][0], out["streaming"][0])
     assert np.array_equal(out["reg"][1], out["streaming"][1])
+
+
+@pytest.mark.parametrize("precision", [0, 1])
+@pytest.mark.parametrize("H,W,tv,pd", [(150, 97, 13, 9), (61, 29, 4, 5), (7, 300, 3, 2),
+                                        (260, 346, 50, 50)])
+def test_tile_kernels_bitwise_equal_to_march(H, W, tv, pd, precision):
+    """Temporally blocked tiles (K = 2, 3, 4 iterations per launch) give the
+    bits of one march launch per iteration, chained over packets, in float64
+    and float32, with tile edges crossing the sensor edges."""
+    from paper_1607_06283_b200 import _lib
+
+    rng = np.random.default_rng(H * W + tv)
+    sc = evr.SolverConfig(max_iterations=pd)
+    mc = evr.ManifoldConfig(denoise_iterations=tv)
+    n = 400
+    ev = evr.make_event_array(rng.integers(0, W, 3 * n), rng.integers(0, H, 3 * n),
+                              rng.choice([-1, 1], 3 * n), np.arange(3 * n, dtype=np.int64) * 7)
+    out = {}
+    for k in (1, 2, 3, 4):
+        st = evr.init_state(evr.SensorGeometry(W, H), sc, precision=precision, engine=1)
+        st.context().call("evr_set_tile_k", k)
+        frames = []
+        for s in range(0, 3 * n, n):
+            _, fr, res = evr.process_packet_arrays(st, ev[s:s + n], mc, sc, evr.Thresholds())
+            frames.append((fr.copy(), res.rel_change))
+        out[k] = (frames, st.p.copy(), st.context().engine_detail())
+    for k in (2, 3, 4):
+        assert f"K={k}" in out[k][2]
+        for (a, ra), (b, rb) in zip(out[1][0], out[k][0]):
+            assert np.array_equal(a, b) and ra == rb
+        assert np.array_equal(out[1][1], out[k][1])
+    if precision == 0:  # and the oracle
+        ref = O.OracleStream(H, W, O.make_config(max_iterations=pd, denoise_iterations=tv))
+        for s in range(0, 3 * n, n):
+            ref.process(np.ascontiguousarray(ev[s:s + n]))
+        assert np.array_equal(out[2][0][-1][0], ref.u)
