@@ -253,9 +253,9 @@ std::vector<Step> packet_steps(const evr_config& g, int which, bool fused, int t
 
 // temporal blocking of the whole-sensor fused list: iterations per tile
 // launch (EVR_TILE_K overrides; 1 = one march launch per iteration).
-// Measured on B200 (tools/tilerun.sh): float32 K=4 (C3 0.94 -> 0.74 ms,
-// C4 0.38 -> 0.24, C5 3.2 -> 2.0); float64 tiles are register-bound (one
-// CTA per SM) and not faster than the march yet.
+// Measured on B200 (tools/tilerun.sh, tools/f64run.sh), K = 4: float32 C3
+// 0.94 -> 0.72 ms, C4 0.38 -> 0.23, C5 3.2 -> 1.9; float64 C3 2.84 -> 2.27,
+// C4 0.66 -> 0.57.
 int tile_k(int prec) {
   static const int env = [] {
     const char* e = getenv("EVR_TILE_K");
@@ -264,7 +264,7 @@ int tile_k(int prec) {
     return v >= 1 && v <= 4 ? v : 1;
   }();
   if (env) return env;
-  return prec == EVR_PREC_F32 ? 4 : 1;
+  return 4;
 }
 
 // fused iterations: rows per warp strip (RY), rows of loads in flight ahead
@@ -357,9 +357,31 @@ void relchange(evr_ctx* ctx, const T* un, const T* u, int iterations, int stride
 
 // temporally blocked tiles (evr_tile.cuh): a CTA of G warps covers 32 x
 // G*RPT region pixels and keeps the (32 - 2K) x (G*RPT - 2K) interior
+#ifndef EVR_TILE32_RPT
+#define EVR_TILE32_RPT 8
+#endif
+#ifndef EVR_TILE32_G
+#define EVR_TILE32_G 8
+#endif
+#ifndef EVR_TILE32_MINB
+#define EVR_TILE32_MINB 1
+#endif
+#ifndef EVR_TILE64_RPT
+#define EVR_TILE64_RPT 4
+#endif
+#ifndef EVR_TILE64_G
+#define EVR_TILE64_G 8
+#endif
+#ifndef EVR_TILE64_MINB
+#define EVR_TILE64_MINB 2  // 2 CTAs per SM (<= 128 registers): C3 f64 2.84 -> 2.27 ms
+#endif
 template <class T> struct TileShape;
-template <> struct TileShape<float> { static constexpr int RPT = 8, G = 8; };
-template <> struct TileShape<double> { static constexpr int RPT = 4, G = 8; };
+template <> struct TileShape<float> {
+  static constexpr int RPT = EVR_TILE32_RPT, G = EVR_TILE32_G, MINB = EVR_TILE32_MINB;
+};
+template <> struct TileShape<double> {
+  static constexpr int RPT = EVR_TILE64_RPT, G = EVR_TILE64_G, MINB = EVR_TILE64_MINB;
+};
 template <class T, int K> dim3 tile_grid(const evr_ctx* c) {
   constexpr int TIW = 32 - 2 * K, TIH = TileShape<T>::G * TileShape<T>::RPT - 2 * K;
   return dim3((c->W + TIW - 1) / TIW, (c->H + TIH - 1) / TIH);
@@ -380,35 +402,35 @@ void launch_pdl2(void (*k)(KArgs...), dim3 grid, unsigned block, cudaStream_t s,
 template <class T>
 int launch_tv_tile(evr_ctx* ctx, int K, const Q4<T>* in, const T* f0, Q4<T>* out, T sigma,
                    T tau, T shrink) {
-  constexpr int RPT = TileShape<T>::RPT, G = TileShape<T>::G;
+  constexpr int RPT = TileShape<T>::RPT, G = TileShape<T>::G, MB = TileShape<T>::MINB;
   const int H = ctx->H, W = ctx->W;
   cudaStream_t s = ctx->stream;
   if (K == 2)
-    launch_pdl2(k_tv_tile<T, 2, RPT, G>, tile_grid<T, 2>(ctx), 32 * G, s, in, f0, out, H, W,
+    launch_pdl2(k_tv_tile<T, 2, RPT, G, MB>, tile_grid<T, 2>(ctx), 32 * G, s, in, f0, out, H, W,
                 sigma, tau, shrink);
   else if (K == 3)
-    launch_pdl2(k_tv_tile<T, 3, RPT, G>, tile_grid<T, 3>(ctx), 32 * G, s, in, f0, out, H, W,
+    launch_pdl2(k_tv_tile<T, 3, RPT, G, MB>, tile_grid<T, 3>(ctx), 32 * G, s, in, f0, out, H, W,
                 sigma, tau, shrink);
   else
-    launch_pdl2(k_tv_tile<T, 4, RPT, G>, tile_grid<T, 4>(ctx), 32 * G, s, in, f0, out, H, W,
+    launch_pdl2(k_tv_tile<T, 4, RPT, G, MB>, tile_grid<T, 4>(ctx), 32 * G, s, in, f0, out, H, W,
                 sigma, tau, shrink);
   return 1;
 }
 template <class T, class M>
 int launch_pd_tile(evr_ctx* ctx, int K, const Q4<T>* in, const M& m, Q4<T>* out) {
-  constexpr int RPT = TileShape<T>::RPT, G = TileShape<T>::G;
+  constexpr int RPT = TileShape<T>::RPT, G = TileShape<T>::G, MB = TileShape<T>::MINB;
   const evr_config& g = ctx->cfg;
   const int H = ctx->H, W = ctx->W;
   cudaStream_t s = ctx->stream;
   const T tau = (T)g.tau, sigma = (T)g.sigma, lo = (T)g.u_min, hi = (T)g.u_max;
   if (K == 2)
-    launch_pdl2(k_pd_tile<T, 2, RPT, G, M>, tile_grid<T, 2>(ctx), 32 * G, s, in, m, out, H, W,
+    launch_pdl2(k_pd_tile<T, 2, RPT, G, MB, M>, tile_grid<T, 2>(ctx), 32 * G, s, in, m, out, H, W,
                 tau, sigma, lo, hi);
   else if (K == 3)
-    launch_pdl2(k_pd_tile<T, 3, RPT, G, M>, tile_grid<T, 3>(ctx), 32 * G, s, in, m, out, H, W,
+    launch_pdl2(k_pd_tile<T, 3, RPT, G, MB, M>, tile_grid<T, 3>(ctx), 32 * G, s, in, m, out, H, W,
                 tau, sigma, lo, hi);
   else
-    launch_pdl2(k_pd_tile<T, 4, RPT, G, M>, tile_grid<T, 4>(ctx), 32 * G, s, in, m, out, H, W,
+    launch_pdl2(k_pd_tile<T, 4, RPT, G, MB, M>, tile_grid<T, 4>(ctx), 32 * G, s, in, m, out, H, W,
                 tau, sigma, lo, hi);
   return 1;
 }

@@ -37,14 +37,22 @@ template <> struct Arith<double> {
     return __dadd_rn(__dmul_rn(a, b), c);
   }
 };
+// The .ftz forms are single MUFU ops (+ FMUL for the quotient); without
+// .ftz ptxas wraps each in a subnormal range test and rescale.  The float
+// engine's operands (u in [u_min, u_max], slopes, duals in the unit ball)
+// are never subnormal where it matters.
 template <> struct Arith<float> {
-  static __device__ __forceinline__ float div(float a, float b) { return __fdividef(a, b); }
+  static __device__ __forceinline__ float div(float a, float b) {
+    float r;
+    asm("div.approx.ftz.f32 %0, %1, %2;" : "=f"(r) : "f"(a), "f"(b));
+    return r;
+  }
   static __device__ __forceinline__ float mad(float a, float b, float c) {
     return __fmaf_rn(a, b, c);
   }
   static __device__ __forceinline__ float sqrt(float x) {
     float r;
-    asm("sqrt.approx.f32 %0, %1;" : "=f"(r) : "f"(x));
+    asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
     return r;
   }
 };

@@ -34,8 +34,8 @@ namespace evr {
 
 // TV-L1 (surface.py:167-193), K iterations: dual ascent + projection, then
 // divergence + L1 shrink + over-relaxation.  f0 is the t plane.
-template <class T, int K, int RPT, int G>
-__global__ void __launch_bounds__(32 * G)
+template <class T, int K, int RPT, int G, int MINB>
+__global__ void __launch_bounds__(32 * G, MINB)
 k_tv_tile(const Q4<T>* __restrict__ in, const T* __restrict__ f0, Q4<T>* __restrict__ out,
           int H, int W, T sigma, T tau, T shrink) {
   constexpr int RH = G * RPT, TIW = 32 - 2 * K, TIH = RH - 2 * K;
@@ -98,8 +98,8 @@ k_tv_tile(const Q4<T>* __restrict__ in, const T* __restrict__ f0, Q4<T>* __restr
 // The metric constants of the region are loaded once (M: MetricPackF32
 // recomputes the matrix from the slopes, MetricPackF64 reads it) and stay
 // in registers for the K iterations.
-template <class T, int K, int RPT, int G, class M>
-__global__ void __launch_bounds__(32 * G)
+template <class T, int K, int RPT, int G, int MINB, class M>
+__global__ void __launch_bounds__(32 * G, MINB)
 k_pd_tile(const Q4<T>* __restrict__ in, M m, Q4<T>* __restrict__ out, int H, int W, T tau,
           T sigma, T umin, T umax) {
   constexpr int RH = G * RPT, TIW = 32 - 2 * K, TIH = RH - 2 * K;

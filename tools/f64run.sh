@@ -1,0 +1,7 @@
+for v in main v64a v64b v64c v64d; do
+  if [ $v = main ]; then L=paper_1607_06283_b200/libevr.so; else L=build_variants/$v.so; fi
+  for c in C3 C4; do for k in 1 2 3 4; do
+    [ $v != main ] && [ $k = 1 ] && continue
+    EVR_LIBRARY=$L EVR_TILE_K=$k timeout 300 python bench.py --config $c --precision f64 --no-cpu-baseline --steps 20 --warmup 3 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read().strip().splitlines()[-1]); print('$v $c f64 K=$k', d['ms_per_step'], d['roofline']['frac'])"
+  done; done
+done
