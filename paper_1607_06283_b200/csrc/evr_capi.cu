@@ -364,7 +364,7 @@ void relchange(evr_ctx* ctx, const T* un, const T* u, int iterations, int stride
 #define EVR_TILE32_G 8
 #endif
 #ifndef EVR_TILE32_MINB
-#define EVR_TILE32_MINB 1
+#define EVR_TILE32_MINB 2
 #endif
 #ifndef EVR_TILE64_RPT
 #define EVR_TILE64_RPT 4
@@ -382,8 +382,32 @@ template <> struct TileShape<float> {
 template <> struct TileShape<double> {
   static constexpr int RPT = EVR_TILE64_RPT, G = EVR_TILE64_G, MINB = EVR_TILE64_MINB;
 };
-template <class T, int K> dim3 tile_grid(const evr_ctx* c) {
-  constexpr int TIW = 32 - 2 * K, TIH = TileShape<T>::G * TileShape<T>::RPT - 2 * K;
+// Rows per thread of a context's tiles: the float kernels come in RPT = 8,
+// 7, 6 (regions of 64, 56, 48 rows); the one whose whole waves (MINB CTAs
+// per SM) cover the sensor with the fewest region rows per SM wins -- e.g.
+// 1280x720, K = 4: RPT 8 -> 702 tiles = 2.4 waves rounded to 3, RPT 7 ->
+// 810 tiles = 2.7 waves, 12 % fewer rows computed per SM.
+int sm_count(int device) {
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+  return sms;
+}
+template <class T> int tile_rpt(const evr_ctx* c, int K) {
+  constexpr int G = TileShape<T>::G;
+  if (!std::is_same<T, float>::value || TileShape<T>::RPT != 8) return TileShape<T>::RPT;
+  const int64_t slots = (int64_t)sm_count(c->device) * TileShape<T>::MINB;
+  int best = 8;
+  int64_t best_cost = -1;
+  for (int rpt = 8; rpt >= 6; --rpt) {
+    const int tiw = 32 - 2 * K, tih = G * rpt - 2 * K;
+    const int64_t ctas = (int64_t)((c->W + tiw - 1) / tiw) * ((c->H + tih - 1) / tih);
+    const int64_t cost = (ctas + slots - 1) / slots * (G * rpt);
+    if (best_cost < 0 || cost < best_cost) best = rpt, best_cost = cost;
+  }
+  return best;
+}
+template <class T, int K, int RPT> dim3 tile_grid(const evr_ctx* c) {
+  constexpr int TIW = 32 - 2 * K, TIH = TileShape<T>::G * RPT - 2 * K;
   return dim3((c->W + TIW - 1) / TIW, (c->H + TIH - 1) / TIH);
 }
 template <class... KArgs, class... Args>
@@ -399,39 +423,60 @@ void launch_pdl2(void (*k)(KArgs...), dim3 grid, unsigned block, cudaStream_t s,
   lc.numAttrs = pdl_enabled() ? 1 : 0;
   cudaLaunchKernelEx(&lc, k, std::forward<Args>(args)...);
 }
-template <class T>
-int launch_tv_tile(evr_ctx* ctx, int K, const Q4<T>* in, const T* f0, Q4<T>* out, T sigma,
-                   T tau, T shrink) {
-  constexpr int RPT = TileShape<T>::RPT, G = TileShape<T>::G, MB = TileShape<T>::MINB;
+template <class T, int RPT>
+void tv_tile_rpt(evr_ctx* ctx, int K, const Q4<T>* in, const T* f0, Q4<T>* out, T sigma, T tau,
+                 T shrink) {
+  constexpr int G = TileShape<T>::G, MB = TileShape<T>::MINB;
   const int H = ctx->H, W = ctx->W;
   cudaStream_t s = ctx->stream;
   if (K == 2)
-    launch_pdl2(k_tv_tile<T, 2, RPT, G, MB>, tile_grid<T, 2>(ctx), 32 * G, s, in, f0, out, H, W,
-                sigma, tau, shrink);
+    launch_pdl2(k_tv_tile<T, 2, RPT, G, MB>, tile_grid<T, 2, RPT>(ctx), 32 * G, s, in, f0, out,
+                H, W, sigma, tau, shrink);
   else if (K == 3)
-    launch_pdl2(k_tv_tile<T, 3, RPT, G, MB>, tile_grid<T, 3>(ctx), 32 * G, s, in, f0, out, H, W,
-                sigma, tau, shrink);
+    launch_pdl2(k_tv_tile<T, 3, RPT, G, MB>, tile_grid<T, 3, RPT>(ctx), 32 * G, s, in, f0, out,
+                H, W, sigma, tau, shrink);
   else
-    launch_pdl2(k_tv_tile<T, 4, RPT, G, MB>, tile_grid<T, 4>(ctx), 32 * G, s, in, f0, out, H, W,
-                sigma, tau, shrink);
+    launch_pdl2(k_tv_tile<T, 4, RPT, G, MB>, tile_grid<T, 4, RPT>(ctx), 32 * G, s, in, f0, out,
+                H, W, sigma, tau, shrink);
+}
+template <class T>
+int launch_tv_tile(evr_ctx* ctx, int K, const Q4<T>* in, const T* f0, Q4<T>* out, T sigma,
+                   T tau, T shrink) {
+  constexpr int R0 = TileShape<T>::RPT;
+  const int rpt = tile_rpt<T>(ctx, K);
+  if constexpr (std::is_same<T, float>::value && R0 == 8) {
+    if (rpt == 7) return tv_tile_rpt<T, 7>(ctx, K, in, f0, out, sigma, tau, shrink), 1;
+    if (rpt == 6) return tv_tile_rpt<T, 6>(ctx, K, in, f0, out, sigma, tau, shrink), 1;
+  }
+  tv_tile_rpt<T, R0>(ctx, K, in, f0, out, sigma, tau, shrink);
   return 1;
 }
-template <class T, class M>
-int launch_pd_tile(evr_ctx* ctx, int K, const Q4<T>* in, const M& m, Q4<T>* out) {
-  constexpr int RPT = TileShape<T>::RPT, G = TileShape<T>::G, MB = TileShape<T>::MINB;
+template <class T, int RPT, class M>
+void pd_tile_rpt(evr_ctx* ctx, int K, const Q4<T>* in, const M& m, Q4<T>* out) {
+  constexpr int G = TileShape<T>::G, MB = TileShape<T>::MINB;
   const evr_config& g = ctx->cfg;
   const int H = ctx->H, W = ctx->W;
   cudaStream_t s = ctx->stream;
   const T tau = (T)g.tau, sigma = (T)g.sigma, lo = (T)g.u_min, hi = (T)g.u_max;
   if (K == 2)
-    launch_pdl2(k_pd_tile<T, 2, RPT, G, MB, M>, tile_grid<T, 2>(ctx), 32 * G, s, in, m, out, H, W,
-                tau, sigma, lo, hi);
+    launch_pdl2(k_pd_tile<T, 2, RPT, G, MB, M>, tile_grid<T, 2, RPT>(ctx), 32 * G, s, in, m, out,
+                H, W, tau, sigma, lo, hi);
   else if (K == 3)
-    launch_pdl2(k_pd_tile<T, 3, RPT, G, MB, M>, tile_grid<T, 3>(ctx), 32 * G, s, in, m, out, H, W,
-                tau, sigma, lo, hi);
+    launch_pdl2(k_pd_tile<T, 3, RPT, G, MB, M>, tile_grid<T, 3, RPT>(ctx), 32 * G, s, in, m, out,
+                H, W, tau, sigma, lo, hi);
   else
-    launch_pdl2(k_pd_tile<T, 4, RPT, G, MB, M>, tile_grid<T, 4>(ctx), 32 * G, s, in, m, out, H, W,
-                tau, sigma, lo, hi);
+    launch_pdl2(k_pd_tile<T, 4, RPT, G, MB, M>, tile_grid<T, 4, RPT>(ctx), 32 * G, s, in, m, out,
+                H, W, tau, sigma, lo, hi);
+}
+template <class T, class M>
+int launch_pd_tile(evr_ctx* ctx, int K, const Q4<T>* in, const M& m, Q4<T>* out) {
+  constexpr int R0 = TileShape<T>::RPT;
+  const int rpt = tile_rpt<T>(ctx, K);
+  if constexpr (std::is_same<T, float>::value && R0 == 8) {
+    if (rpt == 7) return pd_tile_rpt<T, 7>(ctx, K, in, m, out), 1;
+    if (rpt == 6) return pd_tile_rpt<T, 6>(ctx, K, in, m, out), 1;
+  }
+  pd_tile_rpt<T, R0>(ctx, K, in, m, out);
   return 1;
 }
 
@@ -1269,7 +1314,7 @@ int evr_engine_detail(evr_ctx* ctx, char* buf, int len) {
       const int tk = ctx->tile_k > 0 ? ctx->tile_k : tile_k(ctx->prec);
       if (tk > 1) {
         const bool d = ctx->prec == EVR_PREC_F64;
-        const int rpt = d ? TileShape<double>::RPT : TileShape<float>::RPT;
+        const int rpt = d ? tile_rpt<double>(ctx, tk) : tile_rpt<float>(ctx, tk);
         const int G = d ? TileShape<double>::G : TileShape<float>::G;
         const int tiw = 32 - 2 * tk, tih = G * rpt - 2 * tk;
         snprintf(buf, len,

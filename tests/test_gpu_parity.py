@@ -325,7 +325,8 @@ def test_float32_register_engine_matches_streaming_bitwise():
 
 @pytest.mark.parametrize("precision", [0, 1])
 @pytest.mark.parametrize("H,W,tv,pd", [(150, 97, 13, 9), (61, 29, 4, 5), (7, 300, 3, 2),
-                                        (260, 346, 50, 50)])
+                                        (260, 346, 50, 50), (720, 1280, 9, 10),
+                                        (2048, 1100, 5, 6)])
 def test_tile_kernels_bitwise_equal_to_march(H, W, tv, pd, precision):
     """Temporally blocked tiles (K = 2, 3, 4 iterations per launch) give the
     bits of one march launch per iteration, chained over packets, in float64
@@ -352,7 +353,7 @@ def test_tile_kernels_bitwise_equal_to_march(H, W, tv, pd, precision):
         for (a, ra), (b, rb) in zip(out[1][0], out[k][0]):
             assert np.array_equal(a, b) and ra == rb
         assert np.array_equal(out[1][1], out[k][1])
-    if precision == 0:  # and the oracle
+    if precision == 0 and H * W <= 100_000:  # and the oracle
         ref = O.OracleStream(H, W, O.make_config(max_iterations=pd, denoise_iterations=tv))
         for s in range(0, 3 * n, n):
             ref.process(np.ascontiguousarray(ev[s:s + n]))
