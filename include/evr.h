@@ -290,6 +290,21 @@ int evr_op_to_gray(evr_ctx *ctx, const double *image, double lo, double hi,
 int evr_op_rof_solve(evr_ctx *ctx, const double *f, const double *tx,
                      const double *ty, const double *G, const double *sqrtG,
                      double lam, int iterations, double *u_out);
+/* Not in the reference (BASELINE configs[1] names them; parity unpinned,
+ * restated in oracle/evr_oracle.c): manifold TV with the L1 data term
+ * lam * sum |u - f| sqrtG (rof_manifold_solve's loop, cold start), and
+ * second-order manifold TGV
+ *   min_{u,w} alpha1 |A (grad u - w)|_g + alpha0 |E w| + D(u, f)
+ * with D = KL (data_term 0, box [u_min, u_max]), ROF (1) or L1 (2); w_out
+ * (H, W, 2) may be NULL. */
+int evr_op_l1_solve(evr_ctx *ctx, const double *f, const double *tx,
+                    const double *ty, const double *G, const double *sqrtG,
+                    double lam, int iterations, double *u_out);
+int evr_op_tgv_solve(evr_ctx *ctx, const double *f, const double *tx,
+                     const double *ty, const double *G, const double *sqrtG,
+                     double lam, double alpha0, double alpha1, int data_term,
+                     double u_min, double u_max, int iterations,
+                     double *u_out, double *w_out);
 
 /* ---- event simulator: simulate.py:51-103 generate_events - */
 /* Events of a (n, H, W) stack of LOG intensities (the caller takes np.log,

@@ -461,6 +461,161 @@ void evo_rof_solve(const double *f, const double *tx, const double *ty,
     pd_loop_free(&L);
 }
 
+/* ---- data-term / regulariser variants the reference does not ship ------
+ * (BASELINE configs[1]: "TV and TGV regularisers, KL vs ROF/L1 data terms").
+ * Parity is UNPINNED against the reference (it has no such code); these
+ * restate the published algorithms (Chambolle-Pock 2011 primal-dual; TGV of
+ * Bredies-Kunisch-Pock 2010) on the reference's manifold operators, in the
+ * operation order the CUDA kernels use, so the GPU is checked bit for bit. */
+
+/* data-term prox at one pixel: t1 = div*tau + u (the descent point),
+ * beta = (tau*lam)*sqrtG.  kind 0 = KL (solve.py:235-242, box), 1 = ROF
+ * (solve.py:283-287), 2 = L1 (|u - f| sqrtG: soft shrink toward f, the
+ * surface denoiser's rule surface.py:188-191 with a per-pixel threshold). */
+static inline double data_prox(int kind, double t1, double f, double beta,
+                               double u_min, double u_max) {
+    if (kind == 0) {
+        const double s = t1 - beta;
+        return dclip((s + sqrt(s * s + (4.0 * beta) * f)) * 0.5, u_min, u_max);
+    }
+    if (kind == 1) return (t1 + beta * f) * (1.0 / (1.0 + beta));
+    const double g = dclip(t1 - f, -beta, beta);
+    return t1 - g;
+}
+
+/* Manifold TV with the L1 data term: rof_manifold_solve's loop (cold start
+ * u = f, p = 0, tau = sigma = 1/sqrt(8+4*sqrt2)) with the L1 prox. */
+void evo_l1_solve(const double *f, const double *tx, const double *ty,
+                  const double *G, const double *sqrtG, int H, int W,
+                  double lam, int iters, double *u_out) {
+    const int64_t N = (int64_t)H * W;
+    const double step = 1.0 / sqrt(8.0 + 4.0 * sqrt(2.0));
+    const double tl = step * lam;
+    pd_loop L;
+    pd_loop_init(&L, tx, ty, G, H, W, f, NULL, step);
+    for (int it = 0; it < iters; ++it) {
+        pd_descent_point(&L, step, L.un);
+#pragma omp parallel for schedule(static)
+        for (int64_t k = 0; k < N; ++k) {
+            L.un[k] = data_prox(2, L.un[k], f[k], tl * sqrtG[k], 0.0, 0.0);
+            L.v[k] = L.un[k] * 2.0 - L.u[k];
+        }
+        pd_dual_ascent(&L, L.v, sqrtG);
+        double *tmp = L.u;
+        L.u = L.un;
+        L.un = tmp;
+    }
+    memcpy(u_out, L.u, sizeof(double) * N);
+    pd_loop_free(&L);
+}
+
+/* Second-order manifold TGV:
+ *   min_{u,w} alpha1 |A (grad u - w)|_g + alpha0 |E w| + D(u, f)
+ * E w = (fx w1, fy w2, (fy w1 + fx w2) / 2) (forward differences, 0 on the
+ * last column / row, like grad_x / grad_y), |q|^2 = q11^2 + q22^2 + 2 q12^2;
+ * E* q = -(div(q11, q12), div(q12, q22)) with div_xy.  Chambolle-Pock with
+ * tau = sigma = 1/sqrt(17 + 4*sqrt2) (|A grad|^2 <= 8 + 4*sqrt2, |A| <= 1,
+ * |E|^2 <= 8).  Cold start u = f, w = p = q = 0.  Per iteration:
+ *   q = A^T p; u+ = prox_D(div(q)*tau + u);
+ *   w+ = w + (q + div_sym)*tau, div_sym = (div(q11, q12), div(q12, q22));
+ *   u_bar = u+*2 - u, w_bar = w+*2 - w;
+ *   p = proj_{alpha1 sqrtG}(p + sigma A (grad u_bar - w_bar));
+ *   Q = proj_{alpha0}(Q + sigma E w_bar).
+ * w_out (may be NULL) receives w as (H, W, 2). */
+void evo_tgv_solve(const double *f, const double *tx, const double *ty,
+                   const double *G, const double *sqrtG, int H, int W,
+                   double lam, double alpha0, double alpha1, int kind,
+                   double u_min, double u_max, int iters, double *u_out,
+                   double *w_out) {
+    const int64_t N = (int64_t)H * W;
+    const double step = 1.0 / sqrt(17.0 + 4.0 * sqrt(2.0));
+    const double tl = step * lam;
+    pd_loop L;
+    pd_loop_init(&L, tx, ty, G, H, W, f, NULL, step);
+    double *w1 = calloc(N, sizeof(double)), *w2 = calloc(N, sizeof(double));
+    double *w1n = malloc(sizeof(double) * N), *w2n = malloc(sizeof(double) * N);
+    double *b1 = malloc(sizeof(double) * N), *b2 = malloc(sizeof(double) * N);
+    double *q11 = calloc(N, sizeof(double)), *q22 = calloc(N, sizeof(double));
+    double *q12 = calloc(N, sizeof(double));
+    const coeffs_t c = L.c;
+    double *const *sa = L.sa;
+    for (int it = 0; it < iters; ++it) {
+#pragma omp parallel for schedule(static)
+        for (int64_t k = 0; k < N; ++k) {
+            L.qx[k] = c.a11[k] * L.p1[k] + c.a12[k] * L.p2[k] + c.a31[k] * L.p3[k];
+            L.qy[k] = c.a12[k] * L.p1[k] + c.a22[k] * L.p2[k] + c.a32[k] * L.p3[k];
+        }
+#pragma omp parallel for schedule(static)
+        for (int i = 0; i < H; ++i)
+            for (int j = 0; j < W; ++j) {
+                const int64_t k = IDX(i, j);
+                const double t1 = div_at(L.qx, L.qy, H, W, i, j) * step + L.u[k];
+                L.un[k] = data_prox(kind, t1, f[k], tl * sqrtG[k], u_min, u_max);
+                L.v[k] = L.un[k] * 2.0 - L.u[k];
+                const double e1 = div_at(q11, q12, H, W, i, j);
+                const double e2 = div_at(q12, q22, H, W, i, j);
+                w1n[k] = w1[k] + (L.qx[k] + e1) * step;
+                w2n[k] = w2[k] + (L.qy[k] + e2) * step;
+                b1[k] = w1n[k] * 2.0 - w1[k];
+                b2[k] = w2n[k] * 2.0 - w2[k];
+            }
+#pragma omp parallel for schedule(static)
+        for (int i = 0; i < H; ++i)
+            for (int j = 0; j < W; ++j) {
+                const int64_t k = IDX(i, j);
+                const double *v = L.v;
+                const double gx = (j < W - 1 ? v[k + 1] - v[k] : 0.0) - b1[k];
+                const double gy = (i < H - 1 ? v[k + W] - v[k] : 0.0) - b2[k];
+                double p1 = L.p1[k] + sa[0][k] * gx + sa[1][k] * gy;
+                double p2 = L.p2[k] + sa[1][k] * gx + sa[2][k] * gy;
+                double p3 = L.p3[k] + sa[3][k] * gx + sa[4][k] * gy;
+                double n = sqrt(p1 * p1 + p2 * p2 + p3 * p3);
+                n = n / (alpha1 * sqrtG[k]);
+                n = dmax(n, 1.0);
+                L.p1[k] = p1 / n;
+                L.p2[k] = p2 / n;
+                L.p3[k] = p3 / n;
+                const double e11 = j < W - 1 ? b1[k + 1] - b1[k] : 0.0;
+                const double e22 = i < H - 1 ? b2[k + W] - b2[k] : 0.0;
+                const double e12 = ((i < H - 1 ? b1[k + W] - b1[k] : 0.0) +
+                                    (j < W - 1 ? b2[k + 1] - b2[k] : 0.0)) * 0.5;
+                const double a = q11[k] + step * e11;
+                const double b = q22[k] + step * e22;
+                const double d = q12[k] + step * e12;
+                double m = sqrt(a * a + b * b + (d * d) * 2.0);
+                m = dmax(m / alpha0, 1.0);
+                q11[k] = a / m;
+                q22[k] = b / m;
+                q12[k] = d / m;
+            }
+        double *tmp = L.u;
+        L.u = L.un;
+        L.un = tmp;
+        tmp = w1;
+        w1 = w1n;
+        w1n = tmp;
+        tmp = w2;
+        w2 = w2n;
+        w2n = tmp;
+    }
+    memcpy(u_out, L.u, sizeof(double) * N);
+    if (w_out)
+        for (int64_t k = 0; k < N; ++k) {
+            w_out[2 * k] = w1[k];
+            w_out[2 * k + 1] = w2[k];
+        }
+    free(w1);
+    free(w2);
+    free(w1n);
+    free(w2n);
+    free(b1);
+    free(b2);
+    free(q11);
+    free(q22);
+    free(q12);
+    pd_loop_free(&L);
+}
+
 /* pipeline.py:142-171 process_packet (non-empty packet) with the window of
  * pipeline.py:128-132 supplied by the caller. */
 int evo_process_packet(double *u, double *f, int64_t *raw, double *p, int H,

@@ -105,6 +105,18 @@ void evo_rof_solve(const double *f, const double *tx, const double *ty,
                    const double *G, const double *sqrtG, int H, int W,
                    double lam, int iters, double *u_out);
 
+/* Not in the reference (parity unpinned, see evr_oracle.c): manifold TV
+ * with the L1 data term, and second-order manifold TGV with data term kind
+ * 0 = KL (box [u_min, u_max]), 1 = ROF, 2 = L1.  w_out (H,W,2) may be NULL. */
+void evo_l1_solve(const double *f, const double *tx, const double *ty,
+                  const double *G, const double *sqrtG, int H, int W,
+                  double lam, int iters, double *u_out);
+void evo_tgv_solve(const double *f, const double *tx, const double *ty,
+                   const double *G, const double *sqrtG, int H, int W,
+                   double lam, double alpha0, double alpha1, int kind,
+                   double u_min, double u_max, int iters, double *u_out,
+                   double *w_out);
+
 /* pipeline.py:142-171 process_packet for a non-empty packet, given the
  * window the caller derived from packet_starts (pipeline.py:124-132).
  * State arrays are updated in place; t_out/tx_out/... (may be NULL) receive

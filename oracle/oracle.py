@@ -85,6 +85,8 @@ def lib():
         L.evo_pd_solve.argtypes = [P, P, P, P, P, i32, i32, P, P, P, P, P, P]
         L.evo_pd_solve.restype = i32
         L.evo_rof_solve.argtypes = [P, P, P, P, P, i32, i32, d, i32, P]
+        L.evo_l1_solve.argtypes = [P, P, P, P, P, i32, i32, d, i32, P]
+        L.evo_tgv_solve.argtypes = [P, P, P, P, P, i32, i32, d, d, d, i32, d, d, i32, P, P]
         L.evo_process_packet.argtypes = [P, P, P, P, i32, i32, P, i64, d, P, P, P, P]
         L.evo_process_packet.restype = i32
         L.evo_num_threads.restype = i32
@@ -236,6 +238,31 @@ def rof_solve(f, tx, ty, G, sqrtG, lam, iterations=200):
     lib().evo_rof_solve(_p(f), _p(_f64(tx)), _p(_f64(ty)), _p(_f64(G)), _p(_f64(sqrtG)),
                         f.shape[0], f.shape[1], lam, iterations, _p(out))
     return out
+
+
+def l1_solve(f, tx, ty, G, sqrtG, lam, iterations=200):
+    """Manifold TV + L1 data term (not in the reference: parity unpinned)."""
+    f = _f64(f)
+    out = np.empty_like(f)
+    lib().evo_l1_solve(_p(f), _p(_f64(tx)), _p(_f64(ty)), _p(_f64(G)), _p(_f64(sqrtG)),
+                       f.shape[0], f.shape[1], lam, iterations, _p(out))
+    return out
+
+
+DATA_TERMS = {"kl": 0, "rof": 1, "l1": 2}
+
+
+def tgv_solve(f, tx, ty, G, sqrtG, lam, alpha0=2.0, alpha1=1.0, data="kl", u_min=1.0,
+              u_max=2.0, iterations=200):
+    """Second-order manifold TGV (not in the reference: parity unpinned).
+    Returns (u, w) with w of shape (H, W, 2)."""
+    f = _f64(f)
+    out = np.empty_like(f)
+    w = np.empty(f.shape + (2,))
+    lib().evo_tgv_solve(_p(f), _p(_f64(tx)), _p(_f64(ty)), _p(_f64(G)), _p(_f64(sqrtG)),
+                        f.shape[0], f.shape[1], lam, alpha0, alpha1, DATA_TERMS[data], u_min,
+                        u_max, iterations, _p(out), _p(w))
+    return out, w
 
 
 # --- packet driver -----------------------------------------------------------

@@ -140,6 +140,8 @@ _SIGNATURES = {
     "evr_op_pd_solve": ([_P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P], _i32),
     "evr_op_to_gray": ([_P, _P, _d, _d, _P], _i32),
     "evr_op_rof_solve": ([_P, _P, _P, _P, _P, _P, _d, _i32, _P], _i32),
+    "evr_op_l1_solve": ([_P, _P, _P, _P, _P, _P, _d, _i32, _P], _i32),
+    "evr_op_tgv_solve": ([_P, _P, _P, _P, _P, _P, _d, _d, _d, _i32, _d, _d, _i32, _P, _P], _i32),
 }
 
 _lib = None

@@ -111,6 +111,7 @@ struct evr_ctx {
   int64_t fr_ticket[kFrameSlots] = {-1, -1, -1, -1};
   int64_t fr_next = 0;
   int* h_err = nullptr;  // pinned error-flag read-back of evr_synchronize
+  double* tgv = nullptr;  // operator API TGV planes (9 x N), allocated on first use
   std::string err;
 
   template <class T> T* fld(int k) const { return reinterpret_cast<T*>(slab + field_stride * k); }
@@ -1257,6 +1258,7 @@ void evr_destroy(evr_ctx* ctx) {
     if (ctx->fr_done[i]) cudaEventDestroy(ctx->fr_done[i]);
   }
   cudaFree(ctx->d_rec);
+  cudaFree(ctx->tgv);
   if (ctx->h_rec) cudaFreeHost(ctx->h_rec);
   if (ctx->cstream) cudaStreamDestroy(ctx->cstream);
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
@@ -1914,6 +1916,97 @@ int evr_op_rof_solve(evr_ctx* ctx, const double* f, const double* tx, const doub
   ctx->launches += 1 + 2 * (int64_t)iterations;
   if ((rc = launch_err(ctx, "rof"))) return rc;
   return d2h_sync(ctx, u_out, bufs[iterations & 1], B);
+}
+
+// Manifold TV + L1 data term (not in the reference; parity unpinned, CPU
+// restatement oracle/evr_oracle.c evo_l1_solve): rof_manifold_solve's loop
+// (solve.py:264-293) with the L1 prox.
+int evr_op_l1_solve(evr_ctx* ctx, const double* f, const double* tx, const double* ty,
+                    const double* G, const double* sqrtG, double lam, int iterations,
+                    double* u_out) {
+  OP_PROLOGUE(true);
+  if (!(lam > 0)) return fail(ctx, EVR_ERR_INVALID, "lam must be positive, got %g", lam);
+  int rc;
+  if ((rc = upload_metric(ctx, tx, ty, G, sqrtG))) return rc;
+  double* fdev = ctx->aos_b;
+  if ((rc = h2d(ctx, fdev, f, B))) return rc;
+  CK(cudaMemcpyAsync(ctx->fld<double>(F_U), fdev, B, cudaMemcpyDeviceToDevice, s));
+  for (int k : {F_P1, F_P2, F_P3}) CK(cudaMemsetAsync(ctx->fld<double>(k), 0, B, s));
+  const double step = 1.0 / std::sqrt(8.0 + 4.0 * std::sqrt(2.0));
+  k_solver_setup<double><<<grid1d(N), kNT, 0, s>>>(
+      ctx->fld<double>(F_TX), ctx->fld<double>(F_TY), ctx->fld<double>(F_G), ctx->fld<double>(F_SG),
+      fdev, coefs<double>(ctx), ctx->fld<double>(F_BETA), ctx->fld<double>(F_FB), N, step * lam, 0);
+  double* bufs[2] = {ctx->fld<double>(F_U), ctx->fld<double>(F_UN)};
+  for (int it = 0; it < iterations; ++it) {
+    double* v = ctx->fld<double>(F_V);
+    k_l1_primal<double><<<grid2d(ctx), block2d(), 0, s>>>(
+        ctx->fld<double>(F_P1), ctx->fld<double>(F_P2), ctx->fld<double>(F_P3), coefs<double>(ctx),
+        bufs[it & 1], ctx->fld<double>(F_SG), fdev, bufs[(it + 1) & 1], v, ctx->geo_own(), step,
+        step * lam);
+    k_pd_dual<double><<<grid2d(ctx), block2d(), 0, s>>>(v, ctx->fld<double>(F_P1), ctx->fld<double>(F_P2),
+                                                        ctx->fld<double>(F_P3), coefs<double>(ctx),
+                                                        ctx->fld<double>(F_SG), ctx->geo_own(), step);
+  }
+  ctx->launches += 1 + 2 * (int64_t)iterations;
+  if ((rc = launch_err(ctx, "l1"))) return rc;
+  return d2h_sync(ctx, u_out, bufs[iterations & 1], B);
+}
+
+// Second-order manifold TGV with a KL / ROF / L1 data term (not in the
+// reference; parity unpinned, CPU restatement oracle/evr_oracle.c
+// evo_tgv_solve).  Cold start u = f, w = p = Q = 0; tau = sigma =
+// 1/sqrt(17 + 4*sqrt2).  w_out (H, W, 2) may be NULL.
+int evr_op_tgv_solve(evr_ctx* ctx, const double* f, const double* tx, const double* ty,
+                     const double* G, const double* sqrtG, double lam, double alpha0,
+                     double alpha1, int data_term, double u_min, double u_max, int iterations,
+                     double* u_out, double* w_out) {
+  OP_PROLOGUE(true);
+  if (!(lam > 0)) return fail(ctx, EVR_ERR_INVALID, "lam must be positive, got %g", lam);
+  if (!(alpha0 > 0) || !(alpha1 > 0))
+    return fail(ctx, EVR_ERR_INVALID, "TGV weights must be positive, got alpha0=%g alpha1=%g",
+                alpha0, alpha1);
+  if (data_term < 0 || data_term > 2)
+    return fail(ctx, EVR_ERR_INVALID, "unknown data term %d", data_term);
+  if (data_term == 0 && !(u_min < u_max))
+    return fail(ctx, EVR_ERR_INVALID, "box must satisfy u_min < u_max");
+  int rc;
+  if (!ctx->tgv) CK(cudaMalloc(&ctx->tgv, 9 * B));
+  if ((rc = upload_metric(ctx, tx, ty, G, sqrtG))) return rc;
+  double* fdev = ctx->aos_b;
+  if ((rc = h2d(ctx, fdev, f, B))) return rc;
+  CK(cudaMemcpyAsync(ctx->fld<double>(F_U), fdev, B, cudaMemcpyDeviceToDevice, s));
+  for (int k : {F_P1, F_P2, F_P3}) CK(cudaMemsetAsync(ctx->fld<double>(k), 0, B, s));
+  double* t = ctx->tgv;
+  CK(cudaMemsetAsync(t, 0, 9 * B, s));
+  const double step = 1.0 / std::sqrt(17.0 + 4.0 * std::sqrt(2.0));
+  k_solver_setup<double><<<grid1d(N), kNT, 0, s>>>(
+      ctx->fld<double>(F_TX), ctx->fld<double>(F_TY), ctx->fld<double>(F_G), ctx->fld<double>(F_SG),
+      fdev, coefs<double>(ctx), ctx->fld<double>(F_BETA), ctx->fld<double>(F_FB), N, step * lam, 0);
+  double* ub[2] = {ctx->fld<double>(F_U), ctx->fld<double>(F_UN)};
+  double* w[2][2] = {{t, t + N}, {t + 2 * N, t + 3 * N}};
+  for (int it = 0; it < iterations; ++it) {
+    const int a = it & 1;
+    TgvPlanes<double> tp{w[a][0], w[a][1], w[a ^ 1][0], w[a ^ 1][1], t + 4 * N, t + 5 * N,
+                         t + 6 * N, t + 7 * N, t + 8 * N};
+    double* v = ctx->fld<double>(F_V);
+    k_tgv_primal<double><<<grid2d(ctx), block2d(), 0, s>>>(
+        ctx->fld<double>(F_P1), ctx->fld<double>(F_P2), ctx->fld<double>(F_P3), coefs<double>(ctx),
+        ub[a], ctx->fld<double>(F_SG), fdev, ub[a ^ 1], v, tp, ctx->geo_own(), step, step * lam,
+        data_term, u_min, u_max);
+    k_tgv_dual<double><<<grid2d(ctx), block2d(), 0, s>>>(
+        v, tp, ctx->fld<double>(F_P1), ctx->fld<double>(F_P2), ctx->fld<double>(F_P3),
+        coefs<double>(ctx), ctx->fld<double>(F_SG), ctx->geo_own(), step, alpha0, alpha1);
+  }
+  ctx->launches += 1 + 2 * (int64_t)iterations;
+  if ((rc = launch_err(ctx, "tgv"))) return rc;
+  if (w_out) {  // (H, W, 2) interleaved
+    double* wl = w[iterations & 1][0];
+    CK(cudaMemcpy2DAsync(w_out, 2 * sizeof(double), wl, sizeof(double), sizeof(double), N,
+                         cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpy2DAsync(w_out + 1, 2 * sizeof(double), wl + N, sizeof(double), sizeof(double),
+                         N, cudaMemcpyDeviceToHost, s));
+  }
+  return d2h_sync(ctx, u_out, ub[iterations & 1], B);
 }
 
 }  // extern "C"

@@ -239,6 +239,113 @@ __global__ void k_rof_primal(const T* __restrict__ p1, const T* __restrict__ p2,
   v[k] = Arith<T>::mad(nu, T(2), -uk);
 }
 
+// ---- variants the reference does not ship (parity unpinned; the CPU
+// oracle oracle/evr_oracle.c evo_l1_solve / evo_tgv_solve restates them in
+// this operation order): the L1 data term and second-order manifold TGV.
+
+// data-term prox of the descent point t1 with beta = (tau*lam)*sqrtG:
+// kind 0 = KL (box), 1 = ROF, 2 = L1 (soft shrink toward f)
+template <class T>
+__device__ __forceinline__ T data_prox(int kind, T t1, T f, T beta, T umin, T umax) {
+  if (kind == 0) {
+    const T s = t1 - beta;
+    return vclip((s + Arith<T>::sqrt(Arith<T>::mad(s, s, (T(4) * beta) * f))) * T(0.5), umin,
+                 umax);
+  }
+  if (kind == 1) return Arith<T>::mad(beta, f, t1) * Arith<T>::div(T(1), T(1) + beta);
+  const T g = vclip(t1 - f, -beta, beta);
+  return t1 - g;
+}
+
+// manifold TV + L1 data term: rof_manifold_solve's primal with the L1 prox
+template <class T>
+__global__ void k_l1_primal(const T* __restrict__ p1, const T* __restrict__ p2,
+                            const T* __restrict__ p3, CoefPlanes<T> c,
+                            const T* __restrict__ u, const T* __restrict__ sg,
+                            const double* __restrict__ f, T* __restrict__ un, T* __restrict__ v,
+                            Geo g, T tau, T tl) {
+  EVR_GEO_INDEX
+  const T d = div_q(c, p1, p2, p3, gi, j, g.Htot, W, k);
+  const T uk = u[k];
+  const T nu = data_prox(2, Arith<T>::mad(d, tau, uk), (T)f[k], tl * sg[k], T(0), T(0));
+  un[k] = nu;
+  v[k] = Arith<T>::mad(nu, T(2), -uk);
+}
+
+// TGV state planes: w (in), w+ (out), w_bar (out), symmetric dual Q
+template <class T> struct TgvPlanes {
+  T *w1, *w2, *w1n, *w2n, *b1, *b2, *q11, *q22, *q12;
+};
+
+// TGV primal: u+ = prox_D(div(A^T p)*tau + u), w+ = w + (A^T p + div_sym Q)*tau,
+// over-relaxed u_bar (v) and w_bar
+template <class T>
+__global__ void k_tgv_primal(const T* __restrict__ p1, const T* __restrict__ p2,
+                             const T* __restrict__ p3, CoefPlanes<T> c,
+                             const T* __restrict__ u, const T* __restrict__ sg,
+                             const double* __restrict__ f, T* __restrict__ un,
+                             T* __restrict__ v, TgvPlanes<T> tp, Geo g, T tau, T tl, int kind,
+                             T umin, T umax) {
+  EVR_GEO_INDEX
+  const int H = g.Htot;
+  T qx, qy, qxl = T(0), qyu = T(0), dummy;
+  q_at(c, p1, p2, p3, k, qx, qy);
+  if (j > 0) q_at(c, p1, p2, p3, k - 1, qxl, dummy);
+  if (gi > 0) q_at(c, p1, p2, p3, k - W, dummy, qyu);
+  const T d = div_at(qx, qxl, qy, qyu, gi, j, H, W);
+  const T uk = u[k];
+  const T nu = data_prox(kind, Arith<T>::mad(d, tau, uk), (T)f[k], tl * sg[k], umin, umax);
+  un[k] = nu;
+  v[k] = Arith<T>::mad(nu, T(2), -uk);
+  const T e1 = div_at(tp.q11[k], j > 0 ? tp.q11[k - 1] : T(0), tp.q12[k],
+                      gi > 0 ? tp.q12[k - W] : T(0), gi, j, H, W);
+  const T e2 = div_at(tp.q12[k], j > 0 ? tp.q12[k - 1] : T(0), tp.q22[k],
+                      gi > 0 ? tp.q22[k - W] : T(0), gi, j, H, W);
+  const T w1 = tp.w1[k], w2 = tp.w2[k];
+  const T n1 = Arith<T>::mad(qx + e1, tau, w1), n2 = Arith<T>::mad(qy + e2, tau, w2);
+  tp.w1n[k] = n1;
+  tp.w2n[k] = n2;
+  tp.b1[k] = Arith<T>::mad(n1, T(2), -w1);
+  tp.b2[k] = Arith<T>::mad(n2, T(2), -w2);
+}
+
+// TGV dual: p = proj_{alpha1 sqrtG}(p + sigma A (grad u_bar - w_bar)),
+// Q = proj_{alpha0}(Q + sigma E w_bar), |Q|^2 = q11^2 + q22^2 + 2 q12^2
+template <class T>
+__global__ void k_tgv_dual(const T* __restrict__ v, TgvPlanes<T> tp, T* __restrict__ p1,
+                           T* __restrict__ p2, T* __restrict__ p3, CoefPlanes<T> c,
+                           const T* __restrict__ sg, Geo g, T sigma, T alpha0, T alpha1) {
+  EVR_GEO_INDEX
+  const int H = g.Htot;
+  const bool xr = j < W - 1, yd = gi < H - 1;
+  const T* b1 = tp.b1;
+  const T* b2 = tp.b2;
+  const T gx = (xr ? v[k + 1] - v[k] : T(0)) - b1[k];
+  const T gy = (yd ? v[k + W] - v[k] : T(0)) - b2[k];
+  const Coef<T> a = c.at(k);
+  const T s11 = sigma * a.a11, s12 = sigma * a.a12, s22 = sigma * a.a22;
+  const T s31 = sigma * a.a31, s32 = sigma * a.a32;
+  const T q1 = Arith<T>::mad(s12, gy, Arith<T>::mad(s11, gx, p1[k]));
+  const T q2 = Arith<T>::mad(s22, gy, Arith<T>::mad(s12, gx, p2[k]));
+  const T q3 = Arith<T>::mad(s32, gy, Arith<T>::mad(s31, gx, p3[k]));
+  T n = Arith<T>::sqrt(Arith<T>::mad(q3, q3, Arith<T>::mad(q2, q2, q1 * q1)));
+  n = vmax(Arith<T>::div(n, alpha1 * sg[k]), T(1));
+  p1[k] = Arith<T>::div(q1, n);
+  p2[k] = Arith<T>::div(q2, n);
+  p3[k] = Arith<T>::div(q3, n);
+  const T e11 = xr ? b1[k + 1] - b1[k] : T(0);
+  const T e22 = yd ? b2[k + W] - b2[k] : T(0);
+  const T e12 = ((yd ? b1[k + W] - b1[k] : T(0)) + (xr ? b2[k + 1] - b2[k] : T(0))) * T(0.5);
+  const T qa = Arith<T>::mad(sigma, e11, tp.q11[k]);
+  const T qb = Arith<T>::mad(sigma, e22, tp.q22[k]);
+  const T qd = Arith<T>::mad(sigma, e12, tp.q12[k]);
+  T m = Arith<T>::sqrt(Arith<T>::mad(qd * qd, T(2), Arith<T>::mad(qb, qb, qa * qa)));
+  m = vmax(Arith<T>::div(m, alpha0), T(1));
+  tp.q11[k] = Arith<T>::div(qa, m);
+  tp.q22[k] = Arith<T>::div(qb, m);
+  tp.q12[k] = Arith<T>::div(qd, m);
+}
+
 // dual ascent + ball projection (solve.py:170-201)
 template <class T>
 __global__ void k_pd_dual(const T* __restrict__ v, T* __restrict__ p1, T* __restrict__ p2,

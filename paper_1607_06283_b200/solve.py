@@ -149,3 +149,64 @@ def rof_manifold_solve(f, m, lam, iterations=200):
                              _lib.ptr(_f64(m.ty)), _lib.ptr(_f64(m.G)), _lib.ptr(_f64(m.sqrtG)),
                              ctypes.c_double(lam), int(iterations), _lib.ptr(out))
     return out
+
+
+# --- variants the reference does not ship -----------------------------------
+# BASELINE configs[1] names "TV and TGV regularisers, KL vs ROF/L1 data
+# terms"; the reference has the KL (primal_dual_solve) and ROF
+# (rof_manifold_solve) data terms with manifold TV only.  These two follow
+# the published algorithms on the reference's manifold operators; their
+# parity is against the CPU restatement (oracle/evr_oracle.c), not the
+# reference.
+
+DATA_TERMS = {"kl": 0, "rof": 1, "l1": 2}
+
+
+def l1_manifold_solve(f, m, lam, iterations=200):
+    """Manifold TV with the L1 data term lam * sum |u - f| sqrtG:
+    rof_manifold_solve's loop with the soft-shrink prox (no box, cold start)."""
+    if lam <= 0:
+        raise ValueError(f"lam must be positive, got {lam}")
+    if f.shape != m.shape:
+        raise ValueError(f"image shape {f.shape} != metric shape {m.shape}")
+    f = _f64(f)
+    out = np.empty_like(f)
+    op_context(f.shape).call("evr_op_l1_solve", _lib.ptr(f), _lib.ptr(_f64(m.tx)),
+                             _lib.ptr(_f64(m.ty)), _lib.ptr(_f64(m.G)), _lib.ptr(_f64(m.sqrtG)),
+                             ctypes.c_double(lam), int(iterations), _lib.ptr(out))
+    return out
+
+
+def tgv_manifold_solve(f, m, lam, alpha0=2.0, alpha1=1.0, iterations=200, data="kl",
+                       cfg: SolverConfig | None = None, return_w=False):
+    """Second-order manifold TGV:
+
+        min_{u,w}  alpha1 |A (grad u - w)|_g + alpha0 |E w| + D(u, f)
+
+    with the reference's metric matrix A (surface_gradient) and
+    g-tensor norm, the symmetrised gradient E w, and D the KL (box from
+    ``cfg``, default SolverConfig()), ROF or L1 data term.  Chambolle-Pock,
+    tau = sigma = 1/sqrt(17 + 4 sqrt 2), cold start u = f.  Returns u, or
+    (u, w) with w of shape (H, W, 2) when ``return_w``."""
+    if lam <= 0:
+        raise ValueError(f"lam must be positive, got {lam}")
+    if alpha0 <= 0 or alpha1 <= 0:
+        raise ValueError(f"TGV weights must be positive, got alpha0={alpha0} alpha1={alpha1}")
+    if data not in DATA_TERMS:
+        raise ValueError(f"data term must be one of {sorted(DATA_TERMS)}, got {data!r}")
+    if f.shape != m.shape:
+        raise ValueError(f"image shape {f.shape} != metric shape {m.shape}")
+    cfg = cfg or SolverConfig()
+    f = _f64(f)
+    if data == "kl" and (np.any(f < cfg.u_min) or np.any(f > cfg.u_max)):
+        raise ValueError(f"f must lie in the box [{cfg.u_min}, {cfg.u_max}]")
+    out = np.empty_like(f)
+    w = np.empty(f.shape + (2,)) if return_w else None
+    op_context(f.shape).call("evr_op_tgv_solve", _lib.ptr(f), _lib.ptr(_f64(m.tx)),
+                             _lib.ptr(_f64(m.ty)), _lib.ptr(_f64(m.G)), _lib.ptr(_f64(m.sqrtG)),
+                             ctypes.c_double(lam), ctypes.c_double(alpha0),
+                             ctypes.c_double(alpha1), DATA_TERMS[data],
+                             ctypes.c_double(cfg.u_min), ctypes.c_double(cfg.u_max),
+                             int(iterations), _lib.ptr(out), _lib.ptr(w))
+    return (out, w) if return_w else out
+

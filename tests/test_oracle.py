@@ -196,3 +196,48 @@ def test_duplicate_events_are_order_sensitive():
     want = min(max(min(max(min(max(1.95 * c_pos, 1.0), 2.0) * c_neg, 1.0), 2.0) * c_pos, 1.0), 2.0)
     assert f[0, 0] == want
     assert raw[0, 0] == 3
+
+
+# --- variants the reference does not ship (parity unpinned) -----------------
+# TGV and the L1 data term restate published algorithms; these property
+# tests pin the restatement's behaviour instead of reference vectors.
+
+
+def _flat(H, W):
+    z = np.zeros((H, W))
+    return z, z, np.ones((H, W)), np.ones((H, W))
+
+
+def test_tgv_keeps_affine_ramps_that_tv_flattens():
+    """TGV's w absorbs a constant gradient (E w = 0), so an affine ramp is a
+    minimiser of TGV-ROF; TV-ROF shrinks its contrast at the borders."""
+    H, W = 40, 50
+    yy, xx = np.mgrid[0:H, 0:W]
+    f = 1.2 + 0.01 * xx + 0.005 * yy
+    m = _flat(H, W)
+    u, w = O.tgv_solve(f, *m, lam=8.0, data="rof", iterations=500)
+    ut = O.rof_solve(f, *m, 8.0, 500)
+    assert np.abs(u - f).max() < 0.2 * np.abs(ut - f).max()
+    inner = (slice(2, -2), slice(2, -2))
+    assert abs(w[..., 0][inner].mean() - 0.01) < 2e-3 and abs(w[..., 1][inner].mean() - 0.005) < 2e-3
+
+
+def test_tgv_and_l1_fixed_points_and_denoising():
+    H, W = 24, 30
+    m = _flat(H, W)
+    c = np.full((H, W), 1.4)
+    for data in ("kl", "rof", "l1"):  # a constant image is a fixed point
+        u, w = O.tgv_solve(c, *m, lam=2.0, data=data, iterations=60)
+        assert np.array_equal(u, c) and not w.any()
+    assert np.array_equal(O.l1_solve(c, *m, 2.0, 60), c)
+    rng = np.random.default_rng(0)
+    xx = np.mgrid[0:H, 0:W][1]
+    clean = np.where(xx < W // 2, 1.3, 1.7)
+    noisy = np.clip(clean + rng.normal(0, 0.05, (H, W)), 1.0, 2.0)
+    for data, lam in (("kl", 8.0), ("rof", 8.0), ("l1", 1.0)):
+        u, _ = O.tgv_solve(noisy, *m, lam=lam, data=data, iterations=300)
+        assert np.abs(u - clean).mean() < 0.6 * np.abs(noisy - clean).mean()
+    # L1 removes an isolated outlier completely (TV-L1's defining property)
+    spike = c.copy()
+    spike[10, 10] = 1.9
+    assert abs(O.l1_solve(spike, *m, 1.0, 400)[10, 10] - 1.4) < 1e-3
