@@ -28,6 +28,7 @@
 // to the one-iteration-per-launch kernels.
 #pragma once
 
+#include "evr_fastdp.cuh"
 #include "evr_kernels.cuh"
 
 namespace evr {
@@ -62,14 +63,50 @@ k_tv_tile(const Q4<T>* __restrict__ in, const T* __restrict__ f0, Q4<T>* __restr
     ub_top[g][l] = ub[0];
     __syncthreads();
     const T ub_below = ub_top[g < G - 1 ? g + 1 : g][l];
+    if constexpr (sizeof(T) == 8) {
+      // float64: branch-free fast div / sqrt so the rows' latency chains
+      // overlap (evr_fastdp.cuh; rare out-of-range rows redone with IEEE)
+      T dx[RPT], dy[RPT], nx[RPT], ny[RPT], nn[RPT];
+      bool slow = false, proj = false;
 #pragma unroll
-    for (int r = 0; r < RPT; ++r) {  // dual (surface.py:168-183)
-      const int gi = gi0 + r;
-      const T ub_r = __shfl_down_sync(0xffffffffu, ub[r], 1);
-      const T ub_n = r < RPT - 1 ? ub[r + 1] : ub_below;
-      const T dx = gj < W - 1 ? ub_r - ub[r] : T(0);
-      const T dy = gi < H - 1 ? ub_n - ub[r] : T(0);
-      tv_dual_step(dx, dy, sigma, px[r], py[r]);
+      for (int r = 0; r < RPT; ++r) {  // dual (surface.py:168-183)
+        const int gi = gi0 + r;
+        const T ub_r = __shfl_down_sync(0xffffffffu, ub[r], 1);
+        const T ub_n = r < RPT - 1 ? ub[r + 1] : ub_below;
+        dx[r] = gj < W - 1 ? ub_r - ub[r] : T(0);
+        dy[r] = gi < H - 1 ? ub_n - ub[r] : T(0);
+        nx[r] = px[r];
+        ny[r] = py[r];
+        nn[r] = tv_dual_pre_fx(dx[r], dy[r], sigma, nx[r], ny[r], slow);
+        proj |= nn[r] != T(1);
+      }
+      if (__any_sync(0xffffffffu, proj)) {
+#pragma unroll
+        for (int r = 0; r < RPT; ++r) fdp_div2(nx[r], ny[r], nn[r], slow);
+      }
+      if (slow) {
+#pragma unroll
+        for (int r = 0; r < RPT; ++r) {
+          nx[r] = px[r];
+          ny[r] = py[r];
+          tv_dual_step(dx[r], dy[r], sigma, nx[r], ny[r]);
+        }
+      }
+#pragma unroll
+      for (int r = 0; r < RPT; ++r) {
+        px[r] = nx[r];
+        py[r] = ny[r];
+      }
+    } else {
+#pragma unroll
+      for (int r = 0; r < RPT; ++r) {  // dual (surface.py:168-183)
+        const int gi = gi0 + r;
+        const T ub_r = __shfl_down_sync(0xffffffffu, ub[r], 1);
+        const T ub_n = r < RPT - 1 ? ub[r + 1] : ub_below;
+        const T dx = gj < W - 1 ? ub_r - ub[r] : T(0);
+        const T dy = gi < H - 1 ? ub_n - ub[r] : T(0);
+        tv_dual_step(dx, dy, sigma, px[r], py[r]);
+      }
     }
     py_bot[g][l] = py[RPT - 1];
     __syncthreads();
@@ -131,27 +168,78 @@ k_pd_tile(const Q4<T>* __restrict__ in, M m, Q4<T>* __restrict__ out, int H, int
     qy_bot[g][l] = qy[RPT - 1];
     __syncthreads();
     const T qy_above = qy_bot[g > 0 ? g - 1 : g][l];
+    {
+      T d[RPT], nu[RPT];
+      bool slow = false;
 #pragma unroll
-    for (int r = 0; r < RPT; ++r) {  // primal (solve.py:233-245)
-      const int gi = gi0 + r;
-      const T qxl = __shfl_up_sync(0xffffffffu, qx[r], 1);
-      const T qyu = r > 0 ? qy[r - 1] : qy_above;
-      const T d = div_at(qx[r], gj > 0 ? qxl : T(0), qy[r], gi > 0 ? qyu : T(0), gi, gj, H, W);
-      const T nu = kl_primal(d, u[r], beta[r], fb[r], tau, umin, umax);
-      v[r] = Arith<T>::mad(nu, T(2), -u[r]);
-      u[r] = nu;
+      for (int r = 0; r < RPT; ++r) {  // primal (solve.py:233-245)
+        const int gi = gi0 + r;
+        const T qxl = __shfl_up_sync(0xffffffffu, qx[r], 1);
+        const T qyu = r > 0 ? qy[r - 1] : qy_above;
+        d[r] = div_at(qx[r], gj > 0 ? qxl : T(0), qy[r], gi > 0 ? qyu : T(0), gi, gj, H, W);
+        if constexpr (sizeof(T) == 8)
+          nu[r] = kl_primal_fx(d[r], u[r], beta[r], fb[r], tau, umin, umax, slow);
+        else
+          nu[r] = kl_primal(d[r], u[r], beta[r], fb[r], tau, umin, umax);
+      }
+      if (sizeof(T) == 8 && slow) {
+#pragma unroll
+        for (int r = 0; r < RPT; ++r) nu[r] = kl_primal(d[r], u[r], beta[r], fb[r], tau, umin, umax);
+      }
+#pragma unroll
+      for (int r = 0; r < RPT; ++r) {
+        v[r] = Arith<T>::mad(nu[r], T(2), -u[r]);
+        u[r] = nu[r];
+      }
     }
     v_top[g][l] = v[0];
     __syncthreads();
     const T v_below = v_top[g < G - 1 ? g + 1 : g][l];
+    if constexpr (sizeof(T) == 8) {
+      T gx[RPT], gy[RPT], n1[RPT], n2[RPT], n3[RPT], nn[RPT];
+      bool slow = false, proj = false;
 #pragma unroll
-    for (int r = 0; r < RPT; ++r) {  // dual (solve.py:246-252)
-      const int gi = gi0 + r;
-      const T vr = __shfl_down_sync(0xffffffffu, v[r], 1);
-      const T vd = r < RPT - 1 ? v[r + 1] : v_below;
-      const T gx = gj < W - 1 ? vr - v[r] : T(0);
-      const T gy = gi < H - 1 ? vd - v[r] : T(0);
-      dual_step(cf[r], sigma, gx, gy, sg[r], p1[r], p2[r], p3[r]);
+      for (int r = 0; r < RPT; ++r) {  // dual (solve.py:246-252)
+        const int gi = gi0 + r;
+        const T vr = __shfl_down_sync(0xffffffffu, v[r], 1);
+        const T vd = r < RPT - 1 ? v[r + 1] : v_below;
+        gx[r] = gj < W - 1 ? vr - v[r] : T(0);
+        gy[r] = gi < H - 1 ? vd - v[r] : T(0);
+        n1[r] = p1[r];
+        n2[r] = p2[r];
+        n3[r] = p3[r];
+        nn[r] = dual_pre_fx(cf[r], sigma, gx[r], gy[r], sg[r], n1[r], n2[r], n3[r], slow);
+        proj |= nn[r] != T(1);
+      }
+      if (__any_sync(0xffffffffu, proj)) {
+#pragma unroll
+        for (int r = 0; r < RPT; ++r) fdp_div3(n1[r], n2[r], n3[r], nn[r], slow);
+      }
+      if (slow) {
+#pragma unroll
+        for (int r = 0; r < RPT; ++r) {
+          n1[r] = p1[r];
+          n2[r] = p2[r];
+          n3[r] = p3[r];
+          dual_step(cf[r], sigma, gx[r], gy[r], sg[r], n1[r], n2[r], n3[r]);
+        }
+      }
+#pragma unroll
+      for (int r = 0; r < RPT; ++r) {
+        p1[r] = n1[r];
+        p2[r] = n2[r];
+        p3[r] = n3[r];
+      }
+    } else {
+#pragma unroll
+      for (int r = 0; r < RPT; ++r) {  // dual (solve.py:246-252)
+        const int gi = gi0 + r;
+        const T vr = __shfl_down_sync(0xffffffffu, v[r], 1);
+        const T vd = r < RPT - 1 ? v[r + 1] : v_below;
+        const T gx = gj < W - 1 ? vr - v[r] : T(0);
+        const T gy = gi < H - 1 ? vd - v[r] : T(0);
+        dual_step(cf[r], sigma, gx, gy, sg[r], p1[r], p2[r], p3[r]);
+      }
     }
   }
   if (l < K || l >= 32 - K || gj >= W) return;
