@@ -401,7 +401,8 @@ template <class T> int tile_rpt(const evr_ctx* c, int K) {
   int64_t best_cost = -1;
   for (int rpt = 8; rpt >= 6; --rpt) {
     const int tiw = 32 - 2 * K, tih = G * rpt - 2 * K;
-    const int64_t ctas = (int64_t)((c->W + tiw - 1) / tiw) * ((c->H + tih - 1) / tih);
+    const int64_t ctas =
+        (int64_t)((c->W + tiw - 1) / tiw) * ((c->own_hi - c->own_lo + tih) / tih);
     const int64_t cost = (ctas + slots - 1) / slots * (G * rpt);
     if (best_cost < 0 || cost < best_cost) best = rpt, best_cost = cost;
   }
@@ -409,7 +410,8 @@ template <class T> int tile_rpt(const evr_ctx* c, int K) {
 }
 template <class T, int K, int RPT> dim3 tile_grid(const evr_ctx* c) {
   constexpr int TIW = 32 - 2 * K, TIH = TileShape<T>::G * RPT - 2 * K;
-  return dim3((c->W + TIW - 1) / TIW, (c->H + TIH - 1) / TIH);
+  const int rows = c->own_hi - c->own_lo + 1;
+  return dim3((c->W + TIW - 1) / TIW, (rows + TIH - 1) / TIH);
 }
 template <class... KArgs, class... Args>
 void launch_pdl2(void (*k)(KArgs...), dim3 grid, unsigned block, cudaStream_t s, Args&&... args) {
@@ -424,60 +426,75 @@ void launch_pdl2(void (*k)(KArgs...), dim3 grid, unsigned block, cudaStream_t s,
   lc.numAttrs = pdl_enabled() ? 1 : 0;
   cudaLaunchKernelEx(&lc, k, std::forward<Args>(args)...);
 }
-template <class T, int RPT>
-void tv_tile_rpt(evr_ctx* ctx, int K, const Q4<T>* in, const T* f0, Q4<T>* out, T sigma, T tau,
-                 T shrink) {
+template <class T, int RPT, bool B>
+void tv_tile_rpt(evr_ctx* ctx, int K, const MarchRows<Q4<T>>& in, const MarchRows<T>& f0,
+                 Q4<T>* out, T sigma, T tau, T shrink) {
   constexpr int G = TileShape<T>::G, MB = TileShape<T>::MINB;
-  const int H = ctx->H, W = ctx->W;
+  const int H = ctx->Htot, W = ctx->W;
   cudaStream_t s = ctx->stream;
   if (K == 2)
-    launch_pdl2(k_tv_tile<T, 2, RPT, G, MB>, tile_grid<T, 2, RPT>(ctx), 32 * G, s, in, f0, out,
+    launch_pdl2(k_tv_tile<T, 2, RPT, G, MB, B>, tile_grid<T, 2, RPT>(ctx), 32 * G, s, in, f0, out,
                 H, W, sigma, tau, shrink);
   else if (K == 3)
-    launch_pdl2(k_tv_tile<T, 3, RPT, G, MB>, tile_grid<T, 3, RPT>(ctx), 32 * G, s, in, f0, out,
+    launch_pdl2(k_tv_tile<T, 3, RPT, G, MB, B>, tile_grid<T, 3, RPT>(ctx), 32 * G, s, in, f0, out,
                 H, W, sigma, tau, shrink);
   else
-    launch_pdl2(k_tv_tile<T, 4, RPT, G, MB>, tile_grid<T, 4, RPT>(ctx), 32 * G, s, in, f0, out,
+    launch_pdl2(k_tv_tile<T, 4, RPT, G, MB, B>, tile_grid<T, 4, RPT>(ctx), 32 * G, s, in, f0, out,
                 H, W, sigma, tau, shrink);
 }
-template <class T>
-int launch_tv_tile(evr_ctx* ctx, int K, const Q4<T>* in, const T* f0, Q4<T>* out, T sigma,
-                   T tau, T shrink) {
+template <class T, bool B>
+void tv_tile_shape(evr_ctx* ctx, int K, const MarchRows<Q4<T>>& in, const MarchRows<T>& f0,
+                   Q4<T>* out, T sigma, T tau, T shrink) {
   constexpr int R0 = TileShape<T>::RPT;
   const int rpt = tile_rpt<T>(ctx, K);
   if constexpr (std::is_same<T, float>::value && R0 == 8) {
-    if (rpt == 7) return tv_tile_rpt<T, 7>(ctx, K, in, f0, out, sigma, tau, shrink), 1;
-    if (rpt == 6) return tv_tile_rpt<T, 6>(ctx, K, in, f0, out, sigma, tau, shrink), 1;
+    if (rpt == 7) return tv_tile_rpt<T, 7, B>(ctx, K, in, f0, out, sigma, tau, shrink);
+    if (rpt == 6) return tv_tile_rpt<T, 6, B>(ctx, K, in, f0, out, sigma, tau, shrink);
   }
-  tv_tile_rpt<T, R0>(ctx, K, in, f0, out, sigma, tau, shrink);
+  tv_tile_rpt<T, R0, B>(ctx, K, in, f0, out, sigma, tau, shrink);
+}
+template <class T>
+int launch_tv_tile(evr_ctx* ctx, int K, const MarchRows<Q4<T>>& in, const MarchRows<T>& f0,
+                   Q4<T>* out, T sigma, T tau, T shrink) {
+  if (ctx->banded)
+    tv_tile_shape<T, true>(ctx, K, in, f0, out, sigma, tau, shrink);
+  else
+    tv_tile_shape<T, false>(ctx, K, in, f0, out, sigma, tau, shrink);
   return 1;
 }
-template <class T, int RPT, class M>
-void pd_tile_rpt(evr_ctx* ctx, int K, const Q4<T>* in, const M& m, Q4<T>* out) {
+template <class T, int RPT, bool B, class M>
+void pd_tile_rpt(evr_ctx* ctx, int K, const MarchRows<Q4<T>>& in, const M& m, Q4<T>* out) {
   constexpr int G = TileShape<T>::G, MB = TileShape<T>::MINB;
   const evr_config& g = ctx->cfg;
-  const int H = ctx->H, W = ctx->W;
+  const int H = ctx->Htot, W = ctx->W;
   cudaStream_t s = ctx->stream;
   const T tau = (T)g.tau, sigma = (T)g.sigma, lo = (T)g.u_min, hi = (T)g.u_max;
   if (K == 2)
-    launch_pdl2(k_pd_tile<T, 2, RPT, G, MB, M>, tile_grid<T, 2, RPT>(ctx), 32 * G, s, in, m, out,
-                H, W, tau, sigma, lo, hi);
+    launch_pdl2(k_pd_tile<T, 2, RPT, G, MB, M, B>, tile_grid<T, 2, RPT>(ctx), 32 * G, s, in, m,
+                out, H, W, tau, sigma, lo, hi);
   else if (K == 3)
-    launch_pdl2(k_pd_tile<T, 3, RPT, G, MB, M>, tile_grid<T, 3, RPT>(ctx), 32 * G, s, in, m, out,
-                H, W, tau, sigma, lo, hi);
+    launch_pdl2(k_pd_tile<T, 3, RPT, G, MB, M, B>, tile_grid<T, 3, RPT>(ctx), 32 * G, s, in, m,
+                out, H, W, tau, sigma, lo, hi);
   else
-    launch_pdl2(k_pd_tile<T, 4, RPT, G, MB, M>, tile_grid<T, 4, RPT>(ctx), 32 * G, s, in, m, out,
-                H, W, tau, sigma, lo, hi);
+    launch_pdl2(k_pd_tile<T, 4, RPT, G, MB, M, B>, tile_grid<T, 4, RPT>(ctx), 32 * G, s, in, m,
+                out, H, W, tau, sigma, lo, hi);
 }
-template <class T, class M>
-int launch_pd_tile(evr_ctx* ctx, int K, const Q4<T>* in, const M& m, Q4<T>* out) {
+template <class T, bool B, class M>
+void pd_tile_shape(evr_ctx* ctx, int K, const MarchRows<Q4<T>>& in, const M& m, Q4<T>* out) {
   constexpr int R0 = TileShape<T>::RPT;
   const int rpt = tile_rpt<T>(ctx, K);
   if constexpr (std::is_same<T, float>::value && R0 == 8) {
-    if (rpt == 7) return pd_tile_rpt<T, 7>(ctx, K, in, m, out), 1;
-    if (rpt == 6) return pd_tile_rpt<T, 6>(ctx, K, in, m, out), 1;
+    if (rpt == 7) return pd_tile_rpt<T, 7, B>(ctx, K, in, m, out);
+    if (rpt == 6) return pd_tile_rpt<T, 6, B>(ctx, K, in, m, out);
   }
-  pd_tile_rpt<T, R0>(ctx, K, in, m, out);
+  pd_tile_rpt<T, R0, B>(ctx, K, in, m, out);
+}
+template <class T, class M>
+int launch_pd_tile(evr_ctx* ctx, int K, const MarchRows<Q4<T>>& in, const M& m, Q4<T>* out) {
+  if (ctx->banded)
+    pd_tile_shape<T, true>(ctx, K, in, m, out);
+  else
+    pd_tile_shape<T, false>(ctx, K, in, m, out);
   return 1;
 }
 
@@ -547,8 +564,10 @@ template <class T> int launch_step(evr_ctx* ctx, const Step& st) {
       const auto in = march_rows<Q4<T>>(ctx, [a](const evr_ctx* c) { return packed<T>(c).tv[a]; }, 1);
       Q4<T>* out = packed<T>(ctx).tv[a ^ 1];
       const T sh = (T)(step * g.denoise_weight);
-      if (st.k > 1)
-        return launch_tv_tile<T>(ctx, st.k, in.own, (const T*)t, out, (T)step, (T)step, sh);
+      if (st.k > 1) {
+        const auto f0 = march_rows<T>(ctx, [](const evr_ctx* c) { return c->fld<T>(F_T); }, 1);
+        return launch_tv_tile<T>(ctx, st.k, in, f0, out, (T)step, (T)step, sh);
+      }
       if (ctx->banded)
         launch_pdl(k_tv_march<T, kMarchRY, MarchDepth<T>::tv, true>, march_grid(ctx), kMarchNT, s,
                    in.own, in, (const T*)t, out, ctx->Htot, ctx->W, (T)step, (T)step, sh);
@@ -586,7 +605,7 @@ template <class T> int launch_step(evr_ctx* ctx, const Step& st) {
       else
         m = M{cr.own, cr};
       Q4<T>* out = packed<T>(ctx).pd[a ^ 1];
-      if (st.k > 1) return launch_pd_tile<T>(ctx, st.k, in.own, m, out);
+      if (st.k > 1) return launch_pd_tile<T>(ctx, st.k, in, m, out);
       if (ctx->banded)
         launch_pdl(k_pd_march<T, kMarchRY, MarchDepth<T>::pd, M, true>, march_grid(ctx), kMarchNT,
                    s, in.own, in, m, out, ctx->Htot, ctx->W, (T)g.tau, (T)g.sigma, (T)g.u_min,
@@ -2139,7 +2158,12 @@ int exchange_after(evr_group* grp, int kind) {
 }
 
 template <class T> int group_packet(evr_group* grp) {
-  const std::vector<Step> steps = packet_steps(grp->cfg, 2, grp->fused);
+  // fused bands run the tiles too (K rows of each neighbour read in place)
+  // when every band has at least K own rows
+  int tk = grp->fused ? tile_k(grp->prec) : 1;
+  for (const evr_ctx* c : grp->band)
+    if (c->own_hi - c->own_lo + 1 < tk) tk = 1;
+  const std::vector<Step> steps = packet_steps(grp->cfg, 2, grp->fused, tk);
   const int n = grp->n;
   for (const Step& st : steps) {
     for (int b = 0; b < n; ++b) {

@@ -407,9 +407,19 @@ template <class T> struct alignas(4 * sizeof(T)) Q4 {
 // exchange is part of the iteration kernel itself.
 template <class Q> struct MarchRows {
   const Q* own;
-  const Q* up;  // row y0 - 1 of the band above (BANDED only)
-  const Q* dn;  // row y1 of the band below (BANDED only)
+  const Q* up;  // row y0 - 1 of the band above (BANDED only; the tile kernels
+                // also read rows y0 - K .. y0 - 2 at negative row offsets)
+  const Q* dn;  // row y1 of the band below (BANDED only; tiles: .. y1 + K - 1)
   int y0, y1, olo, E;
+  // element of global row gr (a band's own rows or K rows either side)
+  template <bool BANDED> __device__ __forceinline__ const Q& at(int gr, int jc, int W) const {
+    if constexpr (BANDED)
+      return gr < y0   ? up[(int64_t)(gr - y0 + 1) * W + jc]
+             : gr >= y1 ? dn[(int64_t)(gr - y1) * W + jc]
+                        : own[(int64_t)(gr - y0 + olo) * W + jc];
+    else
+      return own[gr * W + jc];
+  }
 };
 
 struct Strip {
@@ -504,8 +514,8 @@ struct MetricPackF32 {
   template <bool BANDED>
   __device__ __forceinline__ Raw load(int gr, int y1, int jc, int W) const {
     if constexpr (BANDED)
-      return gr < rows.y0 ? rows.up[jc]
-             : gr >= y1   ? rows.dn[jc]
+      return gr < rows.y0 ? rows.up[(int64_t)(gr - rows.y0 + 1) * W + jc]
+             : gr >= y1   ? rows.dn[(int64_t)(gr - y1) * W + jc]
                           : c[(int64_t)(gr - rows.y0 + rows.olo) * W + jc];
     else
       return c[gr * W + jc];
@@ -528,8 +538,8 @@ struct MetricPackF64 {
   template <bool BANDED>
   __device__ __forceinline__ Raw load(int gr, int y1, int jc, int W) const {
     if constexpr (BANDED) {
-      const Q4<double>* p = gr < rows.y0 ? rows.up + 2 * jc
-                            : gr >= y1   ? rows.dn + 2 * jc
+      const Q4<double>* p = gr < rows.y0 ? rows.up + 2 * ((int64_t)(gr - rows.y0 + 1) * W + jc)
+                            : gr >= y1   ? rows.dn + 2 * ((int64_t)(gr - y1) * W + jc)
                                          : c + 2 * ((int64_t)(gr - rows.y0 + rows.olo) * W + jc);
       return Raw{p[0], p[1]};
     } else {

@@ -35,28 +35,34 @@ namespace evr {
 
 // TV-L1 (surface.py:167-193), K iterations: dual ascent + projection, then
 // divergence + L1 shrink + over-relaxation.  f0 is the t plane.
-template <class T, int K, int RPT, int G, int MINB>
+// Band contexts (evr_group, BANDED): the tiles cover the band's own rows
+// [y0, y1) and read the K rows either side from the neighbour bands'
+// buffers in place (MarchRows::at; peer memory across GPUs); out is
+// indexed like in.own.
+template <class T, int K, int RPT, int G, int MINB, bool BANDED>
 __global__ void __launch_bounds__(32 * G, MINB)
-k_tv_tile(const Q4<T>* __restrict__ in, const T* __restrict__ f0, Q4<T>* __restrict__ out,
-          int H, int W, T sigma, T tau, T shrink) {
+k_tv_tile(const MarchRows<Q4<T>> in, const MarchRows<T> f0, Q4<T>* __restrict__ out, int H,
+          int W, T sigma, T tau, T shrink) {
   constexpr int RH = G * RPT, TIW = 32 - 2 * K, TIH = RH - 2 * K;
   __shared__ T ub_top[G][32];  // u_bar of each warp's first row
   __shared__ T py_bot[G][32];  // py of each warp's last row
   const int l = threadIdx.x & 31, g = threadIdx.x >> 5;
+  const int y0 = BANDED ? in.y0 : 0, y1 = BANDED ? in.y1 : H;
+  const int rlo = max(y0 - K, 0), rhi = min(y1 + K, H) - 1;  // rows a tile may read
   const int gj = (int)blockIdx.x * TIW - K + l;
-  const int gi0 = (int)blockIdx.y * TIH - K + g * RPT;
+  const int gi0 = y0 + (int)blockIdx.y * TIH - K + g * RPT;
   const int jc = min(max(gj, 0), W - 1);
   pdl_wait_and_release();
   T u[RPT], ub[RPT], px[RPT], py[RPT], f[RPT];
 #pragma unroll
   for (int r = 0; r < RPT; ++r) {
-    const int k = min(max(gi0 + r, 0), H - 1) * W + jc;
-    const Q4<T> q = in[k];
+    const int gr = min(max(gi0 + r, rlo), rhi);
+    const Q4<T> q = in.template at<BANDED>(gr, jc, W);
     u[r] = q.x;
     ub[r] = q.y;
     px[r] = q.z;
     py[r] = q.w;
-    f[r] = f0[k];
+    f[r] = f0.template at<BANDED>(gr, jc, W);
   }
 #pragma unroll 1
   for (int it = 0; it < K; ++it) {
@@ -126,7 +132,8 @@ k_tv_tile(const Q4<T>* __restrict__ in, const T* __restrict__ f0, Q4<T>* __restr
 #pragma unroll
   for (int r = 0; r < RPT; ++r) {
     const int R = g * RPT + r, gi = gi0 + r;
-    if (R >= K && R < RH - K && gi < H) out[gi * W + gj] = Q4<T>{u[r], ub[r], px[r], py[r]};
+    if (R >= K && R < RH - K && gi < y1)
+      out[(int64_t)(gi - y0 + (BANDED ? in.olo : 0)) * W + gj] = Q4<T>{u[r], ub[r], px[r], py[r]};
   }
 }
 
@@ -135,16 +142,18 @@ k_tv_tile(const Q4<T>* __restrict__ in, const T* __restrict__ f0, Q4<T>* __restr
 // The metric constants of the region are loaded once (M: MetricPackF32
 // recomputes the matrix from the slopes, MetricPackF64 reads it) and stay
 // in registers for the K iterations.
-template <class T, int K, int RPT, int G, int MINB, class M>
+template <class T, int K, int RPT, int G, int MINB, class M, bool BANDED>
 __global__ void __launch_bounds__(32 * G, MINB)
-k_pd_tile(const Q4<T>* __restrict__ in, M m, Q4<T>* __restrict__ out, int H, int W, T tau,
+k_pd_tile(const MarchRows<Q4<T>> in, M m, Q4<T>* __restrict__ out, int H, int W, T tau,
           T sigma, T umin, T umax) {
   constexpr int RH = G * RPT, TIW = 32 - 2 * K, TIH = RH - 2 * K;
   __shared__ T qy_bot[G][32];  // qy of each warp's last row
   __shared__ T v_top[G][32];   // v of each warp's first row
   const int l = threadIdx.x & 31, g = threadIdx.x >> 5;
+  const int y0 = BANDED ? in.y0 : 0, y1 = BANDED ? in.y1 : H;
+  const int rlo = max(y0 - K, 0), rhi = min(y1 + K, H) - 1;
   const int gj = (int)blockIdx.x * TIW - K + l;
-  const int gi0 = (int)blockIdx.y * TIH - K + g * RPT;
+  const int gi0 = y0 + (int)blockIdx.y * TIH - K + g * RPT;
   const int jc = min(max(gj, 0), W - 1);
   pdl_wait_and_release();
   T p1[RPT], p2[RPT], p3[RPT], u[RPT];
@@ -152,13 +161,13 @@ k_pd_tile(const Q4<T>* __restrict__ in, M m, Q4<T>* __restrict__ out, int H, int
   T sg[RPT], beta[RPT], fb[RPT];
 #pragma unroll
   for (int r = 0; r < RPT; ++r) {
-    const int gr = min(max(gi0 + r, 0), H - 1);
-    const Q4<T> q = in[gr * W + jc];
+    const int gr = min(max(gi0 + r, rlo), rhi);
+    const Q4<T> q = in.template at<BANDED>(gr, jc, W);
     p1[r] = q.x;
     p2[r] = q.y;
     p3[r] = q.z;
     u[r] = q.w;
-    m.finish(m.template load<false>(gr, H, jc, W), cf[r], sg[r], beta[r], fb[r]);
+    m.finish(m.template load<BANDED>(gr, y1, jc, W), cf[r], sg[r], beta[r], fb[r]);
   }
 #pragma unroll 1
   for (int it = 0; it < K; ++it) {
@@ -246,7 +255,8 @@ k_pd_tile(const Q4<T>* __restrict__ in, M m, Q4<T>* __restrict__ out, int H, int
 #pragma unroll
   for (int r = 0; r < RPT; ++r) {
     const int R = g * RPT + r, gi = gi0 + r;
-    if (R >= K && R < RH - K && gi < H) out[gi * W + gj] = Q4<T>{p1[r], p2[r], p3[r], u[r]};
+    if (R >= K && R < RH - K && gi < y1)
+      out[(int64_t)(gi - y0 + (BANDED ? in.olo : 0)) * W + gj] = Q4<T>{p1[r], p2[r], p3[r], u[r]};
   }
 }
 
