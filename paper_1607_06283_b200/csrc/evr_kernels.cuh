@@ -396,6 +396,17 @@ __device__ __forceinline__ void pdl_wait_and_release() {
 template <class T> struct alignas(4 * sizeof(T)) Q4 {
   T x, y, z, w;
 };
+// read-only (non-coherent) loads of the packed quads: the iteration kernels
+// read ping-pong set a and write set a ^ 1, so nothing they read is written
+// while they run
+__device__ __forceinline__ Q4<float> ldg(const Q4<float>* p) {
+  const float4 v = __ldg(reinterpret_cast<const float4*>(p));
+  return Q4<float>{v.x, v.y, v.z, v.w};
+}
+// (a 32-byte quad stays one plain 256-bit load)
+__device__ __forceinline__ Q4<double> ldg(const Q4<double>* p) { return *p; }
+__device__ __forceinline__ float ldg(const float* p) { return __ldg(p); }
+__device__ __forceinline__ double ldg(const double* p) { return __ldg(p); }
 
 // Row sources of a march kernel.  A context owns global sensor rows
 // [y0, y1), global row gr living at local row gr - y0 + olo of `own` (E
@@ -412,13 +423,17 @@ template <class Q> struct MarchRows {
   const Q* dn;  // row y1 of the band below (BANDED only; tiles: .. y1 + K - 1)
   int y0, y1, olo, E;
   // element of global row gr (a band's own rows or K rows either side)
-  template <bool BANDED> __device__ __forceinline__ const Q& at(int gr, int jc, int W) const {
+  // own row gr (32-bit offsets; the caller knows gr is in [y0, y1))
+  __device__ __forceinline__ Q at_own(int gr, int jc, int W) const {
+    return ldg(own + ((gr - y0 + olo) * W + jc));
+  }
+  template <bool BANDED> __device__ __forceinline__ Q at(int gr, int jc, int W) const {
     if constexpr (BANDED)
-      return gr < y0   ? up[(int64_t)(gr - y0 + 1) * W + jc]
-             : gr >= y1 ? dn[(int64_t)(gr - y1) * W + jc]
-                        : own[(int64_t)(gr - y0 + olo) * W + jc];
+      return ldg(gr < y0   ? up + ((int64_t)(gr - y0 + 1) * W + jc)
+                 : gr >= y1 ? dn + ((int64_t)(gr - y1) * W + jc)
+                            : own + ((int64_t)(gr - y0 + olo) * W + jc));
     else
-      return own[gr * W + jc];
+      return ldg(own + (gr * W + jc));
   }
 };
 
@@ -514,11 +529,14 @@ struct MetricPackF32 {
   template <bool BANDED>
   __device__ __forceinline__ Raw load(int gr, int y1, int jc, int W) const {
     if constexpr (BANDED)
-      return gr < rows.y0 ? rows.up[(int64_t)(gr - rows.y0 + 1) * W + jc]
-             : gr >= y1   ? rows.dn[(int64_t)(gr - y1) * W + jc]
-                          : c[(int64_t)(gr - rows.y0 + rows.olo) * W + jc];
+      return ldg(gr < rows.y0 ? rows.up + ((int64_t)(gr - rows.y0 + 1) * W + jc)
+                 : gr >= y1   ? rows.dn + ((int64_t)(gr - y1) * W + jc)
+                              : c + ((int64_t)(gr - rows.y0 + rows.olo) * W + jc));
     else
-      return c[gr * W + jc];
+      return ldg(c + (gr * W + jc));
+  }
+  __device__ __forceinline__ Raw load_own(int gr, int y0, int olo, int jc, int W) const {
+    return ldg(c + ((gr - y0 + olo) * W + jc));
   }
   __device__ __forceinline__ void finish(const Raw& r, Coef<float>& cf, float& sg, float& beta,
                                          float& fb) const {
@@ -541,11 +559,15 @@ struct MetricPackF64 {
       const Q4<double>* p = gr < rows.y0 ? rows.up + 2 * ((int64_t)(gr - rows.y0 + 1) * W + jc)
                             : gr >= y1   ? rows.dn + 2 * ((int64_t)(gr - y1) * W + jc)
                                          : c + 2 * ((int64_t)(gr - rows.y0 + rows.olo) * W + jc);
-      return Raw{p[0], p[1]};
+      return Raw{ldg(p), ldg(p + 1)};
     } else {
       const int k = gr * W + jc;
-      return Raw{c[2 * k], c[2 * k + 1]};
+      return Raw{ldg(c + 2 * k), ldg(c + 2 * k + 1)};
     }
+  }
+  __device__ __forceinline__ Raw load_own(int gr, int y0, int olo, int jc, int W) const {
+    const int k = (gr - y0 + olo) * W + jc;
+    return Raw{ldg(c + 2 * k), ldg(c + 2 * k + 1)};
   }
   __device__ __forceinline__ void finish(const Raw& r, Coef<double>& cf, double& sg,
                                          double& beta, double& fb) const {

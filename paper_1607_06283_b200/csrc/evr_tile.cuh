@@ -54,15 +54,17 @@ k_tv_tile(const MarchRows<Q4<T>> in, const MarchRows<T> f0, Q4<T>* __restrict__ 
   const int jc = min(max(gj, 0), W - 1);
   pdl_wait_and_release();
   T u[RPT], ub[RPT], px[RPT], py[RPT], f[RPT];
+  // a band's warps whose rows are all its own skip the neighbour selects
+  const bool inner = !BANDED || (gi0 >= y0 && gi0 + RPT <= y1);
 #pragma unroll
   for (int r = 0; r < RPT; ++r) {
     const int gr = min(max(gi0 + r, rlo), rhi);
-    const Q4<T> q = in.template at<BANDED>(gr, jc, W);
+    const Q4<T> q = inner ? in.at_own(gr, jc, W) : in.template at<BANDED>(gr, jc, W);
     u[r] = q.x;
     ub[r] = q.y;
     px[r] = q.z;
     py[r] = q.w;
-    f[r] = f0.template at<BANDED>(gr, jc, W);
+    f[r] = inner ? f0.at_own(gr, jc, W) : f0.template at<BANDED>(gr, jc, W);
   }
 #pragma unroll 1
   for (int it = 0; it < K; ++it) {
@@ -159,15 +161,17 @@ k_pd_tile(const MarchRows<Q4<T>> in, M m, Q4<T>* __restrict__ out, int H, int W,
   T p1[RPT], p2[RPT], p3[RPT], u[RPT];
   Coef<T> cf[RPT];
   T sg[RPT], beta[RPT], fb[RPT];
+  const bool inner = !BANDED || (gi0 >= y0 && gi0 + RPT <= y1);
 #pragma unroll
   for (int r = 0; r < RPT; ++r) {
     const int gr = min(max(gi0 + r, rlo), rhi);
-    const Q4<T> q = in.template at<BANDED>(gr, jc, W);
+    const Q4<T> q = inner ? in.at_own(gr, jc, W) : in.template at<BANDED>(gr, jc, W);
     p1[r] = q.x;
     p2[r] = q.y;
     p3[r] = q.z;
     u[r] = q.w;
-    m.finish(m.template load<BANDED>(gr, y1, jc, W), cf[r], sg[r], beta[r], fb[r]);
+    m.finish(inner ? m.load_own(gr, in.y0, in.olo, jc, W) : m.template load<BANDED>(gr, y1, jc, W),
+             cf[r], sg[r], beta[r], fb[r]);
   }
 #pragma unroll 1
   for (int it = 0; it < K; ++it) {

@@ -27,3 +27,12 @@ for split in ("0", "1"):
     dt = (time.perf_counter() - t0) / (len(pk) - 4)
     print(f"{cfg} {'f32' if prec else 'f64'} bands={bands} {'split' if split == '1' else 'fused'}: "
           f"{dt * 1e3:.3f} ms/packet (host clock, no frame download)")
+# the whole-sensor context, same host clock (synchronous packet, no frame)
+st = evr.init_state(evr.SensorGeometry(W, H), sc, precision=prec)
+for p in pk[:4]:
+    evr.process_packet_arrays(st, p, mc, sc, evr.Thresholds(), want_frame=False)
+t0 = time.perf_counter()
+for p in pk[4:]:
+    evr.process_packet_arrays(st, p, mc, sc, evr.Thresholds(), want_frame=False)
+dt = (time.perf_counter() - t0) / (len(pk) - 4)
+print(f"{cfg} {'f32' if prec else 'f64'} single context: {dt * 1e3:.3f} ms/packet (host clock, no frame download)")
