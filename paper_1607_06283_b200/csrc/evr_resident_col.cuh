@@ -367,20 +367,50 @@ __global__ void __launch_bounds__(NT, 1) k_resident_col(const ResArgs<T> a) {
   // ------------------------------------------------------------ metric ---
   // compute_metric + coeffs (surface.py:81-90, :199-205), solver constants
   Coef<T> c[NR];
-  T sg[NR], fb[NR];
+  T sg[NR], fb[NR], ysg[NR];
+  T gxs[NR], gys[NR], gs[NR];
+  {
+    bool slow = false;
+#pragma unroll
+    for (int r = 0; r < NR; ++r) {
+      const int gi = r0 - 1 + r;
+      T gx = T(0), gy = T(0);
+      if (a.manifold) {
+        const T tr = XA[r * W + jr];
+        gx = j < W - 1 ? tr - td[r] : T(0);
+        gy = gi < H - 1 ? td[r + 1] - td[r] : T(0);
+      }
+      gxs[r] = gx;
+      gys[r] = gy;
+      gs[r] = metric_G(gx, gy);
+      if constexpr (kFast) {  // shared reciprocal of G, branch-free sqrt
+        c[r] = coeffs_fx(gx, gy, gs[r], slow);
+        sg[r] = fdp_sqrt(gs[r], slow);
+      } else {
+        c[r] = coeffs_of(gx, gy, gs[r]);
+        sg[r] = Arith<T>::sqrt(gs[r]);
+      }
+    }
+    if (kFast && slow) {
+#pragma unroll
+      for (int r = 0; r < NR; ++r) {
+        c[r] = coeffs_of(gxs[r], gys[r], gs[r]);
+        sg[r] = Arith<T>::sqrt(gs[r]);
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < NR; ++r) {
+      if constexpr (kFast)
+        ysg[r] = fdp_recip(sg[r]);  // the dual's divisor, constant over the solve
+      else
+        ysg[r] = T(1);
+    }
+  }
 #pragma unroll
   for (int r = 0; r < NR; ++r) {
-    const int gi = r0 - 1 + r;
-    T gx = T(0), gy = T(0);
-    if (a.manifold) {
-      const T tr = XA[r * W + jr];
-      gx = j < W - 1 ? tr - td[r] : T(0);
-      gy = gi < H - 1 ? td[r + 1] - td[r] : T(0);
-    }
-    const T g = metric_G(gx, gy);
-    const T s = Arith<T>::sqrt(g);
-    c[r] = coeffs_of(gx, gy, g);
-    sg[r] = s;
+    const T gx = gxs[r], gy = gys[r];
+    const T g = gs[r];
+    const T s = sg[r];
     fb[r] = r >= 1 && col && live(r) ? T(4) * (a.tl * s) * (T)F64[r * W + j] : T(0);
     if (r >= 1 && r <= Rb && col) {
       const int64_t gk = gk_of(r);
@@ -480,7 +510,8 @@ __global__ void __launch_bounds__(NT, 1) k_resident_col(const ResArgs<T> a) {
         n2[r] = p2[r];
         n3[r] = p3[r];
         if constexpr (kFast) {
-          nn[r] = dual_pre_fx(c[r], a.sigma, gx[r], gy[r], sg[r], n1[r], n2[r], n3[r], slow);
+          nn[r] = dual_pre_fx_r(c[r], a.sigma, gx[r], gy[r], sg[r], ysg[r], n1[r], n2[r], n3[r],
+                                slow);
           proj |= nn[r] != T(1);
         } else {
           dual_step(c[r], a.sigma, gx[r], gy[r], sg[r], n1[r], n2[r], n3[r]);
