@@ -16,10 +16,19 @@ import sys
 _SAVED = {}
 
 
-def install(evrecon_pipeline=None):
-    """Patch evrecon.pipeline.{init_state, process_packet} (and the module's
-    primal_dual_solve binding) with this package's versions.  The reference
-    config dataclasses are duck-type compatible (same fields)."""
+def _patch(mod, name, repl):
+    _SAVED.setdefault((id(mod), name), (mod, getattr(mod, name)))
+    setattr(mod, name, repl)
+
+
+def install(evrecon_pipeline=None, evrecon_cli=None):
+    """Patch evrecon.pipeline.{init_state, process_packet, run_stream} (and
+    the module's primal_dual_solve binding) with this package's versions,
+    and evrecon.cli's import-time run_stream binding (cli.py:18) when the
+    CLI module is loaded, so `evrecon reconstruct` / `evrecon bench` stream
+    through the pipelined run_stream (packet k+1 computes while frame k is
+    read back).  The reference config dataclasses and Event objects are
+    duck-type compatible (same fields)."""
     from . import pipeline as ours
     from . import solve as ours_solve
 
@@ -27,9 +36,13 @@ def install(evrecon_pipeline=None):
     if mod is None:
         import evrecon.pipeline as mod  # noqa: F811
     for name, repl in (("init_state", ours.init_state), ("process_packet", ours.process_packet),
-                       ("primal_dual_solve", ours_solve.primal_dual_solve)):
-        _SAVED.setdefault((id(mod), name), (mod, getattr(mod, name)))
-        setattr(mod, name, repl)
+                       ("primal_dual_solve", ours_solve.primal_dual_solve),
+                       ("run_stream", ours.run_stream)):
+        if hasattr(mod, name):
+            _patch(mod, name, repl)
+    cli = evrecon_cli or sys.modules.get("evrecon.cli")
+    if cli is not None and hasattr(cli, "run_stream"):
+        _patch(cli, "run_stream", ours.run_stream)
     return mod
 
 

@@ -210,14 +210,17 @@ def test_install_reroutes_reference_stream():
     import types
 
     fake = types.ModuleType("evrecon.pipeline")
-    fake.init_state = fake.process_packet = fake.primal_dual_solve = None
-    evr.install(fake)
+    fake.init_state = fake.process_packet = fake.primal_dual_solve = fake.run_stream = None
+    cli = types.ModuleType("evrecon.cli")
+    cli.run_stream = None
+    evr.install(fake, cli)
     try:
         assert fake.process_packet is evr.process_packet
         assert fake.init_state is evr.init_state
+        assert fake.run_stream is evr.run_stream and cli.run_stream is evr.run_stream
     finally:
         evr.uninstall()
-    assert fake.process_packet is None
+    assert fake.process_packet is None and cli.run_stream is None
 
 
 def test_engine_detail_names_the_kernel():
