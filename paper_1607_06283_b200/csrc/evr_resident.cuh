@@ -65,6 +65,7 @@ template <class T> struct ResArgs {
   evr_solve_info* info;
   int* err;
   unsigned long long* trace;     // optional [nb][256] phase timestamps (ns)
+  const int* perm;               // k_resident_col: band of CTA blockIdx.x (null = identity)
   int H, W, nb, R;
   int tv_iters, pd_iters, manifold;
   double t_scale, c_pos, c_neg, u_min, u_max;

@@ -93,7 +93,7 @@ __global__ void __launch_bounds__(NT, 1) k_resident_col(const ResArgs<T> a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ double red[64];
   const int tid = threadIdx.x;
-  const int b = blockIdx.x;
+  const int b = a.perm ? a.perm[blockIdx.x] : (int)blockIdx.x;  // this CTA's band
   const int H = a.H, W = a.W;
   const int r0 = b * RB;  // first own row; local row r is global row r0 - 1 + r
   const int Rb = min(RB, H - r0);
@@ -141,6 +141,11 @@ __global__ void __launch_bounds__(NT, 1) k_resident_col(const ResArgs<T> a) {
     }
   };
   mark();
+  if (tracing) {  // the SM this band runs on (slot 255 of the timeline)
+    unsigned smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    a.trace[(size_t)b * 256 + 255] = smid;
+  }
 
   // boundary values of local row r (1 = first own row -> the band above,
   // Rb = last own row -> the band below) as tagged words: nv = 1 (u_bar) or

@@ -63,3 +63,12 @@ W8 = np.concatenate([e[1] for e in eff])
 S = np.concatenate([e[2] for e in eff])
 print(f"handoff after the later neighbour's put: median {np.median(L):.2f} us (p10 {np.percentile(L, 10):.2f}, p90 {np.percentile(L, 90):.2f}); "
       f"own wait {np.median(W8):.2f} us; neighbour lag behind own put {np.median(S):.2f} us")
+
+# per CTA: the SM it ran on (slot 255) and its mean halo fetch per iteration
+print("CTA smid TV/it PDfetch PD/it")
+for r in rows:
+    a = (tr[r] - t0)[k + 2:k + 2 + 4 * pd].reshape(pd, 4) / 1e3
+    m = (tr[r] - t0) / 1e3
+    tvd = np.diff(m[1:2 + tv]).mean()
+    fetch = (a[1:, 0] - a[:-1, 3]).mean()
+    print(f"{r:3d} {int(buf.reshape(-1, 256)[r, 255]):3d} {tvd:.2f} {fetch:.2f} {np.diff(a[:, 0]).mean():.2f}")
