@@ -24,7 +24,7 @@ def packets(H, W, n_packets, epp, seed, t_step=1):
 @pytest.mark.parametrize("H,W,bands,prec", [(64, 48, 1, 0), (64, 48, 2, 0), (37, 29, 4, 0),
                                             (5, 17, 5, 0), (130, 96, 3, 0), (64, 48, 3, 1),
                                             (23, 70, 6, 0), (90, 64, 2, 1), (300, 200, 3, 0),
-                                            (301, 150, 4, 1)])
+                                            (301, 150, 4, 1), (2048, 2048, 4, 0)])
 def test_banded_equals_single_context(H, W, bands, prec, split, monkeypatch):
     """Fused bands (the iteration kernels read the neighbours' halo rows in
     place) and split bands (half-step kernels + halo row copies) are both

@@ -382,3 +382,30 @@ def test_tgv_and_l1_solvers_bit_exact_vs_oracle(data):
         evr.tgv_manifold_solve(f, m, 1.0, alpha0=0.0)
     with pytest.raises(ValueError, match="data term"):
         evr.tgv_manifold_solve(f, m, 1.0, data="huber")
+
+
+@pytest.mark.parametrize("cfg", ["C4", "C3", "C5"])
+def test_baseline_sizes_streaming_vs_oracle(cfg):
+    """BASELINE configs at their full sizes on the streaming engine (tile
+    kernels, 4 iterations per launch): 640x480 (2 chained packets), 1280x720
+    at 100 primal-dual iterations and 2048x2048 (1 packet each), generator U
+    at 1 Mev/s, 1000-event packets: float64 bit-exact with the C oracle, and
+    the float32 engine within the north-star 1e-4 on log u."""
+    H, W, pd, n = {"C4": (480, 640, 50, 2), "C3": (720, 1280, 100, 1),
+                   "C5": (2048, 2048, 50, 1)}[cfg]
+    sc = evr.SolverConfig(max_iterations=pd)
+    mc = evr.ManifoldConfig()
+    pks = uniform_packets(H, W, n, 1000, seed=H + W + pd, t_step=1)
+    st = evr.init_state(evr.SensorGeometry(W, H), sc, precision=0, engine=1)
+    s32 = evr.init_state(evr.SensorGeometry(W, H), sc, precision=1, engine=1)
+    ref = O.OracleStream(H, W, O.make_config(max_iterations=pd))
+    for pk in pks:
+        _, frame, res = evr.process_packet(st, pk, mc, sc, evr.Thresholds())
+        _, f32, _ = evr.process_packet(s32, pk, mc, sc, evr.Thresholds())
+        it, rel = ref.process(np.ascontiguousarray(pk))
+        assert res.iterations == it == pd
+        assert np.array_equal(frame, ref.u)
+        assert res.rel_change == pytest.approx(rel, rel=1e-9)
+        assert np.abs(np.log(f32) - np.log(ref.u)).max() <= LOG_TOL
+    assert np.array_equal(st.p, ref.p) and np.array_equal(st.f, ref.f)
+    assert "k_pd_tile" in st.context().engine_detail()
