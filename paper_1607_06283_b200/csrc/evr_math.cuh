@@ -151,6 +151,14 @@ __device__ __forceinline__ void dual_step(const Coef<T>& c, T sigma, T gx, T gy,
   const T q2 = Arith<T>::mad(s22, gy, Arith<T>::mad(s12, gx, p2));
   const T q3 = Arith<T>::mad(s32, gy, Arith<T>::mad(s31, gx, p3));
   T n = Arith<T>::sqrt(Arith<T>::mad(q3, q3, Arith<T>::mad(q2, q2, q1 * q1)));
+  if constexpr (sizeof(T) == 4) {
+    // binary32: a * rcp(b) unconditionally (no selects; rcp(1) == 1)
+    n = vmax(Arith<T>::div(n, sqrtG), T(1));
+    p1 = Arith<T>::div(q1, n);
+    p2 = Arith<T>::div(q2, n);
+    p3 = Arith<T>::div(q3, n);
+    return;
+  }
   if (sqrtG != T(1)) n = Arith<T>::div(n, sqrtG);  // x / 1 == x exactly
   n = vmax(n, T(1));
   if (n != T(1)) {  // interior point: p / 1 == p exactly
@@ -170,6 +178,11 @@ __device__ __forceinline__ void tv_dual_step(T dx, T dy, T sigma, T& px, T& py) 
   const T a = Arith<T>::mad(dx, sigma, px);
   const T b = Arith<T>::mad(dy, sigma, py);
   const T n = vmax(Arith<T>::sqrt(Arith<T>::mad(b, b, a * a)), T(1));
+  if constexpr (sizeof(T) == 4) {  // binary32: unconditional a * rcp(n)
+    px = Arith<T>::div(a, n);
+    py = Arith<T>::div(b, n);
+    return;
+  }
   if (n != T(1)) {
     px = Arith<T>::div(a, n);
     py = Arith<T>::div(b, n);
