@@ -101,6 +101,14 @@ __device__ __forceinline__ MetricPx metric_px(float tx, float ty) {
 template <class T>
 __device__ __forceinline__ T div_at(T qx_c, T qx_l, T qy_c, T qy_u, int i, int j,
                                     int H, int W) {
+  if constexpr (sizeof(T) == 4) {
+    // binary32 (callers pass qx_l = 0 on the first column, qy_u = 0 on the
+    // first row): one select per axis; the last-column / last-row forms
+    // 0 - qx_l, 0 - qy_u equal -qx_l, -qy_u up to the sign of a zero, which
+    // never reaches u (t1 = d * tau + u)
+    const T d = (j < W - 1 ? qx_c : T(0)) - qx_l;
+    return d + ((i < H - 1 ? qy_c : T(0)) - qy_u);
+  }
   T d;
   if (j == 0)
     d = qx_c;
