@@ -161,6 +161,7 @@ k_pd_tile(const MarchRows<Q4<T>> in, M m, Q4<T>* __restrict__ out, int H, int W,
   T p1[RPT], p2[RPT], p3[RPT], u[RPT];
   Coef<T> cf[RPT];
   T sg[RPT], beta[RPT], fb[RPT];
+  T ysg[sizeof(T) == 8 ? RPT : 1];  // float64: refined 1 / sqrtG, hoisted
   const bool inner = !BANDED || (gi0 >= y0 && gi0 + RPT <= y1);
 #pragma unroll
   for (int r = 0; r < RPT; ++r) {
@@ -172,6 +173,7 @@ k_pd_tile(const MarchRows<Q4<T>> in, M m, Q4<T>* __restrict__ out, int H, int W,
     u[r] = q.w;
     m.finish(inner ? m.load_own(gr, in.y0, in.olo, jc, W) : m.template load<BANDED>(gr, y1, jc, W),
              cf[r], sg[r], beta[r], fb[r]);
+    if constexpr (sizeof(T) == 8) ysg[r] = fdp_recip(sg[r]);
   }
 #pragma unroll 1
   for (int it = 0; it < K; ++it) {
@@ -221,7 +223,8 @@ k_pd_tile(const MarchRows<Q4<T>> in, M m, Q4<T>* __restrict__ out, int H, int W,
         n1[r] = p1[r];
         n2[r] = p2[r];
         n3[r] = p3[r];
-        nn[r] = dual_pre_fx(cf[r], sigma, gx[r], gy[r], sg[r], n1[r], n2[r], n3[r], slow);
+        nn[r] = dual_pre_fx_r(cf[r], sigma, gx[r], gy[r], sg[r], ysg[r], n1[r], n2[r], n3[r],
+                              slow);
         proj |= nn[r] != T(1);
       }
       if (__any_sync(0xffffffffu, proj)) {
