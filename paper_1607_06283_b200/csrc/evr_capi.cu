@@ -258,15 +258,19 @@ std::vector<Step> packet_steps(const evr_config& g, int which, bool fused, int t
 // Measured on B200 (tools/tilerun.sh, tools/f64run.sh), K = 4: float32 C3
 // 0.94 -> 0.72 ms, C4 0.38 -> 0.23, C5 3.2 -> 1.9; float64 C3 2.84 -> 2.27,
 // C4 0.66 -> 0.57.
-int tile_k(int prec) {
+int env_tile_k() {
   static const int env = [] {
     const char* e = getenv("EVR_TILE_K");
     if (!e) return 0;
     const int v = atoi(e);
     return v >= 1 && v <= 4 ? v : 1;
   }();
-  if (env) return env;
-  return 4;
+  return env;
+}
+bool env_tile_k_set() { return env_tile_k() > 0; }
+int tile_k(int prec) {
+  (void)prec;
+  return env_tile_k() ? env_tile_k() : 4;
 }
 
 // fused iterations: rows per warp strip (RY), rows of loads in flight ahead
@@ -394,20 +398,45 @@ int sm_count(int device) {
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
   return sms;
 }
-template <class T> int tile_rpt(const evr_ctx* c, int K) {
+// whole waves x region rows of one launch shape (the model both choices use)
+template <class T> int64_t tile_cost(const evr_ctx* c, int K, int rpt) {
   constexpr int G = TileShape<T>::G;
-  if (!std::is_same<T, float>::value || TileShape<T>::RPT != 8) return TileShape<T>::RPT;
   const int64_t slots = (int64_t)sm_count(c->device) * TileShape<T>::MINB;
+  const int tiw = 32 - 2 * K, tih = G * rpt - 2 * K;
+  const int64_t ctas = (int64_t)((c->W + tiw - 1) / tiw) * ((c->own_hi - c->own_lo + tih) / tih);
+  return (ctas + slots - 1) / slots * (G * rpt);
+}
+template <class T> int tile_rpt(const evr_ctx* c, int K) {
+  if (!std::is_same<T, float>::value || TileShape<T>::RPT != 8) return TileShape<T>::RPT;
   int best = 8;
   int64_t best_cost = -1;
   for (int rpt = 8; rpt >= 6; --rpt) {
-    const int tiw = 32 - 2 * K, tih = G * rpt - 2 * K;
-    const int64_t ctas =
-        (int64_t)((c->W + tiw - 1) / tiw) * ((c->own_hi - c->own_lo + tih) / tih);
-    const int64_t cost = (ctas + slots - 1) / slots * (G * rpt);
+    const int64_t cost = tile_cost<T>(c, K, rpt);
     if (best_cost < 0 || cost < best_cost) best = rpt, best_cost = cost;
   }
   return best;
+}
+// Iterations per tile launch when neither EVR_TILE_K nor evr_set_tile_k
+// fixes it: a launch of K iterations costs K x its waves, so the time per
+// iteration goes with the waves of the K's best shape; ties go to the larger
+// K (fewer HBM round trips).  Measured float64: 1280x720 K=3 1.82 ms vs K=4
+// 1.86 (4.7 vs 5.5 waves), 2048^2 4.71 vs 4.92, 640x480 K=4 0.455 vs 0.481.
+template <class T> int auto_tile_k(const evr_ctx* c) {
+  int best = 4;
+  int64_t best_cost = -1;
+  for (int K = 4; K >= 3; --K) {
+    const int64_t cost = tile_cost<T>(c, K, tile_rpt<T>(c, K));
+    if (best_cost < 0 || cost < best_cost) best = K, best_cost = cost;
+  }
+  return best;
+}
+int ctx_tile_k(const evr_ctx* c) {
+  if (c->tile_k > 0) return c->tile_k;
+  if (env_tile_k_set()) return env_tile_k();
+  // float32 tiles are cheap enough per iteration that the 1/K share of
+  // memory traffic decides: K = 4 measured best on C3-C5 (2048^2: 1.59 ms vs
+  // 1.64 at K = 3 although K = 3 needs fewer waves)
+  return c->prec == EVR_PREC_F64 ? auto_tile_k<double>(c) : 4;
 }
 template <class T, int K, int RPT> dim3 tile_grid(const evr_ctx* c) {
   constexpr int TIW = 32 - 2 * K, TIH = TileShape<T>::G * RPT - 2 * K;
@@ -634,7 +663,7 @@ template <class T> int launch_step(evr_ctx* ctx, const Step& st) {
 
 template <class T> int enqueue_packet(evr_ctx* ctx, int which) {
   int n = 0;
-  const int tk = ctx->banded ? 1 : ctx->tile_k > 0 ? ctx->tile_k : tile_k(ctx->prec);
+  const int tk = ctx->banded ? 1 : ctx_tile_k(ctx);
   for (const Step& st : packet_steps(ctx->cfg, which, !ctx->banded, tk))
     n += launch_step<T>(ctx, st);
   int rc = launch_err(ctx, "packet");
@@ -1392,7 +1421,7 @@ int evr_engine_detail(evr_ctx* ctx, char* buf, int len) {
       snprintf(buf, len, "streaming split half-steps (band rows %d..%d of %d)", ctx->row0,
                ctx->row0 + ctx->H - 1, ctx->Htot);
     else {
-      const int tk = ctx->tile_k > 0 ? ctx->tile_k : tile_k(ctx->prec);
+      const int tk = ctx_tile_k(ctx);
       if (tk > 1) {
         const bool d = ctx->prec == EVR_PREC_F64;
         const int rpt = d ? tile_rpt<double>(ctx, tk) : tile_rpt<float>(ctx, tk);
