@@ -28,6 +28,8 @@
 // to the one-iteration-per-launch kernels.
 #pragma once
 
+#include <type_traits>
+
 #include "evr_fastdp.cuh"
 #include "evr_kernels.cuh"
 
@@ -56,16 +58,28 @@ k_tv_tile(const MarchRows<Q4<T>> in, const MarchRows<T> f0, Q4<T>* __restrict__ 
   T u[RPT], ub[RPT], px[RPT], py[RPT], f[RPT];
   // a band's warps whose rows are all its own skip the neighbour selects
   const bool inner = !BANDED || (gi0 >= y0 && gi0 + RPT <= y1);
+  auto load = [&](auto banded) {
 #pragma unroll
-  for (int r = 0; r < RPT; ++r) {
-    const int gr = min(max(gi0 + r, rlo), rhi);
-    const Q4<T> q = inner ? in.at_own(gr, jc, W) : in.template at<BANDED>(gr, jc, W);
-    u[r] = q.x;
-    ub[r] = q.y;
-    px[r] = q.z;
-    py[r] = q.w;
-    f[r] = inner ? f0.at_own(gr, jc, W) : f0.template at<BANDED>(gr, jc, W);
-  }
+    for (int r = 0; r < RPT; ++r) {
+      const int gr = min(max(gi0 + r, rlo), rhi);
+      Q4<T> q;
+      if constexpr (decltype(banded)::value) {
+        q = in.template at<true>(gr, jc, W);
+        f[r] = f0.template at<true>(gr, jc, W);
+      } else {
+        q = in.at_own(gr, jc, W);
+        f[r] = f0.at_own(gr, jc, W);
+      }
+      u[r] = q.x;
+      ub[r] = q.y;
+      px[r] = q.z;
+      py[r] = q.w;
+    }
+  };
+  if (inner)  // warp-uniform: a band's warps away from its edges skip the selects
+    load(std::false_type{});
+  else if constexpr (BANDED)
+    load(std::true_type{});
 #pragma unroll 1
   for (int it = 0; it < K; ++it) {
     ub_top[g][l] = ub[0];
@@ -163,18 +177,31 @@ k_pd_tile(const MarchRows<Q4<T>> in, M m, Q4<T>* __restrict__ out, int H, int W,
   T sg[RPT], beta[RPT], fb[RPT];
   T ysg[sizeof(T) == 8 ? RPT : 1];  // float64: refined 1 / sqrtG, hoisted
   const bool inner = !BANDED || (gi0 >= y0 && gi0 + RPT <= y1);
+  auto load = [&](auto banded) {
 #pragma unroll
-  for (int r = 0; r < RPT; ++r) {
-    const int gr = min(max(gi0 + r, rlo), rhi);
-    const Q4<T> q = inner ? in.at_own(gr, jc, W) : in.template at<BANDED>(gr, jc, W);
-    p1[r] = q.x;
-    p2[r] = q.y;
-    p3[r] = q.z;
-    u[r] = q.w;
-    m.finish(inner ? m.load_own(gr, in.y0, in.olo, jc, W) : m.template load<BANDED>(gr, y1, jc, W),
-             cf[r], sg[r], beta[r], fb[r]);
-    if constexpr (sizeof(T) == 8) ysg[r] = fdp_recip(sg[r]);
-  }
+    for (int r = 0; r < RPT; ++r) {
+      const int gr = min(max(gi0 + r, rlo), rhi);
+      Q4<T> q;
+      typename M::Raw c;
+      if constexpr (decltype(banded)::value) {
+        q = in.template at<true>(gr, jc, W);
+        c = m.template load<true>(gr, y1, jc, W);
+      } else {
+        q = in.at_own(gr, jc, W);
+        c = m.load_own(gr, in.y0, in.olo, jc, W);
+      }
+      p1[r] = q.x;
+      p2[r] = q.y;
+      p3[r] = q.z;
+      u[r] = q.w;
+      m.finish(c, cf[r], sg[r], beta[r], fb[r]);
+      if constexpr (sizeof(T) == 8) ysg[r] = fdp_recip(sg[r]);
+    }
+  };
+  if (inner)  // warp-uniform: a band's warps away from its edges skip the selects
+    load(std::false_type{});
+  else if constexpr (BANDED)
+    load(std::true_type{});
 #pragma unroll 1
   for (int it = 0; it < K; ++it) {
     T qx[RPT], qy[RPT], v[RPT];
