@@ -80,70 +80,91 @@ k_tv_tile(const MarchRows<Q4<T>> in, const MarchRows<T> f0, Q4<T>* __restrict__ 
     load(std::false_type{});
   else if constexpr (BANDED)
     load(std::true_type{});
+  // CTA-uniform: a tile whose whole region lies inside the sensor, one pixel
+  // away from its edges, runs the iterations without boundary tests (the
+  // reference's interior branch at every pixel, div_at's last else: same
+  // operations, same bits)
+  const int ry0 = gi0 - g * RPT, rx0 = (int)blockIdx.x * TIW - K;
+  const bool interior = ry0 >= 1 && ry0 + RH <= H - 1 && rx0 >= 1 && rx0 + 32 <= W - 1;
+  auto iterate = [&](auto interior_c) {
+    constexpr bool IN = decltype(interior_c)::value;
+    const bool XR = IN || gj < W - 1;
+    auto YD = [&](int gi) { return IN || gi < H - 1; };
+    auto DIV = [&](T xc, T xl, T yc, T yu, int gi) {
+      if constexpr (IN) return (xc - xl) + (yc - yu);
+      else return div_at(xc, gj > 0 ? xl : T(0), yc, gi > 0 ? yu : T(0), gi, gj, H, W);
+    };
 #pragma unroll 1
-  for (int it = 0; it < K; ++it) {
-    ub_top[g][l] = ub[0];
-    __syncthreads();
-    const T ub_below = ub_top[g < G - 1 ? g + 1 : g][l];
-    if constexpr (sizeof(T) == 8) {
-      // float64: branch-free fast div / sqrt so the rows' latency chains
-      // overlap (evr_fastdp.cuh; rare out-of-range rows redone with IEEE)
-      T dx[RPT], dy[RPT], nx[RPT], ny[RPT], nn[RPT];
-      bool slow = false, proj = false;
-#pragma unroll
-      for (int r = 0; r < RPT; ++r) {  // dual (surface.py:168-183)
-        const int gi = gi0 + r;
-        const T ub_r = __shfl_down_sync(0xffffffffu, ub[r], 1);
-        const T ub_n = r < RPT - 1 ? ub[r + 1] : ub_below;
-        dx[r] = gj < W - 1 ? ub_r - ub[r] : T(0);
-        dy[r] = gi < H - 1 ? ub_n - ub[r] : T(0);
-        nx[r] = px[r];
-        ny[r] = py[r];
-        nn[r] = tv_dual_pre_fx(dx[r], dy[r], sigma, nx[r], ny[r], slow);
-        proj |= nn[r] != T(1);
-      }
-      if (__any_sync(0xffffffffu, proj)) {
-#pragma unroll
-        for (int r = 0; r < RPT; ++r) fdp_div2(nx[r], ny[r], nn[r], slow);
-      }
-      if (slow) {
-#pragma unroll
-        for (int r = 0; r < RPT; ++r) {
+    for (int it = 0; it < K; ++it) {
+      ub_top[g][l] = ub[0];
+      __syncthreads();
+      const T ub_below = ub_top[g < G - 1 ? g + 1 : g][l];
+      if constexpr (sizeof(T) == 8) {
+        // float64: branch-free fast div / sqrt so the rows' latency chains
+        // overlap (evr_fastdp.cuh; rare out-of-range rows redone with IEEE)
+        T dx[RPT], dy[RPT], nx[RPT], ny[RPT], nn[RPT];
+        bool slow = false, proj = false;
+  #pragma unroll
+        for (int r = 0; r < RPT; ++r) {  // dual (surface.py:168-183)
+          const int gi = gi0 + r;
+          const T ub_r = __shfl_down_sync(0xffffffffu, ub[r], 1);
+          const T ub_n = r < RPT - 1 ? ub[r + 1] : ub_below;
+          dx[r] = XR ? ub_r - ub[r] : T(0);
+          dy[r] = YD(gi) ? ub_n - ub[r] : T(0);
           nx[r] = px[r];
           ny[r] = py[r];
-          tv_dual_step(dx[r], dy[r], sigma, nx[r], ny[r]);
+          nn[r] = tv_dual_pre_fx(dx[r], dy[r], sigma, nx[r], ny[r], slow);
+          proj |= nn[r] != T(1);
+        }
+        if (__any_sync(0xffffffffu, proj)) {
+  #pragma unroll
+          for (int r = 0; r < RPT; ++r) fdp_div2(nx[r], ny[r], nn[r], slow);
+        }
+        if (slow) {
+  #pragma unroll
+          for (int r = 0; r < RPT; ++r) {
+            nx[r] = px[r];
+            ny[r] = py[r];
+            tv_dual_step(dx[r], dy[r], sigma, nx[r], ny[r]);
+          }
+        }
+  #pragma unroll
+        for (int r = 0; r < RPT; ++r) {
+          px[r] = nx[r];
+          py[r] = ny[r];
+        }
+      } else {
+  #pragma unroll
+        for (int r = 0; r < RPT; ++r) {  // dual (surface.py:168-183)
+          const int gi = gi0 + r;
+          const T ub_r = __shfl_down_sync(0xffffffffu, ub[r], 1);
+          const T ub_n = r < RPT - 1 ? ub[r + 1] : ub_below;
+          const T dx = XR ? ub_r - ub[r] : T(0);
+          const T dy = YD(gi) ? ub_n - ub[r] : T(0);
+          tv_dual_step(dx, dy, sigma, px[r], py[r]);
         }
       }
-#pragma unroll
-      for (int r = 0; r < RPT; ++r) {
-        px[r] = nx[r];
-        py[r] = ny[r];
-      }
-    } else {
-#pragma unroll
-      for (int r = 0; r < RPT; ++r) {  // dual (surface.py:168-183)
+      py_bot[g][l] = py[RPT - 1];
+      __syncthreads();
+      const T py_above = py_bot[g > 0 ? g - 1 : g][l];
+  #pragma unroll
+      for (int r = 0; r < RPT; ++r) {  // primal (surface.py:185-193)
         const int gi = gi0 + r;
-        const T ub_r = __shfl_down_sync(0xffffffffu, ub[r], 1);
-        const T ub_n = r < RPT - 1 ? ub[r + 1] : ub_below;
-        const T dx = gj < W - 1 ? ub_r - ub[r] : T(0);
-        const T dy = gi < H - 1 ? ub_n - ub[r] : T(0);
-        tv_dual_step(dx, dy, sigma, px[r], py[r]);
+        const T pxl = __shfl_up_sync(0xffffffffu, px[r], 1);
+        const T pyu = r > 0 ? py[r - 1] : py_above;
+        const T d = DIV(px[r], pxl, py[r], pyu, gi);
+        T ubar;
+        u[r] = tv_primal_step(d, u[r], f[r], tau, shrink, ubar);
+        ub[r] = ubar;
       }
     }
-    py_bot[g][l] = py[RPT - 1];
-    __syncthreads();
-    const T py_above = py_bot[g > 0 ? g - 1 : g][l];
-#pragma unroll
-    for (int r = 0; r < RPT; ++r) {  // primal (surface.py:185-193)
-      const int gi = gi0 + r;
-      const T pxl = __shfl_up_sync(0xffffffffu, px[r], 1);
-      const T pyu = r > 0 ? py[r - 1] : py_above;
-      const T d = div_at(px[r], gj > 0 ? pxl : T(0), py[r], gi > 0 ? pyu : T(0), gi, gj, H, W);
-      T ubar;
-      u[r] = tv_primal_step(d, u[r], f[r], tau, shrink, ubar);
-      ub[r] = ubar;
-    }
-  }
+  };
+  // float64 only: the float32 boundary form is already two selects, and the
+  // second instance measured slower there (C3 f32 0.614 -> 0.620 ms)
+  if (sizeof(T) == 8 && interior)
+    iterate(std::true_type{});
+  else
+    iterate(std::false_type{});
   if (l < K || l >= 32 - K || gj >= W) return;
 #pragma unroll
   for (int r = 0; r < RPT; ++r) {
@@ -202,89 +223,106 @@ k_pd_tile(const MarchRows<Q4<T>> in, M m, Q4<T>* __restrict__ out, int H, int W,
     load(std::false_type{});
   else if constexpr (BANDED)
     load(std::true_type{});
+  const int ry0 = gi0 - g * RPT, rx0 = (int)blockIdx.x * TIW - K;
+  const bool interior = ry0 >= 1 && ry0 + RH <= H - 1 && rx0 >= 1 && rx0 + 32 <= W - 1;
+  auto iterate = [&](auto interior_c) {
+    constexpr bool IN = decltype(interior_c)::value;
+    const bool XR = IN || gj < W - 1;
+    auto YD = [&](int gi) { return IN || gi < H - 1; };
+    auto DIV = [&](T xc, T xl, T yc, T yu, int gi) {
+      if constexpr (IN) return (xc - xl) + (yc - yu);
+      else return div_at(xc, gj > 0 ? xl : T(0), yc, gi > 0 ? yu : T(0), gi, gj, H, W);
+    };
 #pragma unroll 1
-  for (int it = 0; it < K; ++it) {
-    T qx[RPT], qy[RPT], v[RPT];
-#pragma unroll
-    for (int r = 0; r < RPT; ++r) q_of(cf[r], p1[r], p2[r], p3[r], qx[r], qy[r]);
-    qy_bot[g][l] = qy[RPT - 1];
-    __syncthreads();
-    const T qy_above = qy_bot[g > 0 ? g - 1 : g][l];
-    {
-      T d[RPT], nu[RPT];
-      bool slow = false;
-#pragma unroll
-      for (int r = 0; r < RPT; ++r) {  // primal (solve.py:233-245)
-        const int gi = gi0 + r;
-        const T qxl = __shfl_up_sync(0xffffffffu, qx[r], 1);
-        const T qyu = r > 0 ? qy[r - 1] : qy_above;
-        d[r] = div_at(qx[r], gj > 0 ? qxl : T(0), qy[r], gi > 0 ? qyu : T(0), gi, gj, H, W);
-        if constexpr (sizeof(T) == 8)
-          nu[r] = kl_primal_fx(d[r], u[r], beta[r], fb[r], tau, umin, umax, slow);
-        else
-          nu[r] = kl_primal(d[r], u[r], beta[r], fb[r], tau, umin, umax);
-      }
-      if (sizeof(T) == 8 && slow) {
-#pragma unroll
-        for (int r = 0; r < RPT; ++r) nu[r] = kl_primal(d[r], u[r], beta[r], fb[r], tau, umin, umax);
-      }
-#pragma unroll
-      for (int r = 0; r < RPT; ++r) {
-        v[r] = Arith<T>::mad(nu[r], T(2), -u[r]);
-        u[r] = nu[r];
-      }
-    }
-    v_top[g][l] = v[0];
-    __syncthreads();
-    const T v_below = v_top[g < G - 1 ? g + 1 : g][l];
-    if constexpr (sizeof(T) == 8) {
-      T gx[RPT], gy[RPT], n1[RPT], n2[RPT], n3[RPT], nn[RPT];
-      bool slow = false, proj = false;
-#pragma unroll
-      for (int r = 0; r < RPT; ++r) {  // dual (solve.py:246-252)
-        const int gi = gi0 + r;
-        const T vr = __shfl_down_sync(0xffffffffu, v[r], 1);
-        const T vd = r < RPT - 1 ? v[r + 1] : v_below;
-        gx[r] = gj < W - 1 ? vr - v[r] : T(0);
-        gy[r] = gi < H - 1 ? vd - v[r] : T(0);
-        n1[r] = p1[r];
-        n2[r] = p2[r];
-        n3[r] = p3[r];
-        nn[r] = dual_pre_fx_r(cf[r], sigma, gx[r], gy[r], sg[r], ysg[r], n1[r], n2[r], n3[r],
-                              slow);
-        proj |= nn[r] != T(1);
-      }
-      if (__any_sync(0xffffffffu, proj)) {
-#pragma unroll
-        for (int r = 0; r < RPT; ++r) fdp_div3(n1[r], n2[r], n3[r], nn[r], slow);
-      }
-      if (slow) {
-#pragma unroll
+    for (int it = 0; it < K; ++it) {
+      T qx[RPT], qy[RPT], v[RPT];
+  #pragma unroll
+      for (int r = 0; r < RPT; ++r) q_of(cf[r], p1[r], p2[r], p3[r], qx[r], qy[r]);
+      qy_bot[g][l] = qy[RPT - 1];
+      __syncthreads();
+      const T qy_above = qy_bot[g > 0 ? g - 1 : g][l];
+      {
+        T d[RPT], nu[RPT];
+        bool slow = false;
+  #pragma unroll
+        for (int r = 0; r < RPT; ++r) {  // primal (solve.py:233-245)
+          const int gi = gi0 + r;
+          const T qxl = __shfl_up_sync(0xffffffffu, qx[r], 1);
+          const T qyu = r > 0 ? qy[r - 1] : qy_above;
+          d[r] = DIV(qx[r], qxl, qy[r], qyu, gi);
+          if constexpr (sizeof(T) == 8)
+            nu[r] = kl_primal_fx(d[r], u[r], beta[r], fb[r], tau, umin, umax, slow);
+          else
+            nu[r] = kl_primal(d[r], u[r], beta[r], fb[r], tau, umin, umax);
+        }
+        if (sizeof(T) == 8 && slow) {
+  #pragma unroll
+          for (int r = 0; r < RPT; ++r) nu[r] = kl_primal(d[r], u[r], beta[r], fb[r], tau, umin, umax);
+        }
+  #pragma unroll
         for (int r = 0; r < RPT; ++r) {
+          v[r] = Arith<T>::mad(nu[r], T(2), -u[r]);
+          u[r] = nu[r];
+        }
+      }
+      v_top[g][l] = v[0];
+      __syncthreads();
+      const T v_below = v_top[g < G - 1 ? g + 1 : g][l];
+      if constexpr (sizeof(T) == 8) {
+        T gx[RPT], gy[RPT], n1[RPT], n2[RPT], n3[RPT], nn[RPT];
+        bool slow = false, proj = false;
+  #pragma unroll
+        for (int r = 0; r < RPT; ++r) {  // dual (solve.py:246-252)
+          const int gi = gi0 + r;
+          const T vr = __shfl_down_sync(0xffffffffu, v[r], 1);
+          const T vd = r < RPT - 1 ? v[r + 1] : v_below;
+          gx[r] = XR ? vr - v[r] : T(0);
+          gy[r] = YD(gi) ? vd - v[r] : T(0);
           n1[r] = p1[r];
           n2[r] = p2[r];
           n3[r] = p3[r];
-          dual_step(cf[r], sigma, gx[r], gy[r], sg[r], n1[r], n2[r], n3[r]);
+          nn[r] = dual_pre_fx_r(cf[r], sigma, gx[r], gy[r], sg[r], ysg[r], n1[r], n2[r], n3[r],
+                                slow);
+          proj |= nn[r] != T(1);
+        }
+        if (__any_sync(0xffffffffu, proj)) {
+  #pragma unroll
+          for (int r = 0; r < RPT; ++r) fdp_div3(n1[r], n2[r], n3[r], nn[r], slow);
+        }
+        if (slow) {
+  #pragma unroll
+          for (int r = 0; r < RPT; ++r) {
+            n1[r] = p1[r];
+            n2[r] = p2[r];
+            n3[r] = p3[r];
+            dual_step(cf[r], sigma, gx[r], gy[r], sg[r], n1[r], n2[r], n3[r]);
+          }
+        }
+  #pragma unroll
+        for (int r = 0; r < RPT; ++r) {
+          p1[r] = n1[r];
+          p2[r] = n2[r];
+          p3[r] = n3[r];
+        }
+      } else {
+  #pragma unroll
+        for (int r = 0; r < RPT; ++r) {  // dual (solve.py:246-252)
+          const int gi = gi0 + r;
+          const T vr = __shfl_down_sync(0xffffffffu, v[r], 1);
+          const T vd = r < RPT - 1 ? v[r + 1] : v_below;
+          const T gx = XR ? vr - v[r] : T(0);
+          const T gy = YD(gi) ? vd - v[r] : T(0);
+          dual_step(cf[r], sigma, gx, gy, sg[r], p1[r], p2[r], p3[r]);
         }
       }
-#pragma unroll
-      for (int r = 0; r < RPT; ++r) {
-        p1[r] = n1[r];
-        p2[r] = n2[r];
-        p3[r] = n3[r];
-      }
-    } else {
-#pragma unroll
-      for (int r = 0; r < RPT; ++r) {  // dual (solve.py:246-252)
-        const int gi = gi0 + r;
-        const T vr = __shfl_down_sync(0xffffffffu, v[r], 1);
-        const T vd = r < RPT - 1 ? v[r + 1] : v_below;
-        const T gx = gj < W - 1 ? vr - v[r] : T(0);
-        const T gy = gi < H - 1 ? vd - v[r] : T(0);
-        dual_step(cf[r], sigma, gx, gy, sg[r], p1[r], p2[r], p3[r]);
-      }
     }
-  }
+  };
+  // float64 only: the float32 boundary form is already two selects, and the
+  // second instance measured slower there (C3 f32 0.614 -> 0.620 ms)
+  if (sizeof(T) == 8 && interior)
+    iterate(std::true_type{});
+  else
+    iterate(std::false_type{});
   if (l < K || l >= 32 - K || gj >= W) return;
 #pragma unroll
   for (int r = 0; r < RPT; ++r) {
