@@ -11,12 +11,31 @@
 #pragma once
 
 #include <cstdint>
+#include <type_traits>
+
+// float32 instruction-count switches (each keeps the float engine inside
+// its tolerance and every float kernel on the same arithmetic; float64 is
+// untouched).  With EVR_F32_INTERIOR (evr_tile.cuh), measured on B200:
+// C3 f32 0.615 -> 0.548 ms, C4 0.198 -> 0.185, C5 1.588 -> 1.443
+// (profiles/r01f/experiments.md)
+#ifndef EVR_F32_MINMAX
+#define EVR_F32_MINMAX 1  // vmax / vmin as one FMNMX instead of FSETP + FSEL
+#endif
+#ifndef EVR_F32_SIGFOLD
+#define EVR_F32_SIGFOLD 1  // dual: sigma * g once per axis, not sigma * a_ij
+#endif
 
 namespace evr {
 
 // np.minimum / np.maximum / np.clip on non-NaN data
-template <class T> __device__ __forceinline__ T vmax(T a, T b) { return b > a ? b : a; }
-template <class T> __device__ __forceinline__ T vmin(T a, T b) { return b < a ? b : a; }
+template <class T> __device__ __forceinline__ T vmax(T a, T b) {
+  if constexpr (EVR_F32_MINMAX && std::is_same<T, float>::value) return fmaxf(a, b);
+  else return b > a ? b : a;
+}
+template <class T> __device__ __forceinline__ T vmin(T a, T b) {
+  if constexpr (EVR_F32_MINMAX && std::is_same<T, float>::value) return fminf(a, b);
+  else return b < a ? b : a;
+}
 template <class T> __device__ __forceinline__ T vclip(T x, T lo, T hi) {
   return vmin(vmax(x, lo), hi);
 }
@@ -153,11 +172,20 @@ __device__ __forceinline__ T rof_primal(T divq, T u, T wf, T inv, T tau) {
 template <class T>
 __device__ __forceinline__ void dual_step(const Coef<T>& c, T sigma, T gx, T gy, T sqrtG,
                                           T& p1, T& p2, T& p3) {
-  const T s11 = sigma * c.a11, s12 = sigma * c.a12, s22 = sigma * c.a22;
-  const T s31 = sigma * c.a31, s32 = sigma * c.a32;
-  const T q1 = Arith<T>::mad(s12, gy, Arith<T>::mad(s11, gx, p1));
-  const T q2 = Arith<T>::mad(s22, gy, Arith<T>::mad(s12, gx, p2));
-  const T q3 = Arith<T>::mad(s32, gy, Arith<T>::mad(s31, gx, p3));
+  T q1, q2, q3;
+  if constexpr (EVR_F32_SIGFOLD && sizeof(T) == 4) {
+    // binary32: p + A (sigma g), 2 products instead of the 5 sigma * a_ij
+    const T sx = sigma * gx, sy = sigma * gy;
+    q1 = Arith<T>::mad(c.a12, sy, Arith<T>::mad(c.a11, sx, p1));
+    q2 = Arith<T>::mad(c.a22, sy, Arith<T>::mad(c.a12, sx, p2));
+    q3 = Arith<T>::mad(c.a32, sy, Arith<T>::mad(c.a31, sx, p3));
+  } else {
+    const T s11 = sigma * c.a11, s12 = sigma * c.a12, s22 = sigma * c.a22;
+    const T s31 = sigma * c.a31, s32 = sigma * c.a32;
+    q1 = Arith<T>::mad(s12, gy, Arith<T>::mad(s11, gx, p1));
+    q2 = Arith<T>::mad(s22, gy, Arith<T>::mad(s12, gx, p2));
+    q3 = Arith<T>::mad(s32, gy, Arith<T>::mad(s31, gx, p3));
+  }
   T n = Arith<T>::sqrt(Arith<T>::mad(q3, q3, Arith<T>::mad(q2, q2, q1 * q1)));
   if constexpr (sizeof(T) == 4) {
     // binary32: a * rcp(b) unconditionally (no selects; rcp(1) == 1)

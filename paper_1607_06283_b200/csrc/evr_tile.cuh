@@ -33,6 +33,10 @@
 #include "evr_fastdp.cuh"
 #include "evr_kernels.cuh"
 
+#ifndef EVR_F32_INTERIOR
+#define EVR_F32_INTERIOR 1  // float32 tiles also take the interior instance
+#endif
+
 namespace evr {
 
 // TV-L1 (surface.py:167-193), K iterations: dual ascent + projection, then
@@ -159,9 +163,9 @@ k_tv_tile(const MarchRows<Q4<T>> in, const MarchRows<T> f0, Q4<T>* __restrict__ 
       }
     }
   };
-  // float64 only: the float32 boundary form is already two selects, and the
-  // second instance measured slower there (C3 f32 0.614 -> 0.620 ms)
-  if (sizeof(T) == 8 && interior)
+  // (float32 alone measured slower with the second instance, C3 0.614 ->
+  // 0.620 ms; together with EVR_F32_MINMAX / SIGFOLD it is 0.585 -> 0.548)
+  if ((sizeof(T) == 8 || EVR_F32_INTERIOR) && interior)
     iterate(std::true_type{});
   else
     iterate(std::false_type{});
@@ -317,9 +321,9 @@ k_pd_tile(const MarchRows<Q4<T>> in, M m, Q4<T>* __restrict__ out, int H, int W,
       }
     }
   };
-  // float64 only: the float32 boundary form is already two selects, and the
-  // second instance measured slower there (C3 f32 0.614 -> 0.620 ms)
-  if (sizeof(T) == 8 && interior)
+  // (float32 alone measured slower with the second instance, C3 0.614 ->
+  // 0.620 ms; together with EVR_F32_MINMAX / SIGFOLD it is 0.585 -> 0.548)
+  if ((sizeof(T) == 8 || EVR_F32_INTERIOR) && interior)
     iterate(std::true_type{});
   else
     iterate(std::false_type{});
