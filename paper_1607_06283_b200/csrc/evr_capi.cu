@@ -202,9 +202,10 @@ struct Step {
 // which: 0 = surface (ingest .. metric), 1 = solve (primal-dual + epilogue), 2 = both.
 // fused: one launch per TV-L1 / primal-dual iteration (k_tv_march,
 // k_pd_march) on the packed, ping-ponged state, or -- tk > 1, whole-sensor
-// contexts -- tk iterations per launch (k_tv_tile, k_pd_tile); the last
-// primal-dual iteration always runs alone, so rel_change sees the u of the
-// two last iterations.  Split list (bands with EVR_GROUP_SPLIT): one launch
+// contexts -- tk iterations per launch (k_tv_tile, k_pd_tile; a remainder
+// of 2..tk-1 iterations as one shorter tile, C3 float32 3 + 2 march launches
+// -> 2 tiles); the last primal-dual iteration always runs alone, so
+// rel_change sees the u of the two last iterations.  Split list (bands with EVR_GROUP_SPLIT): one launch
 // per half-step with halo rows exchanged between half-steps.
 std::vector<Step> packet_steps(const evr_config& g, int which, bool fused, int tk = 1) {
   std::vector<Step> v;
@@ -217,7 +218,7 @@ std::vector<Step> packet_steps(const evr_config& g, int which, bool fused, int t
       int b = 0;
       for (int k = 0; k < D;) {
         if (fused) {
-          const int kk = D - k >= tk ? tk : 1;
+          const int kk = std::min(tk, D - k);  // the remainder as one shorter tile
           v.push_back({ST_TVF, k, b, kk});
           b ^= 1;
           k += kk;
@@ -236,7 +237,7 @@ std::vector<Step> packet_steps(const evr_config& g, int which, bool fused, int t
     int b = 0;
     for (int k = 0; k < M;) {
       if (fused) {
-        const int kk = M - 1 - k >= tk ? tk : 1;
+        const int kk = std::max(1, std::min(tk, M - 1 - k));
         v.push_back({ST_PDF, k, b, kk});
         if (k == M - 1) v.push_back({ST_RELF, k, b});
         b ^= 1;
