@@ -64,6 +64,7 @@ struct evr_ctx {
   double* aos_a = nullptr;  // (H, W, 3) staging
   double* aos_b = nullptr;
   double* part = nullptr;   // reduction partials
+  unsigned* rticket = nullptr;  // k_relchange's last-CTA ticket
   double* d_scalar = nullptr;
   int* d_err = nullptr;
   evr_solve_info* d_info = nullptr;
@@ -356,10 +357,9 @@ void launch_pdl(void (*k)(KArgs...), unsigned grid, unsigned block, cudaStream_t
 template <class T>
 void relchange(evr_ctx* ctx, const T* un, const T* u, int iterations, int stride = 1) {
   const int nb = red_blocks(ctx->own_n());
-  k_relchange_partial<T, kNT><<<nb, kNT, 0, ctx->stream>>>(
-      un + ctx->own_off() * stride, u + ctx->own_off() * stride, ctx->own_n(), ctx->part, stride);
-  k_relchange_final<kNT><<<1, kNT, 0, ctx->stream>>>(ctx->part, nb, ctx->d_info, iterations,
-                                                    ctx->d_scalar + 2);
+  launch_pdl(k_relchange<T, kNT>, nb, kNT, ctx->stream, un + ctx->own_off() * stride,
+             u + ctx->own_off() * stride, ctx->own_n(), ctx->part, stride, ctx->rticket,
+             ctx->d_info, iterations, ctx->d_scalar + 2);
 }
 
 // temporally blocked tiles (evr_tile.cuh): a CTA of G warps covers 32 x
@@ -1312,6 +1312,8 @@ int evr_create(evr_ctx** out, int device, int height, int width, int precision) 
     CK(cudaMalloc(&ctx->aos_a, sizeof(double) * 3 * N));
     CK(cudaMalloc(&ctx->aos_b, sizeof(double) * 3 * N));
     CK(cudaMalloc(&ctx->part, sizeof(double) * 2 * kRedBlocks));
+    CK(cudaMalloc(&ctx->rticket, sizeof(unsigned)));
+    CK(cudaMemsetAsync(ctx->rticket, 0, sizeof(unsigned), ctx->stream));
     CK(cudaMalloc(&ctx->d_scalar, sizeof(double) * 4));
     CK(cudaMalloc(&ctx->d_err, sizeof(int)));
     CK(cudaMemsetAsync(ctx->d_err, 0, sizeof(int), ctx->stream));
@@ -1344,6 +1346,7 @@ void evr_destroy(evr_ctx* ctx) {
   cudaFree(ctx->aos_a);
   cudaFree(ctx->aos_b);
   cudaFree(ctx->part);
+  cudaFree(ctx->rticket);
   cudaFree(ctx->d_scalar);
   cudaFree(ctx->d_err);
   cudaFree(ctx->d_info);

@@ -720,12 +720,17 @@ __device__ __forceinline__ double block_sum(double x, double* sh) {
   return x;
 }
 
-// rel_change partials: sum (un-u)^2 and sum u^2 (solve.py:246-249)
+// rel_change = |u+ - u| / max(|u|, 1e-30) (solve.py:246-249) in one launch:
+// each CTA writes its partial sums of (un-u)^2 and u^2 in a fixed order, the
+// last CTA to take the ticket folds the partials in index order and resets
+// the ticket (deterministic: the same bits every run)
 template <class T, int NT>
 __global__ void __launch_bounds__(NT)
-k_relchange_partial(const T* __restrict__ un, const T* __restrict__ u, int64_t N,
-                    double* __restrict__ part, int stride = 1) {
+k_relchange(const T* __restrict__ un, const T* __restrict__ u, int64_t N, double* part,
+            int stride, unsigned* ticket, evr_solve_info* info, int iterations, double* sums) {
   __shared__ double sh[NT / 32];
+  __shared__ bool last;
+  pdl_wait_and_release();
   double d = 0.0, o = 0.0;
   for (int64_t k = (int64_t)blockIdx.x * NT + threadIdx.x; k < N; k += (int64_t)gridDim.x * NT) {
     const double a = (double)un[k * stride], b = (double)u[k * stride];
@@ -737,18 +742,18 @@ k_relchange_partial(const T* __restrict__ un, const T* __restrict__ u, int64_t N
   if (threadIdx.x == 0) {
     part[2 * blockIdx.x] = d;
     part[2 * blockIdx.x + 1] = o;
+    __threadfence();
+    last = atomicAdd(ticket, 1u) == gridDim.x - 1;
   }
-}
-
-template <int NT>
-__global__ void __launch_bounds__(NT)
-k_relchange_final(const double* __restrict__ part, int nb, evr_solve_info* info,
-                  int iterations, double* sums) {
-  __shared__ double sh[NT / 32];
-  double d = 0.0, o = 0.0;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  const int nb = (int)gridDim.x;
+  d = 0.0;
+  o = 0.0;
   for (int b = threadIdx.x; b < nb; b += NT) {
-    d += part[2 * b];
-    o += part[2 * b + 1];
+    d += __ldcg(part + 2 * b);
+    o += __ldcg(part + 2 * b + 1);
   }
   d = block_sum<NT>(d, sh);
   o = block_sum<NT>(o, sh);
@@ -758,6 +763,7 @@ k_relchange_final(const double* __restrict__ part, int nb, evr_solve_info* info,
     info->iterations = iterations;
     sums[0] = d;  // evr_group folds the bands' sums
     sums[1] = o;
+    *ticket = 0u;
   }
 }
 
