@@ -2,7 +2,8 @@
 
 Input: `ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum
 --csv` of a bench.py run.  Packets are split at k_stage_device (the first
-launch of every packet); the first packet (cold start) and a trailing partial
+launch of every packet) and torch's own kernels (bench.py's L2 flush) are
+left out; the first packet (cold start) and a trailing partial
 one are dropped, and the median complete packet is reported with its
 per-kernel breakdown.  ncu flushes the caches before every launch (its default
 cache control), so this is cold-cache traffic: an upper bound on what the
@@ -30,6 +31,8 @@ for r in rows[1:]:
 
 packets, cur = [], None
 for d in launch.values():
+    if d["name"].startswith("at::"):  # torch kernels: bench.py's L2 flush, setup fills
+        continue
     if "k_stage_device" in d["name"]:
         if cur:
             packets.append(cur)
