@@ -132,7 +132,7 @@ __global__ void __launch_bounds__(NT, 1) k_resident_col(const ResArgs<T> a) {
   const bool tracing = a.trace != nullptr && tid == 0;
   auto mark = [&]() {
     if (tracing) {
-      if (tmark < 256) {
+      if (tmark < 255) {  // slot 255: the SM id
         unsigned long long t;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t)::"memory");
         a.trace[(size_t)b * 256 + tmark] = t;
@@ -601,6 +601,7 @@ __global__ void __launch_bounds__(NT, 1) k_resident_col(const ResArgs<T> a) {
       *a.ticket = 0u;
     }
   }
+  mark();  // kernel end (after the epilogue and the rel_change fold)
 }
 
 }  // namespace evr
