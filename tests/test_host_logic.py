@@ -66,6 +66,21 @@ def test_algorithmic_bytes_formula():
     assert abs(bench.algorithmic_bytes(720, 1280, 4, 100, 50) - 5.71e9) < 0.01e9
 
 
+def test_traffic_covers_every_bench_config():
+    """profiles/traffic.json (bench.py's roofline.traffic) has a DRAM figure for
+    every config / precision of bench.py, keyed by the engine AUTO picks, and
+    each figure is below the config's algorithmic bytes (on-chip reuse)."""
+    import json
+
+    tr = json.load(open(os.path.join(os.path.dirname(bench.__file__), "profiles", "traffic.json")))
+    for name, (H, W, _epp, pd, tv, _rate) in bench.CONFIGS.items():
+        for prec, w in (("f64", 8), ("f32", 4)):
+            hits = [k for k in tr if k.startswith(f"{name}/{prec}/")]
+            assert hits, f"no traffic entry for {name}/{prec}"
+            for k in hits:
+                assert 0 < tr[k]["bytes_per_launch"] < bench.algorithmic_bytes(H, W, w, pd, tv), k
+
+
 def _free_port():
     s = socket.socket()
     s.bind(("127.0.0.1", 0))
