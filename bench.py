@@ -3,21 +3,27 @@
 
 One step = one event packet through ingest -> normalize -> TV-L1 -> metric
 -> manifold-TV/KL primal-dual -> re-anchor, on the BASELINE.json workload
-that fits one GPU (configs[1], DAVIS346 346x260, 500-event packets, 50 PD +
-50 TV-L1 iterations; synthetic generator U of SURVEY.md 8(d)).
+the metric is quoted on that fits one GPU: configs[2], 1280x720 at 1 Mev/s,
+1000-event packets, 100 PD + 50 TV-L1 iterations, float64 (the reference's
+arithmetic), synthetic generator U of SURVEY.md 8(d).
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--precision f64|f32]
-  python bench.py --impl reference ...   # the CPU reference path (C port)
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C1..C5]
+                  [--precision f64|f32]
+  python bench.py --impl reference ...    # the reference algorithm on the host cores
+  python bench.py --config C5 --bands N   # one 2048^2 sensor split in N row bands,
+                                          # one band per visible GPU (configs[4])
 
 Multi-GPU (torchrun, one rank per GPU): every rank reconstructs its own
-independent stream (different seed), no collective on the data path
+independent stream (seed 1 + rank), no collective on the data path
 ("scaling": "weak"); timing is the max over ranks.
 
 Rank 0 prints ONE JSON line.  `value` is events/s with the packets resident
 in HBM, timed with CUDA events on the context's stream, L2 flushed before
 every step (outside the per-step event pair); `e2e` is the same metric
-through the public API (process_packet_arrays) from pinned host events,
-including the frame read-back.
+through the public stream API from pinned host events, every frame read
+back.  `roofline` names the binding resource of the dominant kernel (the
+float64 pipe) with its algorithmic operations, and carries
+the measured DRAM traffic of that kernel from the committed ncu capture.
 """
 
 from __future__ import annotations
@@ -25,6 +31,7 @@ from __future__ import annotations
 import argparse
 import ctypes
 import json
+import multiprocessing as mp
 import os
 import statistics
 import subprocess
@@ -52,12 +59,19 @@ DESCR = {
     "C4": "640x480 @ 1 Mev/s per stream, 1000-event packets, 50 PD + 50 TV-L1 iters",
     "C5": "2048x2048 @ 1 Mev/s, 1000-event packets, 50 PD + 50 TV-L1 iters",
 }
+# IEEE float64 operations of the reference per pixel and iteration
+# (DESIGN.md 4.4): primal-dual solve.py:233-252 = 47
+# (q = A^T p 10, s 6, KL root 5, over-relaxation 2, forward differences 2,
+# dual ascent 12, norm / sqrtG 7, projection 3), TV-L1 surface.py:168-193 =
+# 21 (ascent 6, norm 4, projection 2, divergence + step 5, shrink 1,
+# over-relaxation 3); division and square root count as one operation each
+PD_OPS, TV_OPS = 47, 21
 
 
 def gen_packets(H, W, epp, n_packets, rate, seed):
     """Generator U: uniform pixels and polarities,
     t_i = i * 1e6 / rate microseconds."""
-    from paper_1607_06283_b200 import make_event_array
+    from paper_1607_06283_b200.events import make_event_array
 
     rng = np.random.default_rng(seed)
     n = epp * n_packets
@@ -83,6 +97,28 @@ def windows_for(packets, t_window=None, maxlen=10):
 def algorithmic_bytes(H, W, w, pd, tv):
     """B_pkt = N * w * (11 * I_pd + 9 * I_tv)."""
     return H * W * w * (11 * pd + 9 * tv)
+
+
+def algorithmic_ops(H, W, pd, tv):
+    """Reference float64 operations of one packet's iterations."""
+    return H * W * (PD_OPS * pd + TV_OPS * tv)
+
+
+def workload_config(name, precision):
+    """The `config` object both arms print (identical keys and values)."""
+    H, W, epp, pd, tv, rate = CONFIGS[name]
+    return {"workload": DESCR[name], "sensor": f"{W}x{H}", "events_per_packet": epp,
+            "pd_iterations": pd, "tv_iterations": tv, "precision": precision,
+            "generator": "U(seed = 1 + rank, W, H, 1 Mev/s)",
+            "l2": "flushed (256 MiB write) before every timed GPU step"}
+
+
+def load_json(*parts):
+    try:
+        with open(os.path.join(ROOT, *parts)) as fh:
+            return json.load(fh)
+    except (OSError, ValueError):
+        return {}
 
 
 class ClockSampler:
@@ -144,7 +180,7 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def dist_init(args):
+def dist_init():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
@@ -176,12 +212,13 @@ def barrier(world):
         dist.barrier()
 
 
-# ----------------------------------------------------------------------------
+# ------------------------------------------------------------- CPU arms --
 
 
 def cpu_port_run(H, W, epp, pd, tv, rate, n_packets, seed, budget_s):
-    """The reference algorithm on host cores via the C port (oracle/), one
-    packet per step; returns (seconds per packet list, threads)."""
+    """The reference algorithm on host cores via the C port (oracle/, OpenMP
+    over all host threads), one packet per step; returns (seconds per
+    packet, threads)."""
     from oracle import oracle as O
 
     packets = gen_packets(H, W, epp, n_packets, rate, seed)
@@ -197,6 +234,67 @@ def cpu_port_run(H, W, epp, pd, tv, rate, n_packets, seed, budget_s):
     return times, O.num_threads()
 
 
+def _numpy_ref_stream(args):
+    """One stream of the unmodified numpy reference (baseline/_ref, the
+    reference package installed from /root/reference) through its own
+    process_packet, timed per packet as run_stream does (pipeline.py:239-249);
+    runs in its own process pinned to one core."""
+    H, W, epp, pd, tv, rate, seed, n_packets, budget_s, core = args
+    try:
+        if core is not None:
+            os.sched_setaffinity(0, {core})
+    except OSError:
+        pass
+    os.environ["OMP_NUM_THREADS"] = os.environ["OPENBLAS_NUM_THREADS"] = "1"
+    sys.path.insert(0, os.path.join(ROOT, "baseline", "_ref"))
+    from evrecon.events import Event, SensorGeometry
+    from evrecon.pipeline import ManifoldConfig, Thresholds, init_state, process_packet
+    from evrecon.solve import SolverConfig
+
+    packets = gen_packets(H, W, epp, n_packets, rate, seed)
+    sc = SolverConfig(max_iterations=pd)
+    mc = ManifoldConfig(denoise_iterations=tv)
+    th = Thresholds()
+    st = init_state(SensorGeometry(W, H), sc)
+    times = []
+    t_start = time.perf_counter()
+    for pk in packets:
+        evs = [Event(int(e["x"]), int(e["y"]), int(e["polarity"]), int(e["t"])) for e in pk]
+        t0 = time.perf_counter()
+        process_packet(st, evs, mc, sc, th)
+        times.append(time.perf_counter() - t0)
+        if time.perf_counter() - t_start > budget_s:
+            break
+    return times
+
+
+def numpy_reference(H, W, epp, pd, tv, rate, budget_s, processes):
+    """The stock numpy reference, 1 core (seed 1, the GPU arm's rank-0
+    stream) and, when processes > 1, an all-core aggregate of independent
+    streams (one process per core).  None when baseline/_ref is absent."""
+    if not os.path.isdir(os.path.join(ROOT, "baseline", "_ref", "evrecon")):
+        return None
+    cores = sorted(os.sched_getaffinity(0))
+    one = _numpy_ref_stream((H, W, epp, pd, tv, rate, 1, 1000, budget_s, cores[0]))
+    out = {"value": round(epp * len(one) / sum(one), 3), "unit": "events/s", "cores": 1,
+           "kind": "reference", "ms_per_packet": round(1e3 * sum(one) / len(one), 2),
+           "sample": f"{len(one)} packets of the same workload through the unmodified evrecon "
+                     f"process_packet (baseline/_ref, numpy float64), one core"}
+    if processes > 1:
+        n = min(processes, len(cores))
+        jobs = [(H, W, epp, pd, tv, rate, 1 + k, 1000, budget_s, cores[k]) for k in range(n)]
+        t0 = time.perf_counter()
+        with mp.get_context("spawn").Pool(n) as pool:
+            res = pool.map(_numpy_ref_stream, jobs)
+        wall = time.perf_counter() - t0
+        packets = sum(len(r) for r in res)
+        # aggregate rate: every stream's own packets over its own busy time
+        rate_sum = sum(epp * len(r) / sum(r) for r in res)
+        out["all_cores"] = {"value": round(rate_sum, 3), "unit": "events/s", "cores": n,
+                            "streams": n, "packets": packets, "wall_s": round(wall, 2)}
+    return out
+
+
 def run_reference(args):
     # CPU arm: rank 0 alone runs (no process group, no GPU work)
     if int(os.environ.get("RANK", "0")) != 0:
@@ -204,24 +302,23 @@ def run_reference(args):
     H, W, epp, pd, tv, rate = CONFIGS[args.config]
     os.environ.setdefault("OMP_NUM_THREADS", str(len(os.sched_getaffinity(0))))
     n = args.warmup + args.steps
-    times, threads = cpu_port_run(H, W, epp, pd, tv, rate, n, seed=1, budget_s=1e9)
-    timed = times[args.warmup:]
+    times, threads = cpu_port_run(H, W, epp, pd, tv, rate, n, seed=1, budget_s=args.ref_budget)
+    timed = times[args.warmup:] if len(times) > args.warmup else times[-1:]
     sec = sum(timed)
     value = epp * len(timed) / sec
     line = {
         "impl": "reference", "metric": "events/s", "value": round(value, 3), "unit": "events/s",
-        "n_gpus": args.gpus, "steps": len(timed), "warmup": args.warmup,
+        "n_gpus": args.gpus, "steps": len(timed), "warmup": min(args.warmup, len(times) - 1),
         "ms_per_step": round(1e3 * sec / len(timed), 4), "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "scaling": "weak", "vs_baseline": None, "dtype": args.precision, "data": "synthetic",
         "frames_per_s": round(len(timed) / sec, 4),
-        "config": {"workload": DESCR[args.config], "sensor": f"{W}x{H}",
-                   "events_per_packet": epp, "pd_iterations": pd, "tv_iterations": tv,
-                   "engine": "cpu (C port of the reference)", "precision": "f64",
-                   "streams": "1 (rank 0 only)", "generator": "U(seed, W, H, 1 Mev/s)"},
+        "config": workload_config(args.config, args.precision),
+        "engine": "cpu: C port of the reference (oracle/evr_oracle.c), float64",
         "cpu_baseline": {"value": round(value, 3), "unit": "events/s", "cores": threads,
                          "kind": "port",
-                         "sample": f"{len(timed)} packets of the same workload, C port of "
-                                   f"the reference (oracle/evr_oracle.c, OpenMP {threads} threads)"},
+                         "sample": f"{len(timed)} packets of the same workload and seed as the "
+                                   f"GPU arm's rank 0, C port of the reference "
+                                   f"(oracle/evr_oracle.c, OpenMP {threads} threads)"},
         "e2e": {"value": round(value, 3), "unit": "events/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -229,8 +326,74 @@ def run_reference(args):
     return 0
 
 
+# ---------------------------------------------------------------- GPU arm --
+
+
+def roofline_of(args, ctx, st, H, W, pd, tv, step_ms):
+    """Roofline of the dominant kernel.  Streaming engine: the primal-dual
+    tile, timed live (evr_time_iteration_kernel: CUDA events around
+    back-to-back launches on the context stream); resident engine: the one
+    packet launch (the step).  Bound: the float64 pipe; the
+    achieved rate counts the reference's IEEE operations (PD_OPS / TV_OPS),
+    the peak is the measured DFMA rate (profiles/fp64_peak.json)."""
+    from paper_1607_06283_b200 import _lib
+
+    peaks = load_json("MEASURED_PEAKS.json")
+    fp64 = load_json("profiles", "fp64_peak.json")
+    peak = float(fp64.get("fp64_tops", 18.37))
+    hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
+    detail = ctx.engine_detail()
+    engine = st.engine()
+    ncu = load_json("profiles", "roofline_ncu.json")
+    if engine == "streaming":
+        us = ctypes.c_float(0.0)
+        k = ctypes.c_int(0)
+        ctx.call("evr_time_iteration_kernel", 0, 20, ctypes.byref(us), ctypes.byref(k))
+        kern_us = float(us.value)
+        ops = H * W * PD_OPS * k.value
+        launches_per_packet = pd / k.value
+        name = f"k_pd_tile ({k.value} primal-dual iterations per launch)"
+        key = f"{args.config}/{args.precision}/k_pd_tile"
+    else:
+        kern_us = step_ms * 1e3
+        ops = algorithmic_ops(H, W, pd, tv)
+        launches_per_packet = 1
+        name = "k_resident_col (one launch per packet: ingest .. TV-L1 .. metric .. solve)"
+        key = f"{args.config}/{args.precision}/k_resident_col"
+    achieved = ops / (kern_us * 1e-6) / 1e12
+    hit = ncu.get(key)
+    if hit and hit.get("engine_detail") != detail:
+        hit = None  # captured on another kernel shape: not this run's traffic
+    line = {"bound": "fp64", "achieved": round(achieved, 4), "peak": peak, "unit": "TFLOP/s",
+            "frac": round(achieved / peak, 4),
+            "traffic": hit["dram_bytes_per_launch"] if hit else None,
+            "kernel": name, "kernel_us": round(kern_us, 3),
+            "share_of_step": round(min(1.0, kern_us * launches_per_packet / (step_ms * 1e3)), 4),
+            "ops_per_launch": ops,
+            "ops_note": f"reference IEEE float64 operations, {PD_OPS} per pixel and primal-dual "
+                        f"iteration, {TV_OPS} per TV-L1 iteration (div / sqrt = 1)",
+            "peak_source": "profiles/fp64_peak.json (measured DFMA rate, tools/dp_ilp.cu)"
+                           if fp64 else "fallback 18.37 T/s",
+            "engine_detail": detail}
+    if hit:
+        gbs = hit["dram_bytes_per_launch"] / (kern_us * 1e-6) / 1e9
+        line["hbm"] = {"achieved": round(gbs, 1), "peak": hbm_peak, "unit": "GB/s",
+                       "frac": round(gbs / hbm_peak, 4),
+                       "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback"}
+        line["ncu"] = {k2: hit[k2] for k2 in ("fp64_pipe_pct", "issue_pct", "capture")
+                       if k2 in hit}
+    if engine != "streaming":
+        it_us = kern_us / max(pd + tv, 1)
+        line["limiter"] = {"note": "per-iteration neighbour handoff through L2 + float64 "
+                                   "dependency chains (DESIGN.md 4.1)",
+                           "us_per_iteration": round(it_us, 3),
+                           "handoff_floor_us": fp64.get("handoff_floor_us")}
+    line["b_pkt_bytes"] = algorithmic_bytes(H, W, 8 if args.precision == "f64" else 4, pd, tv)
+    return line
+
+
 def run_gpu(args):
-    world, rank, local = dist_init(args)
+    world, rank, local = dist_init()
     os.environ["EVR_DEVICE"] = str(local)
     import torch
 
@@ -240,13 +403,13 @@ def run_gpu(args):
     torch.cuda.set_device(local)
     H, W, epp, pd, tv, rate = CONFIGS[args.config]
     prec = {"f64": 0, "f32": 1}[args.precision]
-    engine = {"auto": 0, "streaming": 1, "resident": 2, "resident_gmem": 3,
-              "resident_reg": 4}[args.engine]
+    engine = {"auto": 0, "streaming": 1, "resident": 2}[args.engine]
     mc = evr.ManifoldConfig(denoise_iterations=tv)
     sc = evr.SolverConfig(max_iterations=pd)
     th = evr.Thresholds()
     n_total = args.warmup + args.steps
-    packets = gen_packets(H, W, epp, 2 * n_total, rate, seed=1000 + rank)
+    # rank r's stream: seed 1 + r (rank 0 = the reference arm's packets)
+    packets = gen_packets(H, W, epp, 2 * n_total, rate, seed=1 + rank)
     wins = windows_for(packets)
 
     st = evr.init_state(evr.SensorGeometry(W, H), sc, precision=prec, engine=engine)
@@ -292,8 +455,9 @@ def run_gpu(args):
     step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
     dev_s = allmax(sum(step_ms) / 1e3, world)
     value = world * epp * args.steps / dev_s
+    roof = roofline_of(args, ctx, st, H, W, pd, tv, statistics.mean(step_ms))
 
-    # end-to-end leg: public API from pinned host events, frame read back
+    # end-to-end legs: the public API from pinned host events, frames back
     pinned = [torch.from_numpy(p.view(np.uint8)).pin_memory().numpy().view(evr.EVENT_DTYPE)
               for p in packets[n_total:]]
     st2 = evr.init_state(evr.SensorGeometry(W, H), sc, precision=prec, engine=engine)
@@ -309,7 +473,7 @@ def run_gpu(args):
             flush.zero_()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        _, frame, _ = evr.process_packet_arrays(st2, pinned[k], mc, sc, th)
+        evr.process_packet_arrays(st2, pinned[k], mc, sc, th)
         e2e_times.append(time.perf_counter() - t0)
     barrier(world)
     blocking = world * epp * args.steps / allmax(sum(e2e_times), world)
@@ -326,39 +490,13 @@ def run_gpu(args):
     barrier(world)
     t0 = time.perf_counter()
     got = 0
-    ticks = []
     for frame, res in evr.stream_packets(st3, pinned[args.warmup:n_total], mc, sc, th):
         got += int(frame is not None and res.iterations == pd)
-        ticks.append(time.perf_counter())
     e2e_s = allmax(time.perf_counter() - t0, world)
-    if os.environ.get("EVR_BENCH_DEBUG"):
-        d = np.diff([t0] + ticks) * 1e3
-        print("e2e stream ms/packet: first %.3f median %.3f max %.3f" % (d[0], np.median(d), d.max()),
-              file=sys.stderr)
     assert got == args.steps
     e2e = world * epp * args.steps / e2e_s
 
-    # roofline of the dominant kernel (one packet = one persistent launch on the
-    # resident engine; whole-graph time on the streaming engine)
-    w = 8 if prec == 0 else 4
-    bpkt = algorithmic_bytes(H, W, w, pd, tv)
-    kern_ms = statistics.mean(step_ms)
-    peaks = {}
-    try:
-        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
-    except OSError:
-        pass
-    peak = float(peaks.get("hbm_gbs", 6650.0))
-    achieved = bpkt / (kern_ms * 1e-3) / 1e9
-    traffic = None
-    try:
-        tr = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))
-        hit = tr.get(f"{args.config}/{args.precision}/{st.engine()}")
-        traffic = hit["bytes_per_launch"] if hit else None
-    except (OSError, ValueError, KeyError):
-        pass
-
-    cpu = None
+    cpu = numpy_ref = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         os.environ.setdefault("OMP_NUM_THREADS", str(len(os.sched_getaffinity(0))))
         times, threads = cpu_port_run(H, W, epp, pd, tv, rate, 400, seed=1,
@@ -366,8 +504,14 @@ def run_gpu(args):
         times = times[1:] if len(times) > 1 else times
         cpu = {"value": round(epp * len(times) / sum(times), 3), "unit": "events/s",
                "cores": threads, "kind": "port",
-               "sample": f"{len(times)} packets of the same workload (first packet excluded), "
-                         f"C port of the reference (oracle/evr_oracle.c), OpenMP {threads} threads"}
+               "sample": f"{len(times)} packets of the same workload and seed as the GPU "
+                         f"arm's rank 0 (first packet excluded), C port of the reference "
+                         f"(oracle/evr_oracle.c), OpenMP {threads} threads"}
+        numpy_ref = numpy_reference(
+            H, W, epp, pd, tv, rate, args.numpy_budget,
+            len(os.sched_getaffinity(0)) if args.config in ("C1", "C4") else 1)
+        if numpy_ref is not None:
+            cpu["numpy_reference"] = numpy_ref
 
     if rank == 0:
         line = {
@@ -376,25 +520,16 @@ def run_gpu(args):
             "ms_per_step": round(dev_s * 1e3 / args.steps, 5), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": args.precision, "data": "synthetic",
             "frames_per_s": round(world * args.steps / dev_s, 2),
-            "config": {"workload": DESCR[args.config], "sensor": f"{W}x{H}",
-                       "events_per_packet": epp, "pd_iterations": pd, "tv_iterations": tv,
-                       "engine": st.engine(), "precision": args.precision,
-                       "streams": f"{world} independent (1 per GPU)",
-                       "l2": "flushed (256 MiB write) before every timed step",
-                       "generator": "U(seed, W, H, 1 Mev/s)"},
+            "config": workload_config(args.config, args.precision),
+            "engine": f"{st.engine()}: {ctx.engine_detail()}",
+            "streams": f"{world} independent (1 per GPU)",
             "e2e": {"value": round(e2e, 1), "unit": "events/s",
                     "h2d_bytes_per_step": 32 + 16 * epp, "d2h_bytes_per_step": 8 * H * W + 24,
                     "api": "stream_packets (run_stream loop, 2 packets in flight)",
                     "blocking_value": round(blocking, 1),
                     "blocking_api": "process_packet_arrays, one synchronous call per step"},
             "gpu_launches": int(launches),
-            "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
-                         "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": traffic,
-                         "kernel": ctx.engine_detail() + (
-                             " (one launch per packet)" if st.engine().startswith("resident")
-                             else " (whole packet graph)"),
-                         "algorithmic_bytes_per_launch": bpkt,
-                         "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback"},
+            "roofline": roof,
             "clocks": clocks.summary(),
             "cpu_baseline": cpu,
         }
@@ -406,23 +541,156 @@ def run_gpu(args):
     return 0
 
 
+def run_bands(args):
+    """configs[4]: one sensor split into row bands, one band per visible GPU
+    (BandedStream over evr_group; the neighbours' halo rows read in place
+    over NVLink peer memory).  Wall time of synchronous packets (the group
+    call synchronizes every band), L2 not flushed (each band's set exceeds
+    the flush's purpose at 2048^2: 33.6 MB per float64 field)."""
+    import torch
+
+    import paper_1607_06283_b200 as evr
+    from paper_1607_06283_b200.group import BandedStream
+
+    if int(os.environ.get("RANK", "0")) != 0:
+        return 0
+    H, W, epp, pd, tv, rate = CONFIGS[args.config]
+    ngpu = torch.cuda.device_count()
+    bands = args.bands
+    devices = [b % ngpu for b in range(bands)]
+    prec = {"f64": 0, "f32": 1}[args.precision]
+    sc = evr.SolverConfig(max_iterations=pd)
+    mc = evr.ManifoldConfig(denoise_iterations=tv)
+    bs = BandedStream(evr.SensorGeometry(W, H), sc, mc, evr.Thresholds(), bands=bands,
+                      devices=devices, precision=prec)
+    packets = gen_packets(H, W, epp, args.warmup + args.steps, rate, seed=1)
+    for k in range(args.warmup):
+        bs.process_packet(packets[k], want_frame=False)
+    n0 = bs.launch_count()
+    with ClockSampler(0) as clocks:
+        t0 = time.perf_counter()
+        for k in range(args.warmup, args.warmup + args.steps):
+            bs.process_packet(packets[k], want_frame=False)
+        sec = time.perf_counter() - t0
+    line = {
+        "metric": "events/s", "value": round(epp * args.steps / sec, 1), "unit": "events/s",
+        "n_gpus": len(set(devices)), "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(1e3 * sec / args.steps, 5), "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": args.precision, "data": "synthetic",
+        "frames_per_s": round(args.steps / sec, 2),
+        "config": workload_config(args.config, args.precision),
+        "engine": f"row bands: {bands} bands on devices {devices} (evr_group, fused tiles, "
+                  f"halo rows read in place from the neighbours)",
+        "timing": "host wall clock around synchronous group packets",
+        "gpu_launches": int(bs.launch_count() - n0),
+        "clocks": clocks.summary(),
+    }
+    print(json.dumps(line), flush=True)
+    bs.close()
+    return 0
+
+
+VARIANTS = {
+    # name: (lam, iterations, what) -- BASELINE configs[1]: "TV and TGV
+    # regularisers, KL vs ROF/L1 data terms" on the DAVIS346 grid
+    "rof": (8.0, 300, "manifold-TV + ROF (rof_manifold_solve, solve.py:264-293), cold start"),
+    "l1": (3.0, 300, "manifold-TV + L1 data term (not in the reference), cold start"),
+    "tgv": (6.0, 300, "second-order manifold TGV + KL (not in the reference), cold start"),
+}
+
+
+def run_variant(args):
+    """One operator-level solve per step on a steep synthetic manifold at the
+    config's sensor size, through the public API with host arrays (the
+    upload of f and the metric and the download of u inside the step)."""
+    import torch
+
+    import paper_1607_06283_b200 as evr
+    from oracle import oracle as O
+    from paper_1607_06283_b200.surface import op_context
+
+    if int(os.environ.get("RANK", "0")) != 0:
+        return 0
+    H, W = CONFIGS[args.config][:2]
+    lam, iters, what = VARIANTS[args.variant]
+    yy, xx = np.mgrid[0:H, 0:W]
+    t = 3.0 * np.sin(xx / 6.0) * np.cos(yy / 9.0) ** 2
+    m = evr.compute_metric(t)
+    rng = np.random.default_rng(1)
+    f = np.clip(1.5 + 0.3 * np.sin(xx / 5.0) + rng.normal(0, 0.05, (H, W)), 1.0, 2.0)
+    run = {"rof": lambda: evr.rof_manifold_solve(f, m, lam, iters),
+           "l1": lambda: evr.l1_manifold_solve(f, m, lam, iters),
+           "tgv": lambda: evr.tgv_manifold_solve(f, m, lam, iterations=iters, data="kl")}[
+        args.variant]
+    for _ in range(args.warmup):
+        run()
+    ctx = op_context((H, W))
+    n0 = ctx.launch_count()
+    torch.cuda.synchronize()
+    with ClockSampler(0) as clocks:
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            run()
+        sec = time.perf_counter() - t0
+    launches = ctx.launch_count() - n0
+    cpu_fn = {"rof": lambda: O.rof_solve(f, m.tx, m.ty, m.G, m.sqrtG, lam, iters),
+              "l1": lambda: O.l1_solve(f, m.tx, m.ty, m.G, m.sqrtG, lam, iters),
+              "tgv": lambda: O.tgv_solve(f, m.tx, m.ty, m.G, m.sqrtG, lam, data="kl",
+                                         iterations=iters)}[args.variant]
+    ct = []
+    tc = time.perf_counter()
+    while time.perf_counter() - tc < args.cpu_budget and len(ct) < 20:
+        a = time.perf_counter()
+        cpu_fn()
+        ct.append(time.perf_counter() - a)
+    line = {
+        "metric": "solves/s", "value": round(args.steps / sec, 2), "unit": "solves/s",
+        "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(1e3 * sec / args.steps, 4), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"{what}, {W}x{H}, {iters} iterations, lam {lam}",
+                   "sensor": f"{W}x{H}", "iterations": iters},
+        "engine": ("temporally blocked tiles k_pd_tile<f64, data term>"
+                   if args.variant != "tgv" else "split TGV half-step kernels"),
+        "e2e": {"value": round(args.steps / sec, 2), "unit": "solves/s",
+                "h2d_bytes_per_step": 8 * H * W * 5, "d2h_bytes_per_step": 8 * H * W,
+                "api": f"paper_1607_06283_b200.{args.variant}_manifold_solve on host arrays"},
+        "gpu_launches": int(launches),
+        "clocks": clocks.summary(),
+        "cpu_baseline": {"value": round(len(ct) / sum(ct), 4), "unit": "solves/s", "cores": 1,
+                         "kind": "port", "sample": f"{len(ct)} solves, C port (oracle/)"},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="C2", choices=sorted(CONFIGS))
+    ap.add_argument("--config", default="C3", choices=sorted(CONFIGS))
     ap.add_argument("--precision", default="f64", choices=["f64", "f32"])
-    ap.add_argument("--engine", default="auto",
-                    choices=["auto", "streaming", "resident", "resident_gmem", "resident_reg"])
+    ap.add_argument("--engine", default="auto", choices=["auto", "streaming", "resident"])
+    ap.add_argument("--variant", default=None, choices=sorted(VARIANTS),
+                    help="operator-level solve with another data term / regulariser")
+    ap.add_argument("--bands", type=int, default=0,
+                    help="split the sensor in N row bands over the visible GPUs (C5)")
     ap.add_argument("--cpu-budget", type=float, default=12.0)
+    ap.add_argument("--numpy-budget", type=float, default=20.0)
+    ap.add_argument("--ref-budget", type=float, default=240.0,
+                    help="--impl reference: stop after this many seconds of packets")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")
     if args.impl == "reference":
         return run_reference(args)
+    if args.variant:
+        return run_variant(args)
+    if args.bands:
+        return run_bands(args)
     return run_gpu(args)
 
 

@@ -50,12 +50,9 @@ typedef enum { EVR_PREC_F64 = 0, EVR_PREC_F32 = 1 } evr_precision;
 typedef enum {
     EVR_ENGINE_AUTO = 0,      /* shared-memory resident for small sensors (<= 2 rows
                                  per SM), else streaming */
-    EVR_ENGINE_STREAMING = 1, /* one launch per half-step, fields in HBM/L2 */
-    EVR_ENGINE_RESIDENT = 2,  /* persistent kernel, row bands in shared memory */
-    EVR_ENGINE_RESIDENT_GMEM = 3, /* persistent kernel, band frames in L2/HBM
-                                     (on request only) */
-    EVR_ENGINE_RESIDENT_REG = 4   /* float32 persistent kernel, per-pixel state in
-                                     registers (on request; RESIDENT falls back to it) */
+    EVR_ENGINE_STREAMING = 1, /* fused list: temporally blocked tiles in HBM/L2 */
+    EVR_ENGINE_RESIDENT = 2   /* persistent kernel, row bands on chip (registers +
+                                 shared memory) */
 } evr_engine;
 
 /* One camera event: events.py:35-43 Event(x, y, polarity, timestamp).
@@ -81,10 +78,13 @@ typedef struct {
     double c_pos, c_neg;
 } evr_config;
 
-/* SolveResult.iterations / .rel_change (solve.py:81-85). */
+/* SolveResult.iterations / .rel_change (solve.py:81-85).  packet_ms: the
+ * packet's device time from the start of its event upload to the end of its
+ * frame download, filled by evr_frame_wait (the frame pipeline's analogue of
+ * run_stream's per-packet solve_ms, pipeline.py:239-249); 0 elsewhere. */
 typedef struct {
     int32_t iterations;
-    int32_t _pad;
+    float packet_ms;
     double rel_change;
 } evr_solve_info;
 
@@ -154,6 +154,14 @@ int evr_get_frame_async(evr_ctx *ctx, double *u_out);
  * launch per iteration, 2..4 = tiles, 0 = the EVR_TILE_K default).
  * Results are bit-identical for every k; this is a performance knob. */
 int evr_set_tile_k(evr_ctx *ctx, int k);
+/* Measurement hook (bench.py's roofline): times `reps` back-to-back launches
+ * of the streaming list's iteration kernel -- which = 0 the primal-dual tile
+ * (solve.py:233-258), 1 the TV-L1 tile (surface.py:167-193) -- on the
+ * context stream with CUDA events, on the packed state the last packet left
+ * (scratch: the next packet re-packs from the state planes).  Whole-sensor
+ * streaming contexts only. */
+int evr_time_iteration_kernel(evr_ctx *ctx, int which, int reps, float *us_per_launch,
+                              int *iterations_per_launch);
 /* Pipelined read-back for streams (run_stream, pipeline.py:206-276, with
  * packet k+1 computing while frame k travels to the host).  Submit, right
  * after evr_process_packet_async, snapshots this packet's frame u (float64

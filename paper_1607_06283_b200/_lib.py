@@ -28,10 +28,7 @@ PREC_F32 = 1
 ENGINE_AUTO = 0
 ENGINE_STREAMING = 1
 ENGINE_RESIDENT = 2
-ENGINE_RESIDENT_GMEM = 3
-ENGINE_RESIDENT_REG = 4
-ENGINE_NAMES = {ENGINE_AUTO: "auto", ENGINE_STREAMING: "streaming", ENGINE_RESIDENT: "resident",
-                ENGINE_RESIDENT_GMEM: "resident_gmem", ENGINE_RESIDENT_REG: "resident_reg"}
+ENGINE_NAMES = {ENGINE_AUTO: "auto", ENGINE_STREAMING: "streaming", ENGINE_RESIDENT: "resident"}
 
 # evr_event (include/evr.h): 16-byte packed camera event
 EVENT_DTYPE = np.dtype([("t", "<i8"), ("x", "<i4"), ("y", "<i2"), ("polarity", "<i2")])
@@ -60,7 +57,7 @@ class Config(ctypes.Structure):
 
 
 class SolveInfo(ctypes.Structure):
-    _fields_ = [("iterations", ctypes.c_int32), ("_pad", ctypes.c_int32),
+    _fields_ = [("iterations", ctypes.c_int32), ("packet_ms", ctypes.c_float),
                 ("rel_change", ctypes.c_double)]
 
 
@@ -98,6 +95,7 @@ _SIGNATURES = {
     "evr_get_frame_async": ([_P, _P], _i32),
     "evr_frame_submit": ([_P, _P, _P], _i32),
     "evr_set_tile_k": ([_P, _i32], _i32),
+    "evr_time_iteration_kernel": ([_P, _i32, _i32, _P, _P], _i32),
     "evr_frame_wait": ([_P, _i64, _P], _i32),
     "evr_host_alloc": ([ctypes.c_size_t, _P], _i32),
     "evr_host_free": ([_P], _i32),

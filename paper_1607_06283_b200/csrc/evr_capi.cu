@@ -21,7 +21,6 @@
 #include "evr_kernels.cuh"
 #include "evr_tile.cuh"
 #include "evr_resident.cuh"
-#include "evr_resident_reg.cuh"
 #include "evr_resident_col.cuh"
 
 using namespace evr;
@@ -65,6 +64,7 @@ struct evr_ctx {
   double* aos_b = nullptr;
   double* part = nullptr;   // reduction partials
   unsigned* rticket = nullptr;  // k_relchange's last-CTA ticket
+  int* d_stop = nullptr;         // fused list, convergence_tol > 0: the stop flag
   double* d_scalar = nullptr;
   int* d_err = nullptr;
   evr_solve_info* d_info = nullptr;
@@ -85,11 +85,11 @@ struct evr_ctx {
   // resident engine plan + buffers
   int r_nb = 0, r_R = 0, r_nt = 0, r_ms = 0;
   size_t r_smem = 0, r_frame = 0;
-  void* d_frames = nullptr;               // PLANES_GMEM per-CTA plane frames
   void* d_pack = nullptr;                 // packed state of the fused streaming list
   unsigned long long* d_flags = nullptr;  // per-CTA progress words
   void* d_xchg = nullptr;                 // boundary-row ping-pong buffer
   unsigned* d_ticket = nullptr;
+  unsigned long long* d_rx = nullptr;     // k_resident_col: per-iteration rel_change partials
   int* d_perm = nullptr;                  // k_resident_col: band of each CTA (SM order)
   unsigned long long* d_trace = nullptr;  // optional resident phase timeline
   // band geometry: local plane rows [0, H) are global rows row0 + [0, H);
@@ -110,6 +110,8 @@ struct evr_ctx {
   double* fr_host[kFrameSlots] = {};
   cudaEvent_t fr_ready[kFrameSlots] = {};
   cudaEvent_t fr_done[kFrameSlots] = {};
+  cudaEvent_t pk_t0[kFrameSlots] = {};    // packet start (before its H2D), timing the frame pipeline
+  int64_t pk_seq[kFrameSlots] = {-1, -1, -1, -1};  // the ticket whose start pk_t0 holds
   int64_t fr_ticket[kFrameSlots] = {-1, -1, -1, -1};
   int64_t fr_next = 0;
   int* h_err = nullptr;  // pinned error-flag read-back of evr_synchronize
@@ -236,11 +238,14 @@ std::vector<Step> packet_steps(const evr_config& g, int which, bool fused, int t
   if (which != 0) {
     if (fused) v.push_back({ST_PACK, 0});
     int b = 0;
+    // convergence_tol > 0 (fused list): one march launch per iteration, each
+    // followed by its rel_change, all no-ops after the stop (device flag)
+    const bool early = fused && g.convergence_tol > 0;
     for (int k = 0; k < M;) {
       if (fused) {
-        const int kk = std::max(1, std::min(tk, M - 1 - k));
+        const int kk = early ? 1 : std::max(1, std::min(tk, M - 1 - k));
         v.push_back({ST_PDF, k, b, kk});
-        if (k == M - 1) v.push_back({ST_RELF, k, b});
+        if (k == M - 1 || early) v.push_back({ST_RELF, k, b});
         b ^= 1;
         k += kk;
       } else {
@@ -355,11 +360,13 @@ void launch_pdl(void (*k)(KArgs...), unsigned grid, unsigned block, cudaStream_t
 }
 
 template <class T>
-void relchange(evr_ctx* ctx, const T* un, const T* u, int iterations, int stride = 1) {
+void relchange(evr_ctx* ctx, const T* un, const T* u, int iterations, int stride = 1,
+               bool early_stop = false) {
   const int nb = red_blocks(ctx->own_n());
   launch_pdl(k_relchange<T, kNT>, nb, kNT, ctx->stream, un + ctx->own_off() * stride,
              u + ctx->own_off() * stride, ctx->own_n(), ctx->part, stride, ctx->rticket,
-             ctx->d_info, iterations, ctx->d_scalar + 2);
+             ctx->d_info, iterations, ctx->d_scalar + 2, early_stop ? ctx->cfg.convergence_tol : 0.0,
+             early_stop ? ctx->d_stop : nullptr);
 }
 
 // temporally blocked tiles (evr_tile.cuh): a CTA of G warps covers 32 x
@@ -493,21 +500,24 @@ int launch_tv_tile(evr_ctx* ctx, int K, const MarchRows<Q4<T>>& in, const MarchR
     tv_tile_shape<T, false>(ctx, K, in, f0, out, sigma, tau, shrink);
   return 1;
 }
-template <class T, int RPT, bool B, class M>
-void pd_tile_rpt(evr_ctx* ctx, int K, const MarchRows<Q4<T>>& in, const M& m, Q4<T>* out) {
+// step: tau = sigma for operator solves (no context config); < 0 = the config's
+template <class T, int RPT, bool B, class M, int DT = DT_KL>
+void pd_tile_rpt(evr_ctx* ctx, int K, const MarchRows<Q4<T>>& in, const M& m, Q4<T>* out,
+                 double step = -1.0) {
   constexpr int G = TileShape<T>::G, MB = TileShape<T>::MINB;
   const evr_config& g = ctx->cfg;
   const int H = ctx->Htot, W = ctx->W;
   cudaStream_t s = ctx->stream;
-  const T tau = (T)g.tau, sigma = (T)g.sigma, lo = (T)g.u_min, hi = (T)g.u_max;
+  const T tau = (T)(step < 0 ? g.tau : step), sigma = (T)(step < 0 ? g.sigma : step);
+  const T lo = (T)g.u_min, hi = (T)g.u_max;
   if (K == 2)
-    launch_pdl2(k_pd_tile<T, 2, RPT, G, MB, M, B>, tile_grid<T, 2, RPT>(ctx), 32 * G, s, in, m,
+    launch_pdl2(k_pd_tile<T, 2, RPT, G, MB, M, B, DT>, tile_grid<T, 2, RPT>(ctx), 32 * G, s, in, m,
                 out, H, W, tau, sigma, lo, hi);
   else if (K == 3)
-    launch_pdl2(k_pd_tile<T, 3, RPT, G, MB, M, B>, tile_grid<T, 3, RPT>(ctx), 32 * G, s, in, m,
+    launch_pdl2(k_pd_tile<T, 3, RPT, G, MB, M, B, DT>, tile_grid<T, 3, RPT>(ctx), 32 * G, s, in, m,
                 out, H, W, tau, sigma, lo, hi);
   else
-    launch_pdl2(k_pd_tile<T, 4, RPT, G, MB, M, B>, tile_grid<T, 4, RPT>(ctx), 32 * G, s, in, m,
+    launch_pdl2(k_pd_tile<T, 4, RPT, G, MB, M, B, DT>, tile_grid<T, 4, RPT>(ctx), 32 * G, s, in, m,
                 out, H, W, tau, sigma, lo, hi);
 }
 template <class T, bool B, class M>
@@ -574,7 +584,7 @@ template <class T> int launch_step(evr_ctx* ctx, const Step& st) {
       return 1;
     case ST_REL:
       relchange<T>(ctx, bufs[(st.it + 1) & 1], bufs[st.it & 1], st.it + 1);
-      return 2;
+      return 1;
     case ST_PDD:
       k_pd_dual<T><<<grid_geo(own), block2d(), 0, s>>>(
           ctx->fld<T>(F_V), ctx->fld<T>(F_P1), ctx->fld<T>(F_P2), ctx->fld<T>(F_P3),
@@ -613,6 +623,7 @@ template <class T> int launch_step(evr_ctx* ctx, const Step& st) {
       return 1;
     case ST_PACK: {
       const Packed<T> P = packed<T>(ctx);
+      if (g.convergence_tol > 0) CK(cudaMemsetAsync(ctx->d_stop, 0, sizeof(int), s));
       constexpr int E = sizeof(T) == 8 ? 2 : 1;
       k_pack_solver<T><<<grid1d(n), kNT, 0, s>>>(
           ctx->fld<T>(F_P1) + off, ctx->fld<T>(F_P2) + off, ctx->fld<T>(F_P3) + off,
@@ -640,23 +651,30 @@ template <class T> int launch_step(evr_ctx* ctx, const Step& st) {
       if (ctx->banded)
         launch_pdl(k_pd_march<T, kMarchRY, MarchDepth<T>::pd, M, true>, march_grid(ctx), kMarchNT,
                    s, in.own, in, m, out, ctx->Htot, ctx->W, (T)g.tau, (T)g.sigma, (T)g.u_min,
-                   (T)g.u_max);
+                   (T)g.u_max, (const int*)nullptr);
       else
         launch_pdl(k_pd_march<T, kMarchRY, MarchDepth<T>::pd, M, false>, march_grid(ctx), kMarchNT,
                    s, in.own, in, m, out, ctx->Htot, ctx->W, (T)g.tau, (T)g.sigma, (T)g.u_min,
-                   (T)g.u_max);
+                   (T)g.u_max, (const int*)(g.convergence_tol > 0 ? ctx->d_stop : nullptr));
       return 1;
     }
     case ST_RELF: {  // u of the last two iterations, the w of the packed quads
       const Packed<T> P = packed<T>(ctx);
-      relchange<T>(ctx, &P.pd[st.buf ^ 1]->w, &P.pd[st.buf]->w, st.it + 1, 4);
-      return 2;
+      relchange<T>(ctx, &P.pd[st.buf ^ 1]->w, &P.pd[st.buf]->w, st.it + 1, 4,
+                   g.convergence_tol > 0 && !ctx->banded);
+      return 1;
     }
     case ST_UNPACK:  // st.buf = the set holding the last iteration
-      k_unpack_solver<T><<<grid1d(n), kNT, 0, s>>>(packed<T>(ctx).pd[st.buf] + off,
-                                                   ctx->fld<T>(F_P1) + off, ctx->fld<T>(F_P2) + off,
-                                                   ctx->fld<T>(F_P3) + off, ctx->fld<T>(F_U) + off,
-                                                   ctx->f + off, n);
+      if (g.convergence_tol > 0)  // the set of the last executed iteration (device count)
+        k_unpack_solver<T><<<grid1d(n), kNT, 0, s>>>(
+            packed<T>(ctx).pd[0] + off, ctx->fld<T>(F_P1) + off, ctx->fld<T>(F_P2) + off,
+            ctx->fld<T>(F_P3) + off, ctx->fld<T>(F_U) + off, ctx->f + off, n,
+            packed<T>(ctx).pd[1] + off, ctx->d_info);
+      else
+        k_unpack_solver<T><<<grid1d(n), kNT, 0, s>>>(packed<T>(ctx).pd[st.buf] + off,
+                                                     ctx->fld<T>(F_P1) + off, ctx->fld<T>(F_P2) + off,
+                                                     ctx->fld<T>(F_P3) + off, ctx->fld<T>(F_U) + off,
+                                                     ctx->f + off, n);
       return 1;
   }
   return 0;
@@ -687,9 +705,6 @@ template <class T> const ResidentKernel<T>* resident_pick(int W, int ms) {
       {128, PLANES_SMEM, k_resident<T, 128, kResidentCH, PLANES_SMEM>},
       {384, PLANES_SMEM, k_resident<T, 384, kResidentCH, PLANES_SMEM>},
       {512, PLANES_SMEM, k_resident<T, 512, kResidentCH, PLANES_SMEM>},
-      {128, PLANES_GMEM, k_resident<T, 128, kResidentCH, PLANES_GMEM>},
-      {384, PLANES_GMEM, k_resident<T, 384, kResidentCH, PLANES_GMEM>},
-      {512, PLANES_GMEM, k_resident<T, 512, kResidentCH, PLANES_GMEM>},
   };
   const int nt = W <= 128 ? 128 : W <= 384 ? 384 : 512;
   for (const auto& k : table)
@@ -720,30 +735,11 @@ template <class T> const ResidentColKernel<T>* resident_col_pick(int W, int R) {
   return nullptr;
 }
 
-// float32 register-state variant (evr_resident_reg.cuh): (NT, CS, RM)
-// shapes, a thread per CS columns of a W <= CS*NT sensor, bands <= RM rows
-struct ResidentRegKernel {
-  int nt, cs, rm;
-  void (*fn)(ResArgs<float>);
-};
-const ResidentRegKernel* resident_reg_pick(int W, int R) {
-  static const ResidentRegKernel table[] = {
-      {640, 1, 2, k_resident_reg<640, 1, 2>}, {640, 1, 4, k_resident_reg<640, 1, 4>},
-      {640, 2, 2, k_resident_reg<640, 2, 2>}, {640, 2, 5, k_resident_reg<640, 2, 5>},
-  };
-  for (const auto& k : table)
-    if (W <= k.cs * k.nt && (k.cs == 1 || W > (k.cs - 1) * k.nt) && R <= k.rm) return &k;
-  return nullptr;
-}
-
-// Band decomposition: one CTA per SM at most, equal band heights R.  The
-// frame goes to shared memory when it fits; float32 sensors too large for
-// that keep the per-pixel state in registers (PLANES_REG); global-memory
-// frames only on request.
-// where a plan may put the per-CTA frames
-enum PlanWant { WANT_SMEM, WANT_SMEM_OR_REG, WANT_REG, WANT_GMEM };
-
-template <class T> bool resident_plan(evr_ctx* ctx, PlanWant want) {
+// Band decomposition: one CTA per SM at most, equal band heights R: the
+// column-per-thread kernel when W <= 512, else the plane-frame kernel with
+// its frame in shared memory (nothing else: an engine that does not fit
+// hands the sensor to the streaming list).
+template <class T> bool resident_plan(evr_ctx* ctx) {
   int sms = 0, optin = 0;
   if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device) != cudaSuccess ||
       cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device) !=
@@ -756,29 +752,17 @@ template <class T> bool resident_plan(evr_ctx* ctx, PlanWant want) {
   const int nt = W <= 128 ? 128 : W <= 384 ? 384 : 512;
   const size_t static_smem = sizeof(IngestShared<512>) + 64 * sizeof(double) + 64;
   const bool smem_fits = frame + static_smem + 1024 <= (size_t)optin;
-  const ResidentRegKernel* rk = std::is_same<T, float>::value ? resident_reg_pick(W, R) : nullptr;
-  const size_t rframe = resident_reg_frame_bytes(R, W);
-  const bool reg_fits =
-      rk && rframe + sizeof(IngestShared<640>) + 64 * sizeof(double) + 1024 <= (size_t)optin;
   const ResidentColKernel<T>* ck = resident_col_pick<T>(W, R);
   const size_t csmem = resident_col_smem<T>(R, W);
   int ms, nt_used = nt;
   size_t smem;
-  if (want != WANT_GMEM && want != WANT_REG && ck &&
-      csmem + sizeof(IngestShared<512>) + 64 * sizeof(double) + 1024 <= (size_t)optin) {
+  if (ck && csmem + sizeof(IngestShared<512>) + 64 * sizeof(double) + 1024 <= (size_t)optin) {
     ms = PLANES_COL;
     smem = csmem;
     nt_used = ck->nt;
-  } else if (want == WANT_GMEM) {
-    ms = PLANES_GMEM;
-    smem = 0;
-  } else if (want != WANT_REG && smem_fits) {
+  } else if (smem_fits) {
     ms = PLANES_SMEM;
     smem = frame;
-  } else if (want != WANT_SMEM && reg_fits) {
-    ms = PLANES_REG;
-    smem = rframe;
-    nt_used = rk->nt;
   } else {
     return false;
   }
@@ -849,11 +833,12 @@ template <class T> int resident_alloc(evr_ctx* ctx) {
   cudaFree(ctx->d_flags);
   cudaFree(ctx->d_xchg);
   cudaFree(ctx->d_ticket);
-  cudaFree(ctx->d_frames);
+  cudaFree(ctx->d_rx);
+  cudaFree(ctx->d_rx);
+  ctx->d_rx = nullptr;
   ctx->d_flags = nullptr;
   ctx->d_xchg = nullptr;
   ctx->d_ticket = nullptr;
-  ctx->d_frames = nullptr;
   CK(cudaMalloc(&ctx->d_flags, sizeof(unsigned long long) * ctx->r_nb));
   CK(cudaMemset(ctx->d_flags, 0, sizeof(unsigned long long) * ctx->r_nb));
   // 4 slots per column: the plane-frame kernel uses 3, k_resident_col 4
@@ -862,12 +847,10 @@ template <class T> int resident_alloc(evr_ctx* ctx) {
   CK(cudaMemset(ctx->d_xchg, 0, xbytes));  // no stale tag can match a live one
   CK(cudaMalloc(&ctx->d_ticket, sizeof(unsigned)));
   CK(cudaMemset(ctx->d_ticket, 0, sizeof(unsigned)));
-  if (ctx->r_ms == PLANES_GMEM) CK(cudaMalloc(&ctx->d_frames, ctx->r_frame * ctx->r_nb));
+  CK(cudaMalloc(&ctx->d_rx, sizeof(unsigned long long) * 8 * ctx->r_nb));
+  CK(cudaMemset(ctx->d_rx, 0, sizeof(unsigned long long) * 8 * ctx->r_nb));
   const void* fn = nullptr;
-  if (ctx->r_ms == PLANES_REG) {
-    const ResidentRegKernel* rk = resident_reg_pick(ctx->W, ctx->r_R);
-    fn = rk ? (const void*)rk->fn : nullptr;
-  } else if (ctx->r_ms == PLANES_COL) {
+  if (ctx->r_ms == PLANES_COL) {
     const ResidentColKernel<T>* ck = resident_col_pick<T>(ctx->W, ctx->r_R);
     fn = ck ? (const void*)ck->fn : nullptr;
   } else {
@@ -900,10 +883,12 @@ template <class T> int resident_enqueue(evr_ctx* ctx, int which) {
   a.G = ctx->fld<T>(F_G);
   a.sg = ctx->fld<T>(F_SG);
   a.xchg = reinterpret_cast<T*>(ctx->d_xchg);
-  a.frames = reinterpret_cast<T*>(ctx->d_frames);
+  a.frames = nullptr;
   a.flags = ctx->d_flags;
   a.part = ctx->part;
   a.ticket = ctx->d_ticket;
+  a.rx = ctx->d_rx;
+  a.tol = g.convergence_tol;
   a.info = ctx->d_info;
   a.err = ctx->d_err;
   a.trace = ctx->d_trace;
@@ -940,13 +925,7 @@ template <class T> int resident_enqueue(evr_ctx* ctx, int which) {
   lc.attrs = attr;
   lc.numAttrs = 1;
   cudaError_t e;
-  if (ctx->r_ms == PLANES_REG) {
-    if constexpr (std::is_same<T, float>::value) {
-      e = cudaLaunchKernelEx(&lc, resident_reg_pick(ctx->W, ctx->r_R)->fn, a);
-    } else {
-      return fail(ctx, EVR_ERR_UNSUPPORTED, "register-state resident engine is float32 only");
-    }
-  } else if (ctx->r_ms == PLANES_COL) {
+  if (ctx->r_ms == PLANES_COL) {
     e = cudaLaunchKernelEx(&lc, resident_col_pick<T>(ctx->W, ctx->r_R)->fn, a);
   } else {
     e = cudaLaunchKernelEx(&lc, resident_pick<T>(ctx->W, ctx->r_ms)->fn, a);
@@ -1062,7 +1041,13 @@ int stage_device_packet(evr_ctx* ctx, const evr_event* dev, int64_t n, double wi
   return launch_err(ctx, "stage");
 }
 
-bool solve_needs_host_loop(const evr_ctx* ctx) { return ctx->cfg.convergence_tol > 0; }
+// convergence_tol > 0: both engines stop on the device (the column resident
+// kernel folds rel_change every iteration; the fused streaming list runs one
+// march launch + rel_change per iteration behind a device stop flag); only
+// band contexts still drive the iterations from the host
+bool solve_needs_host_loop(const evr_ctx* ctx) {
+  return ctx->cfg.convergence_tol > 0 && ctx->banded;
+}
 
 // Host-driven solve for convergence_tol > 0 and/or traces (solve.py:233-258):
 // rel_change every iteration, early stop, optional energy rows.
@@ -1085,7 +1070,7 @@ int solve_host_loop(evr_ctx* ctx, const evr_config& g, evr_solve_info* info, dou
     ctx->launches += 1;
     if (track || it == g.max_iterations - 1) {
       relchange<T>(ctx, nxt, cur, iterations);
-      ctx->launches += 2;
+      ctx->launches += 1;
     }
     k_pd_dual<T><<<grid_geo(own), block2d(), 0, ctx->stream>>>(
         v, ctx->fld<T>(F_P1), ctx->fld<T>(F_P2), ctx->fld<T>(F_P3), coefs<T>(ctx),
@@ -1251,11 +1236,65 @@ int ensure_frame_slots(evr_ctx* ctx) {
   for (int i = 0; i < kFrameSlots; ++i) {
     CK(cudaMalloc(&ctx->d_fr[i], sizeof(double) * std::max<int64_t>(ctx->own_n(), 1)));
     CK(cudaEventCreateWithFlags(&ctx->fr_ready[i], cudaEventDisableTiming));
-    CK(cudaEventCreateWithFlags(&ctx->fr_done[i], cudaEventDisableTiming));
+    CK(cudaEventCreate(&ctx->fr_done[i]));
+    CK(cudaEventCreate(&ctx->pk_t0[i]));
   }
   CK(cudaMalloc(&ctx->d_rec, sizeof(FrameRec) * kFrameSlots));
   CK(cudaMallocHost(&ctx->h_rec, sizeof(FrameRec) * kFrameSlots));
   return EVR_OK;
+}
+
+// start of the packet whose frame the next evr_frame_submit takes (the
+// frame pipeline's per-packet time: H2D .. solve .. frame D2H)
+int mark_packet_start(evr_ctx* ctx) {
+  int rc;
+  if ((rc = ensure_frame_slots(ctx))) return rc;
+  const int s = (int)(ctx->fr_next % kFrameSlots);
+  if (ctx->fr_ticket[s] >= 0) return EVR_OK;  // slot still in flight: no timing for this one
+  CK(cudaEventRecord(ctx->pk_t0[s], ctx->stream));
+  ctx->pk_seq[s] = ctx->fr_next;
+  return EVR_OK;
+}
+
+// float64 operator solves with the ROF / L1 data terms on the temporally
+// blocked tiles (k_pd_tile<.., DT>, bit-identical to the split
+// k_rof_primal / k_l1_primal + k_pd_dual loop): the planes set up by
+// k_solver_setup are packed once, the iterations run K per launch (a
+// remainder of one merges into the last tile, 3 + 1 -> 4 or 4 + 1 -> 3 + 2),
+// and u comes back from the packed set.  iterations >= 2.  Returns the
+// plane holding u.
+template <int DT>
+double* op_tile_solve(evr_ctx* ctx, int iterations, const double* fslot, double step) {
+  cudaStream_t s = ctx->stream;
+  const int64_t N = ctx->N;
+  const Packed<double> P = packed<double>(ctx);
+  k_pack_solver<double><<<grid1d(N), kNT, 0, s>>>(
+      ctx->fld<double>(F_P1), ctx->fld<double>(F_P2), ctx->fld<double>(F_P3),
+      ctx->fld<double>(F_U), ctx->fld<double>(F_TX), ctx->fld<double>(F_TY), coefs<double>(ctx),
+      ctx->fld<double>(F_SG), ctx->fld<double>(F_BETA), ctx->fld<double>(F_FB), P.pd[0], P.cst, N,
+      fslot);
+  const int tk = std::max(2, ctx_tile_k(ctx));
+  std::vector<int> ks;  // iterations per launch, each in [2, 4] (the built tiles)
+  for (int rem = iterations; rem > 0;) {
+    int kk = std::min(tk, rem);
+    if (rem - kk == 1) kk = kk < 4 ? kk + 1 : kk - 1;
+    ks.push_back(kk);
+    rem -= kk;
+  }
+  int b = 0;
+  const auto cr = march_rows<Q4<double>>(ctx, [](const evr_ctx* c) { return packed<double>(c).cst; }, 2);
+  const MetricPackF64 m{cr.own, cr};
+  for (int kk : ks) {
+    const auto in = march_rows<Q4<double>>(ctx, [b](const evr_ctx* c) { return packed<double>(c).pd[b]; }, 1);
+    pd_tile_rpt<double, TileShape<double>::RPT, false, MetricPackF64, DT>(
+        ctx, kk, in, m, packed<double>(ctx).pd[b ^ 1], step);
+    b ^= 1;
+  }
+  k_unpack_solver<double><<<grid1d(N), kNT, 0, s>>>(P.pd[b], ctx->fld<double>(F_P1),
+                                                    ctx->fld<double>(F_P2), ctx->fld<double>(F_P3),
+                                                    ctx->fld<double>(F_U), ctx->f, N);
+  ctx->launches += 2 + (int64_t)ks.size();
+  return ctx->fld<double>(F_U);
 }
 
 }  // namespace
@@ -1313,6 +1352,8 @@ int evr_create(evr_ctx** out, int device, int height, int width, int precision) 
     CK(cudaMalloc(&ctx->aos_b, sizeof(double) * 3 * N));
     CK(cudaMalloc(&ctx->part, sizeof(double) * 2 * kRedBlocks));
     CK(cudaMalloc(&ctx->rticket, sizeof(unsigned)));
+    CK(cudaMalloc(&ctx->d_stop, sizeof(int)));
+    CK(cudaMemsetAsync(ctx->d_stop, 0, sizeof(int), ctx->stream));
     CK(cudaMemsetAsync(ctx->rticket, 0, sizeof(unsigned), ctx->stream));
     CK(cudaMalloc(&ctx->d_scalar, sizeof(double) * 4));
     CK(cudaMalloc(&ctx->d_err, sizeof(int)));
@@ -1340,6 +1381,7 @@ void evr_destroy(evr_ctx* ctx) {
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   drop_graphs(ctx);
   cudaFree(ctx->slab);
+  cudaFree(ctx->d_stop);
   cudaFree(ctx->d_pack);
   cudaFree(ctx->f);
   cudaFree(ctx->raw);
@@ -1355,7 +1397,6 @@ void evr_destroy(evr_ctx* ctx) {
   cudaFree(ctx->d_xchg);
   cudaFree(ctx->d_ticket);
   cudaFree(ctx->d_perm);
-  cudaFree(ctx->d_frames);
   cudaFree(ctx->d_trace);
   for (int i = 0; i < 2; ++i) {
     if (ctx->h_stage[i]) cudaFreeHost(ctx->h_stage[i]);
@@ -1368,6 +1409,7 @@ void evr_destroy(evr_ctx* ctx) {
     cudaFree(ctx->d_fr[i]);
     if (ctx->fr_ready[i]) cudaEventDestroy(ctx->fr_ready[i]);
     if (ctx->fr_done[i]) cudaEventDestroy(ctx->fr_done[i]);
+    if (ctx->pk_t0[i]) cudaEventDestroy(ctx->pk_t0[i]);
   }
   cudaFree(ctx->d_rec);
   cudaFree(ctx->tgv);
@@ -1389,24 +1431,24 @@ int evr_set_config(evr_ctx* ctx, const evr_config* cfg) {
   ctx->cfg_set = true;
   drop_graphs(ctx);
   ctx->engine = EVR_ENGINE_STREAMING;
-  if (cfg->engine != EVR_ENGINE_STREAMING && cfg->convergence_tol <= 0 && ctx->H >= 2 &&
-      ctx->W >= 2) {
-    // AUTO: the shared-memory resident kernel while each CTA owns at most
+  // tags of the resident exchange are (packet << 16) + step: a packet's
+  // steps must stay below 2^16
+  const bool tags_fit = (int64_t)cfg->denoise_iterations + cfg->max_iterations + 4 < 65536;
+  if (cfg->engine == EVR_ENGINE_RESIDENT && !tags_fit)
+    return fail(ctx, EVR_ERR_UNSUPPORTED, "resident engine: more than 65531 iterations per packet");
+  if (cfg->engine != EVR_ENGINE_STREAMING && tags_fit && ctx->H >= 2 && ctx->W >= 2) {
+    // AUTO: the resident kernel while each CTA owns at most
     // kAutoResidentRows rows, else the fused streaming list (measured on
     // B200, profiles/r01_summary.md: at 640x480 and beyond the streaming
-    // march beats every resident variant).  RESIDENT: shared-memory or
-    // (float32) register frames; the GMEM / REG engines on request only.
-    const PlanWant want = cfg->engine == EVR_ENGINE_RESIDENT_GMEM ? WANT_GMEM
-                          : cfg->engine == EVR_ENGINE_RESIDENT_REG ? WANT_REG
-                          : cfg->engine == EVR_ENGINE_RESIDENT    ? WANT_SMEM_OR_REG
-                                                                  : WANT_SMEM;
-    bool ok = ctx->prec == EVR_PREC_F64 ? resident_plan<double>(ctx, want)
-                                        : resident_plan<float>(ctx, want);
+    // tiles beat every resident variant).  RESIDENT: whenever it fits.
+    bool ok = cfg->engine == EVR_ENGINE_AUTO || cfg->engine == EVR_ENGINE_RESIDENT;
+    if (ok)
+      ok = ctx->prec == EVR_PREC_F64 ? resident_plan<double>(ctx) : resident_plan<float>(ctx);
     if (ok && cfg->engine == EVR_ENGINE_AUTO && ctx->r_R > kAutoResidentRows) ok = false;
+    // the device-side early stop lives in the column kernel only
+    if (ok && cfg->convergence_tol > 0 && ctx->r_ms != PLANES_COL) ok = false;
     if (ok) {
-      ctx->engine = ctx->r_ms == PLANES_GMEM ? EVR_ENGINE_RESIDENT_GMEM
-                    : ctx->r_ms == PLANES_REG ? EVR_ENGINE_RESIDENT_REG
-                                              : EVR_ENGINE_RESIDENT;
+      ctx->engine = EVR_ENGINE_RESIDENT;
       int rc = ctx->prec == EVR_PREC_F64 ? resident_alloc<double>(ctx) : resident_alloc<float>(ctx);
       if (rc) return rc;
     } else if (cfg->engine != EVR_ENGINE_AUTO) {
@@ -1442,10 +1484,7 @@ int evr_engine_detail(evr_ctx* ctx, char* buf, int len) {
       }
     }
   } else {
-    const char* k = ctx->r_ms == PLANES_COL    ? "k_resident_col"
-                    : ctx->r_ms == PLANES_REG  ? "k_resident_reg"
-                    : ctx->r_ms == PLANES_GMEM ? "k_resident(gmem frames)"
-                                               : "k_resident(smem frames)";
+    const char* k = ctx->r_ms == PLANES_COL ? "k_resident_col" : "k_resident(smem frames)";
     snprintf(buf, len, "%s<%s,NT=%d,RB=%d> x%d CTAs, %zu B smem", k, ty, ctx->r_nt, ctx->r_R,
              ctx->r_nb, ctx->r_smem);
   }
@@ -1560,6 +1599,7 @@ int evr_process_packet_async(evr_ctx* ctx, const evr_event* events, int64_t n, d
   if (n <= 0 || !events) return fail(ctx, EVR_ERR_INVALID, "empty packet");
   if (solve_needs_host_loop(ctx))
     return fail(ctx, EVR_ERR_UNSUPPORTED, "convergence_tol > 0 needs evr_process_packet");
+  if ((rc = mark_packet_start(ctx))) return rc;
   if ((rc = stage_host_packet(ctx, events, n, window))) return rc;
   return launch_stage(ctx, 2);
 }
@@ -1572,6 +1612,7 @@ int evr_process_packet_device(evr_ctx* ctx, const evr_event* dev_events, int64_t
   if (n <= 0 || !dev_events) return fail(ctx, EVR_ERR_INVALID, "empty packet");
   if (solve_needs_host_loop(ctx))
     return fail(ctx, EVR_ERR_UNSUPPORTED, "convergence_tol > 0 needs evr_process_packet");
+  if ((rc = mark_packet_start(ctx))) return rc;
   if ((rc = stage_device_packet(ctx, dev_events, n, window))) return rc;
   return launch_stage(ctx, 2);
 }
@@ -1602,6 +1643,41 @@ int evr_set_tile_k(evr_ctx* ctx, int k) {
   CK(cudaStreamSynchronize(ctx->stream));
   ctx->tile_k = k;
   drop_graphs(ctx);
+  return EVR_OK;
+}
+
+int evr_time_iteration_kernel(evr_ctx* ctx, int which, int reps, float* us_per_launch,
+                              int* iterations_per_launch) {
+  CHECK_CTX();
+  if (!us_per_launch || reps < 1 || (which != 0 && which != 1))
+    return fail(ctx, EVR_ERR_INVALID, "bad arguments");
+  int rc;
+  if ((rc = require_config(ctx))) return rc;
+  if (ctx->engine != EVR_ENGINE_STREAMING || ctx->banded || !ctx->d_pack)
+    return fail(ctx, EVR_ERR_UNSUPPORTED, "only the whole-sensor streaming list has iteration kernels");
+  const int tk = ctx_tile_k(ctx);
+  // the packed sets hold the last packet's state: re-running iterations on
+  // them changes nothing the next packet reads (it packs from the planes)
+  Step st{which == 0 ? ST_PDF : ST_TVF, 0, 0, tk};
+  cudaEvent_t e0, e1;
+  CK(cudaEventCreate(&e0));
+  CK(cudaEventCreate(&e1));
+  auto one = [&](int i) {
+    st.buf = i & 1;
+    return ctx->prec == EVR_PREC_F64 ? launch_step<double>(ctx, st) : launch_step<float>(ctx, st);
+  };
+  one(0);
+  CK(cudaEventRecord(e0, ctx->stream));
+  for (int i = 0; i < reps; ++i) one(i + 1);
+  CK(cudaEventRecord(e1, ctx->stream));
+  CK(cudaEventSynchronize(e1));
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, e0, e1);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  if ((rc = launch_err(ctx, "time_iteration_kernel"))) return rc;
+  *us_per_launch = 1000.f * ms / reps;
+  if (iterations_per_launch) *iterations_per_launch = tk;
   return EVR_OK;
 }
 
@@ -1649,7 +1725,12 @@ int evr_frame_wait(evr_ctx* ctx, int64_t ticket, evr_solve_info* info) {
   ctx->fr_ticket[s] = -1;
   ctx->fr_host[s] = nullptr;
   const FrameRec r = ctx->h_rec[s];
-  if (info) *info = r.info;
+  if (info) {
+    *info = r.info;
+    info->packet_ms = 0.0f;
+    if (ctx->pk_seq[s] == ticket) cudaEventElapsedTime(&info->packet_ms, ctx->pk_t0[s], ctx->fr_done[s]);
+  }
+  ctx->pk_seq[s] = -1;
   if (r.err)
     return fail(ctx, EVR_ERR_RANGE, "a device-side event lay outside the %dx%d sensor", ctx->W,
                 ctx->H);
@@ -2013,6 +2094,12 @@ int evr_op_rof_solve(evr_ctx* ctx, const double* f, const double* tx, const doub
   k_solver_setup<double><<<grid1d(N), kNT, 0, s>>>(
       ctx->fld<double>(F_TX), ctx->fld<double>(F_TY), ctx->fld<double>(F_G), ctx->fld<double>(F_SG),
       fdev, coefs<double>(ctx), ctx->fld<double>(F_BETA), ctx->fld<double>(F_FB), N, step * lam, 1);
+  if (iterations >= 2 && !ctx->banded) {  // the tiles (K iterations per launch)
+    double* uo = op_tile_solve<DT_ROF>(ctx, iterations, nullptr, step);
+    ctx->launches += 1;
+    if ((rc = launch_err(ctx, "rof"))) return rc;
+    return d2h_sync(ctx, u_out, uo, B);
+  }
   double* bufs[2] = {ctx->fld<double>(F_U), ctx->fld<double>(F_UN)};
   for (int it = 0; it < iterations; ++it) {
     double* cur = bufs[it & 1];
@@ -2048,6 +2135,12 @@ int evr_op_l1_solve(evr_ctx* ctx, const double* f, const double* tx, const doubl
   k_solver_setup<double><<<grid1d(N), kNT, 0, s>>>(
       ctx->fld<double>(F_TX), ctx->fld<double>(F_TY), ctx->fld<double>(F_G), ctx->fld<double>(F_SG),
       fdev, coefs<double>(ctx), ctx->fld<double>(F_BETA), ctx->fld<double>(F_FB), N, step * lam, 0);
+  if (iterations >= 2 && !ctx->banded) {  // the tiles: beta = (tau lam) sqrtG, f in the last slot
+    double* uo = op_tile_solve<DT_L1>(ctx, iterations, fdev, step);
+    ctx->launches += 1;
+    if ((rc = launch_err(ctx, "l1"))) return rc;
+    return d2h_sync(ctx, u_out, uo, B);
+  }
   double* bufs[2] = {ctx->fld<double>(F_U), ctx->fld<double>(F_UN)};
   for (int it = 0; it < iterations; ++it) {
     double* v = ctx->fld<double>(F_V);

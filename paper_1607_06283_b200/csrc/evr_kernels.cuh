@@ -588,10 +588,12 @@ template <> struct MetricPack<double> { using type = MetricPackF64; };
 template <class T, int RY, int D, class M, bool BANDED>
 __global__ void __launch_bounds__(128)
 k_pd_march(const Q4<T>* __restrict__ own, const MarchRows<Q4<T>> in, M m,
-           Q4<T>* __restrict__ out, int H, int W, T tau, T sigma, T umin, T umax) {
+           Q4<T>* __restrict__ out, int H, int W, T tau, T sigma, T umin, T umax,
+           const int* __restrict__ stop = nullptr) {
   const int y1 = BANDED ? in.y1 : H;  // end of the own rows (global)
   const Strip s = strip_of<RY>(BANDED ? in.y0 : 0, y1, W);
   pdl_wait_and_release();
+  if (stop && *stop) return;  // convergence_tol reached (k_relchange): the iteration is skipped
   if (!s.live) return;  // whole warp
   const int j = s.j;
   const int jc = min(max(j, 0), W - 1);
@@ -677,15 +679,17 @@ __global__ void k_pack_solver(const T* __restrict__ p1, const T* __restrict__ p2
                               const T* __restrict__ tx, const T* __restrict__ ty,
                               CoefPlanes<T> c, const T* __restrict__ sg,
                               const T* __restrict__ beta, const T* __restrict__ fb,
-                              Q4<T>* __restrict__ st, Q4<T>* __restrict__ cst, int64_t N) {
+                              Q4<T>* __restrict__ st, Q4<T>* __restrict__ cst, int64_t N,
+                              const double* __restrict__ fslot = nullptr) {
   const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= N) return;
   st[k] = Q4<T>{p1[k], p2[k], p3[k], u[k]};
   if constexpr (sizeof(T) == 4) {
     cst[k] = Q4<T>{tx[k], ty[k], fb[k], T(0)};
   } else {
+    // fslot: the L1 data term keeps f itself in the last slot
     cst[2 * k] = Q4<T>{c.a11[k], c.a12[k], c.a22[k], c.a31[k]};
-    cst[2 * k + 1] = Q4<T>{c.a32[k], sg[k], beta[k], fb[k]};
+    cst[2 * k + 1] = Q4<T>{c.a32[k], sg[k], beta[k], fslot ? (T)fslot[k] : fb[k]};
   }
 }
 
@@ -693,10 +697,14 @@ __global__ void k_pack_solver(const T* __restrict__ p1, const T* __restrict__ p2
 template <class T>
 __global__ void k_unpack_solver(const Q4<T>* __restrict__ st, T* __restrict__ p1,
                                 T* __restrict__ p2, T* __restrict__ p3, T* __restrict__ u,
-                                double* __restrict__ f, int64_t N) {
+                                double* __restrict__ f, int64_t N,
+                                const Q4<T>* __restrict__ st_odd = nullptr,
+                                const evr_solve_info* __restrict__ info = nullptr) {
   const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= N) return;
-  const Q4<T> q = st[k];
+  // early stop: the set holding the last executed iteration is decided on
+  // the device (iterations n -> set n & 1)
+  const Q4<T> q = (st_odd && (info->iterations & 1)) ? st_odd[k] : st[k];
   p1[k] = q.x;
   p2[k] = q.y;
   p3[k] = q.z;
@@ -727,10 +735,16 @@ __device__ __forceinline__ double block_sum(double x, double* sh) {
 template <class T, int NT>
 __global__ void __launch_bounds__(NT)
 k_relchange(const T* __restrict__ un, const T* __restrict__ u, int64_t N, double* part,
-            int stride, unsigned* ticket, evr_solve_info* info, int iterations, double* sums) {
+            int stride, unsigned* ticket, evr_solve_info* info, int iterations, double* sums,
+            double tol = 0.0, int* stop = nullptr) {
   __shared__ double sh[NT / 32];
   __shared__ bool last;
   pdl_wait_and_release();
+  // early stop (solve.py:257-258): once an iteration's rel_change fell below
+  // tol, the remaining iterations and their rel_change launches are no-ops
+  // (every CTA reads the flag before the last CTA of the stopping launch
+  // can write it)
+  if (stop && *stop) return;
   double d = 0.0, o = 0.0;
   for (int64_t k = (int64_t)blockIdx.x * NT + threadIdx.x; k < N; k += (int64_t)gridDim.x * NT) {
     const double a = (double)un[k * stride], b = (double)u[k * stride];
@@ -759,11 +773,13 @@ k_relchange(const T* __restrict__ un, const T* __restrict__ u, int64_t N, double
   o = block_sum<NT>(o, sh);
   if (threadIdx.x == 0) {
     const double den = sqrt(o);
-    info->rel_change = sqrt(d) / (den > 1e-30 ? den : 1e-30);
+    const double rel = sqrt(d) / (den > 1e-30 ? den : 1e-30);
+    info->rel_change = rel;
     info->iterations = iterations;
     sums[0] = d;  // evr_group folds the bands' sums
     sums[1] = o;
     *ticket = 0u;
+    if (stop && rel < tol) *stop = 1;
   }
 }
 

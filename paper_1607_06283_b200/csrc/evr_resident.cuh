@@ -4,10 +4,9 @@
 // Decomposition.  CTA b of a cooperative grid (<= 1 CTA per SM) owns the
 // row band [r0, r1) of the sensor (full width, equal band heights).  Every
 // per-pixel field of the band -- plus one halo row above (r0-1) and one
-// below (r1) -- lives in a private frame of planes: in shared memory when
-// the band fits (PLANES_SMEM), otherwise in a per-CTA slice of global
-// memory that stays L1/L2-resident (PLANES_GMEM).  Global memory outside the
-// frame is touched only to load the state at the start, to exchange two
+// below (r1) -- lives in a private frame of planes in shared memory
+// (PLANES_SMEM; the global-memory frame form is retired, `frames` stays
+// unused).  Global memory outside the frame is touched only to load the state at the start, to exchange two
 // boundary rows per iteration, and to write the state back at the end.
 //
 // Thread mapping.  Thread t owns sensor column(s) j = t, t+NT, ... and walks
@@ -66,6 +65,8 @@ template <class T> struct ResArgs {
   int* err;
   unsigned long long* trace;     // optional [nb][256] phase timestamps (ns)
   const int* perm;               // k_resident_col: band of CTA blockIdx.x (null = identity)
+  unsigned long long* rx;        // k_resident_col, tol > 0: tagged rel_change partials [2][nb][4]
+  double tol;                    // convergence_tol (k_resident_col: > 0 = early stop on device)
   int H, W, nb, R;
   int tv_iters, pd_iters, manifold;
   double t_scale, c_pos, c_neg, u_min, u_max;

@@ -445,9 +445,43 @@ __global__ void __launch_bounds__(NT, 1) k_resident_col(const ResArgs<T> a) {
     v[r] = T(0);
   }
   mark();
+  // convergence_tol > 0 (solve.py:246-258): rel_change of every iteration,
+  // folded on the device -- each CTA publishes its partial sums after the
+  // primal step as tagged words, runs the dual step, then reads all the
+  // bands' partials and folds them in band order (the same bits in every
+  // CTA, so every band takes the same stop decision after the same dual)
+  const bool track = a.tol > 0.0;
+  int iters_done = a.pd_iters;
+  double rel_track = 0.0;
+  __shared__ double rel_sh;
+  auto fold_rel = [&](int it) {
+    const unsigned want = tag_base + (unsigned)it;
+    const unsigned long long* slot = a.rx + (size_t)(it & 1) * a.nb * 4;
+    double d = 0.0, o = 0.0;
+    for (int k = tid; k < a.nb; k += NT) {
+      unsigned long long w[4];
+      bool ready;
+      do {
+        ld_v4(slot + (size_t)k * 4, w);
+        ready = (unsigned)(w[0] >> 32) == want && (unsigned)(w[1] >> 32) == want &&
+                (unsigned)(w[2] >> 32) == want && (unsigned)(w[3] >> 32) == want;
+      } while (!ready);
+      d += LLWords<double>::unpack(w);
+      o += LLWords<double>::unpack(w + 2);
+    }
+    d = block_sum<NT>(d, red);
+    o = block_sum<NT>(o, red);
+    if (tid == 0) {
+      const double den = sqrt(o);
+      rel_sh = sqrt(d) / (den > 1e-30 ? den : 1e-30);
+    }
+    __syncthreads();
+    return rel_sh;
+  };
   double rd = 0.0, ro = 0.0;
   for (int it = 0; it < a.pd_iters; ++it) {
     const bool last = it == a.pd_iters - 1;
+    if (track) rd = ro = 0.0;
     if (it > 0) {  // p of the previous step on the halo rows (+ their q)
       T h[2][3];
       ll_fetch(step, 3, h);
@@ -490,7 +524,7 @@ __global__ void __launch_bounds__(NT, 1) k_resident_col(const ResArgs<T> a) {
         const T uk = u[r];
         v[r] = Arith<T>::mad(nu[r], T(2), -uk);
         u[r] = nu[r];
-        if (last && r <= Rb && col) {
+        if ((last || track) && r <= Rb && col) {
           const double e = (double)nu[r] - (double)uk;
           rd += e * e;
           ro += (double)uk * (double)uk;
@@ -499,6 +533,16 @@ __global__ void __launch_bounds__(NT, 1) k_resident_col(const ResArgs<T> a) {
       }
     }
     mark();
+    if (track) {  // this band's partials of iteration it (block_sum syncs the CTA)
+      const double sd = block_sum<NT>(rd, red);
+      const double so = block_sum<NT>(ro, red);
+      if (tid == 0) {
+        unsigned long long w[4];
+        LLWords<double>::pack(sd, tag_base + (unsigned)it, w);
+        LLWords<double>::pack(so, tag_base + (unsigned)it, w + 2);
+        st_v4(a.rx + ((size_t)(it & 1) * a.nb + b) * 4, w);
+      }
+    }
     __syncthreads();
     mark();
     // dual ascent + ball projection (solve.py:170-201); boundary rows go out
@@ -549,9 +593,16 @@ __global__ void __launch_bounds__(NT, 1) k_resident_col(const ResArgs<T> a) {
       }
     }
     mark();
+    if (track) {
+      rel_track = fold_rel(it);
+      if (rel_track < a.tol) {  // solve.py:257-258, after the dual step
+        iters_done = it + 1;
+        break;
+      }
+    }
     if (!last) ++step;
   }
-  if (a.pd_iters < 2) {
+  if (iters_done < 2) {
     // neighbours may still be loading our rows of u / p as halos
     flag_publish(s_met + 1);
     flag_wait(has_up ? b - 1 : b, has_dn ? b + 1 : b, s_met + 1);
@@ -573,6 +624,14 @@ __global__ void __launch_bounds__(NT, 1) k_resident_col(const ResArgs<T> a) {
     }
   }
 
+  if (track) {  // every CTA holds the folded rel_change of the last iteration
+    if (b == 0 && tid == 0) {
+      a.info->rel_change = rel_track;
+      a.info->iterations = iters_done;
+    }
+    mark();
+    return;
+  }
   // rel_change = |u+ - u| / max(|u|, 1e-30) (solve.py:246-249): fixed-order
   // block tree, per-CTA partials, last CTA folds them in index order
   const double sd = block_sum<NT>(rd, red);

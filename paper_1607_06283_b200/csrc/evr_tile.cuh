@@ -182,8 +182,12 @@ k_tv_tile(const MarchRows<Q4<T>> in, const MarchRows<T> f0, Q4<T>* __restrict__ 
 // divergence, KL prox + over-relaxation, dual ascent + ball projection.
 // The metric constants of the region are loaded once (M: MetricPackF32
 // recomputes the matrix from the slopes, MetricPackF64 reads it) and stay
-// in registers for the K iterations.
-template <class T, int K, int RPT, int G, int MINB, class M, bool BANDED>
+// in registers for the K iterations.  DT, the data term of the primal step
+// (float64 operator solves): 0 = KL (packed slots beta, 4 beta f), 1 = ROF
+// (rof_manifold_solve, solve.py:285-287: slots 1 / (1 + w), w f), 2 = L1
+// (slots w = tau lam sqrtG, f; the soft shrink of k_l1_primal).
+enum : int { DT_KL = 0, DT_ROF = 1, DT_L1 = 2 };
+template <class T, int K, int RPT, int G, int MINB, class M, bool BANDED, int DT = DT_KL>
 __global__ void __launch_bounds__(32 * G, MINB)
 k_pd_tile(const MarchRows<Q4<T>> in, M m, Q4<T>* __restrict__ out, int H, int W, T tau,
           T sigma, T umin, T umax) {
@@ -254,12 +258,18 @@ k_pd_tile(const MarchRows<Q4<T>> in, M m, Q4<T>* __restrict__ out, int H, int W,
           const T qxl = __shfl_up_sync(0xffffffffu, qx[r], 1);
           const T qyu = r > 0 ? qy[r - 1] : qy_above;
           d[r] = DIV(qx[r], qxl, qy[r], qyu, gi);
-          if constexpr (sizeof(T) == 8)
+          if constexpr (DT == DT_ROF) {
+            nu[r] = rof_primal(d[r], u[r], fb[r], beta[r], tau);  // fb = w f, beta = 1 / (1 + w)
+          } else if constexpr (DT == DT_L1) {
+            const T t1 = Arith<T>::mad(d[r], tau, u[r]);  // fb = f, beta = w
+            nu[r] = t1 - vclip(t1 - fb[r], -beta[r], beta[r]);
+          } else if constexpr (sizeof(T) == 8) {
             nu[r] = kl_primal_fx(d[r], u[r], beta[r], fb[r], tau, umin, umax, slow);
-          else
+          } else {
             nu[r] = kl_primal(d[r], u[r], beta[r], fb[r], tau, umin, umax);
+          }
         }
-        if (sizeof(T) == 8 && slow) {
+        if (DT == DT_KL && sizeof(T) == 8 && slow) {
   #pragma unroll
           for (int r = 0; r < RPT; ++r) nu[r] = kl_primal(d[r], u[r], beta[r], fb[r], tau, umin, umax);
         }

@@ -42,8 +42,6 @@ ADAPTIVE_WINDOW_PACKETS = 10
 _PRECISIONS = {"f64": _lib.PREC_F64, "fp64": _lib.PREC_F64, "float64": _lib.PREC_F64,
                "f32": _lib.PREC_F32, "fp32": _lib.PREC_F32, "float32": _lib.PREC_F32}
 _ENGINES = {"auto": _lib.ENGINE_AUTO, "streaming": _lib.ENGINE_STREAMING,
-            "resident_gmem": _lib.ENGINE_RESIDENT_GMEM,
-            "resident_reg": _lib.ENGINE_RESIDENT_REG,
             "resident": _lib.ENGINE_RESIDENT}
 
 
@@ -284,6 +282,14 @@ def _window(state, now, manifold_cfg):
     return max(float(now - oldest), 1.0)
 
 
+def _device_early_stop(ctx):
+    """convergence_tol > 0 folds rel_change and stops on the device on both
+    engines (the resident column kernel's per-iteration fold; the fused
+    streaming list's stop flag), so such packets take the one-round-trip
+    path too."""
+    return ctx.engine() in ("resident", "streaming")
+
+
 def process_packet_arrays(state, events, manifold_cfg, solver_cfg, thresholds, trace=None,
                           debug_sink=None, want_frame=True):
     """process_packet for an EVENT_DTYPE array (no per-event Python work).
@@ -301,7 +307,8 @@ def process_packet_arrays(state, events, manifold_cfg, solver_cfg, thresholds, t
     now = int(events["t"][-1])
     window = _window(state, now, manifold_cfg) if manifold_cfg.enabled else 1.0
     info = _lib.SolveInfo()
-    split = (debug_sink is not None or trace is not None or solver_cfg.convergence_tol > 0)
+    split = (debug_sink is not None or trace is not None
+             or (solver_cfg.convergence_tol > 0 and not _device_early_stop(ctx)))
     frame = None
     if not split:
         # one round trip: packet, solve and (pinned) frame download on the
@@ -339,7 +346,11 @@ def process_packet_arrays(state, events, manifold_cfg, solver_cfg, thresholds, t
     if frame is None:
         frame = _lib.pinned_empty(state.shape)
         ctx.call("evr_get_frame", _lib.ptr(frame))
-    state._mirror["u"] = frame  # frame aliases state.u, like the reference
+    # frame aliases state.u, like the reference -- as a read-only snapshot:
+    # an in-place edit would not reach the device state, so it raises
+    # instead (assign state.u to change the warm start)
+    frame.flags.writeable = False
+    state._mirror["u"] = frame
     return state, frame, _LazyResult(state, frame, info)
 
 
@@ -353,6 +364,9 @@ class _LazyResult(SolveResult):
         self = super().__new__(cls, frame, None, int(info.iterations), float(info.rel_change))
         self._state = state
         self._frame_index = state.frame_index if frame_index is None else frame_index
+        # device time of the packet (event upload .. frame download), when
+        # it went through the frame pipeline (evr_frame_wait); else None
+        self.packet_ms = float(info.packet_ms) if info.packet_ms > 0 else None
         return self
 
     @property
@@ -376,11 +390,12 @@ def stream_packets(state, packets, manifold_cfg, solver_cfg, thresholds, depth=2
     (decimation: frames not wanted come back as None).  A result's ``p`` is
     readable only while the state still holds that packet's solution (the
     last packet of the stream).  Packets that need the host-driven solve
-    (``convergence_tol > 0``) run one at a time.
+    (``convergence_tol > 0`` on the streaming engine) run one at a time.
     """
     if not 1 <= depth <= 4:
         raise ValueError(f"depth must be in [1, 4], got {depth}")
-    if solver_cfg.convergence_tol > 0:
+    if solver_cfg.convergence_tol > 0 and not _device_early_stop(
+            _prepare(state, manifold_cfg, solver_cfg, thresholds)):
         for pk in packets:
             idx = state.frame_index
             want = want_frames(idx) if callable(want_frames) else want_frames
@@ -397,12 +412,27 @@ def stream_packets(state, packets, manifold_cfg, solver_cfg, thresholds, depth=2
         ticket, frame, idx = pending.popleft()
         info = _lib.SolveInfo()
         ctx.call("evr_frame_wait", ticket, ctypes.byref(info))
-        if frame is not None and not pending and idx == state.frame_index:
-            state._mirror["u"] = frame  # frame aliases state.u, like the reference
+        if frame is not None:
+            frame.flags.writeable = False  # a snapshot (see process_packet_arrays)
+            if not pending and idx == state.frame_index:
+                state._mirror["u"] = frame  # frame aliases state.u, like the reference
         return frame, _LazyResult(state, frame, info, frame_index=idx)
 
+    it = iter(packets)
     try:
-        for pk in packets:
+        while True:
+            try:
+                pk = next(it)
+            except StopIteration:
+                break
+            except BaseException:
+                # the packet source failed (e.g. StreamOrderError from
+                # read_stream): the frames already computed go out first,
+                # as the reference's run_stream delivers frame k before it
+                # reads packet k+1
+                while pending:
+                    yield finish()
+                raise
             events = events_to_array(pk)
             n = len(events)
             if n == 0:  # pipeline.py:151-153, after the packets before it
@@ -428,7 +458,7 @@ def stream_packets(state, packets, manifold_cfg, solver_cfg, thresholds, depth=2
         while pending:
             yield finish()
     finally:
-        while pending:  # generator closed early: release the slots
+        while pending:  # generator closed early (GeneratorExit): release the slots
             try:
                 finish()
             except Exception:
@@ -567,7 +597,11 @@ def _run_pipelined(events, state, policy, manifold_cfg, solver_cfg, thresholds, 
         n = sizes.popleft()
         stats.events_consumed += n
         now = time.perf_counter()
-        ms = (now - t_last) * 1e3  # per-packet share of the pipelined wall time
+        # solve_ms as the reference records it (pipeline.py:239-249): the
+        # packet's own processing time -- here its device time from event
+        # upload to frame download (packets overlap in the pipeline, so
+        # wall-clock deltas would be inter-arrival times instead)
+        ms = result.packet_ms if result.packet_ms is not None else (now - t_last) * 1e3
         t_last = now
         stats.packets += 1
         stats.solve_ms.append(ms)

@@ -247,7 +247,11 @@ def test_frames_are_fresh_pinned_arrays():
     keep = f1.copy()
     _, f2, _ = evr.process_packet(st, ev[30:60], ManifoldConfig(), SolverConfig(), Thresholds())
     assert f1 is not f2 and np.array_equal(f1, keep) and not np.array_equal(f1, f2)
-    assert f2.flags.writeable and f2.flags.c_contiguous and f2.dtype == np.float64
+    assert f2.flags.c_contiguous and f2.dtype == np.float64
+    # a read-only snapshot: an in-place edit would not reach the device state
+    assert not f2.flags.writeable
+    with pytest.raises(ValueError):
+        f2[0, 0] = 1.5
     del f1
     _, f3, _ = evr.process_packet(st, ev[60:], ManifoldConfig(), SolverConfig(), Thresholds())
     assert np.array_equal(f3, st.u) and not np.array_equal(f2, f3)
@@ -314,3 +318,110 @@ def test_stream_packets_decimation_and_errors():
     st2 = evr.init_state(geom, sc)
     out = list(evr.stream_packets(st2, [pk[0], pk[0][:0]], mc, sc, th))
     assert out[1][1] is None and np.array_equal(out[0][0], out[1][0])
+
+
+def _acceptance8_stream(seed_scene="moving_sine", n=60):
+    """The convergence-budget workload of acceptance criterion 8
+    (test_acceptance.py:273-308): 64x64 simulator stream, 500-event packets."""
+    from paper_1607_06283_b200.simulate import generate_events_array, render_scene
+
+    geom = SensorGeometry(width=64, height=64)
+    ev = generate_events_array(render_scene(seed_scene, geom, n), 0.15, 0.15)
+    return geom, [ev[s:s + 500] for s in range(0, len(ev), 500)]
+
+
+@pytest.mark.parametrize("precision", [0, 1])
+def test_device_early_stop_matches_host_loop(precision):
+    """convergence_tol > 0 on the resident engine: rel_change folded on the
+    device every iteration and the stop taken there (one launch per packet,
+    no host round trip per iteration) -- the same iteration counts, frames
+    and duals as the host-driven loop of the streaming engine, and (float64)
+    the same as the C oracle."""
+    from oracle import oracle as O
+
+    geom, pk = _acceptance8_stream()
+    mc, th = ManifoldConfig(), Thresholds()
+    sc = SolverConfig(lam=2.0, max_iterations=50, convergence_tol=1e-3)
+    dev = evr.init_state(geom, sc, precision=precision)
+    host = evr.init_state(geom, sc, precision=precision, engine=1)
+    ref = O.OracleStream(64, 64, O.make_config(lam=2.0, max_iterations=50, convergence_tol=1e-3))
+    its = []
+    for k, p in enumerate(pk[:30]):
+        n0 = dev.context().launch_count()
+        _, fd, rd = evr.process_packet_arrays(dev, p, mc, sc, th)
+        launches = dev.context().launch_count() - n0
+        _, fh, rh = evr.process_packet_arrays(host, p, mc, sc, th)
+        assert dev.engine() == "resident" and launches == 1
+        assert rd.iterations == rh.iterations, k
+        assert np.array_equal(fd, fh), k
+        assert rd.rel_change == pytest.approx(rh.rel_change, rel=1e-9)
+        if precision == 0:
+            it, _ = ref.process(np.ascontiguousarray(p))
+            assert rd.iterations == it and np.array_equal(fd, ref.u), k
+        its.append(rd.iterations)
+    assert np.array_equal(dev.p, host.p)
+    assert min(its) < 50  # the stop is taken
+
+
+def test_stream_packets_early_stop_pipelined():
+    """The pipelined stream keeps packets in flight with convergence_tol > 0
+    when the engine stops on the device (no per-packet fallback)."""
+    geom, pk = _acceptance8_stream("two_bars", 80)
+    mc, th = ManifoldConfig(), Thresholds()
+    sc = SolverConfig(lam=2.0, max_iterations=50, convergence_tol=1e-3)
+    a = evr.init_state(geom, sc)
+    ref = [evr.process_packet_arrays(a, p, mc, sc, th) for p in pk[:12]]
+    b = evr.init_state(geom, sc)
+    got = list(evr.stream_packets(b, pk[:12], mc, sc, th))
+    for (_, fr, rr), (fg, rg) in zip(ref, got):
+        assert np.array_equal(fr, fg) and rr.iterations == rg.iterations
+        assert rg.packet_ms is not None and rg.packet_ms > 0
+
+
+def test_stream_source_error_delivers_computed_frames():
+    """A packet source that fails (e.g. StreamOrderError from read_stream)
+    still gets every frame computed before the failure, in order, and then
+    the exception -- as the reference's run_stream, which hands frame k to
+    the sink before it reads packet k+1."""
+    geom = SensorGeometry(width=20, height=14)
+    ev = evr.events_to_array(make_events(400, geom, seed=4))
+    pk = [ev[s:s + 100] for s in range(0, 400, 100)]
+    mc, sc, th = ManifoldConfig(), SolverConfig(max_iterations=10), Thresholds()
+    ref_state = evr.init_state(geom, sc)
+    ref = [evr.process_packet_arrays(ref_state, p, mc, sc, th)[1].copy() for p in pk[:3]]
+
+    def source():
+        yield from pk[:3]
+        raise evr.StreamOrderError(0, "timestamp went backwards")
+
+    st = evr.init_state(geom, sc)
+    got = []
+    with pytest.raises(evr.StreamOrderError):
+        for frame, _ in evr.stream_packets(st, source(), mc, sc, th, depth=3):
+            got.append(frame.copy())
+    assert len(got) == 3 and all(np.array_equal(a, b) for a, b in zip(got, ref))
+    # run_stream: the sink saw the three frames, then the error propagated
+    seen = []
+    with pytest.raises(evr.StreamOrderError):
+        evr.run_stream(_bad_events(pk), geom, PacketPolicy(events_per_packet=100), mc, sc, th,
+                       sink=lambda i, f: seen.append(i))
+    assert seen == [0, 1, 2]
+
+
+def _bad_events(pk):
+    for p in pk[:3]:
+        for e in p:
+            yield Event(int(e["x"]), int(e["y"]), int(e["polarity"]), int(e["t"]))
+    raise evr.StreamOrderError(0, "timestamp went backwards")
+
+
+def test_run_stream_solve_ms_is_per_packet_device_time():
+    """run_stream's solve_ms is each packet's own processing time (event
+    upload .. frame download on the device), not the pipeline's inter-arrival
+    time (pipeline.py:239-249)."""
+    geom = SensorGeometry(width=40, height=30)
+    ev = evr.events_to_array(make_events(600, geom, seed=8))
+    _, stats = evr.run_stream(ev, geom, PacketPolicy(events_per_packet=100), ManifoldConfig(),
+                              SolverConfig(), Thresholds(), sink=lambda i, f: None)
+    assert stats.packets == 6 and len(stats.solve_ms) == 6
+    assert all(0 < ms < 1000 for ms in stats.solve_ms)

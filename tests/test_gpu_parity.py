@@ -40,7 +40,7 @@ STREAMS = {
                               evr.Thresholds(0.2, 0.1)),
 }
 
-ENGINES = ["streaming", "resident", "resident_gmem"]
+ENGINES = ["streaming", "resident"]
 
 
 def device_state(d, cfg, precision=0, engine=None):
@@ -56,7 +56,7 @@ def device_state(d, cfg, precision=0, engine=None):
 
 
 def engine_id(name):
-    return {"streaming": 1, "resident": 2, "resident_gmem": 3}[name]
+    return {"streaming": 1, "resident": 2}[name]
 
 
 @pytest.mark.parametrize("engine", ENGINES)
@@ -304,23 +304,24 @@ def test_engines_agree_bitwise():
         assert np.array_equal(res["streaming"][1], res[eng][1]), eng
 
 
-def test_float32_register_engine_matches_streaming_bitwise():
-    """The float32 register-state resident kernel (sensors too large for
-    shared-memory frames) recomputes the metric matrix with the float
-    engine's own operations: bit-identical to the streaming float engine."""
-    H, W = 300, 1000
+@pytest.mark.parametrize("precision", [0, 1])
+def test_resident_plane_frames_match_streaming_bitwise(precision):
+    """Sensors wider than the column kernel's 512 threads run the resident
+    engine's shared-memory plane-frame kernel: bit-identical to the streaming
+    engine in both precisions."""
+    H, W = 120, 600
     sc = evr.SolverConfig(max_iterations=20)
     mc = evr.ManifoldConfig(denoise_iterations=10)
     out = {}
-    for eng in ("streaming", "reg"):
-        st = evr.init_state(evr.SensorGeometry(W, H), sc, precision=1,
-                            engine={"streaming": 1, "reg": 4}[eng])
+    for eng in ("streaming", "resident"):
+        st = evr.init_state(evr.SensorGeometry(W, H), sc, precision=precision,
+                            engine=engine_id(eng))
         for pk in uniform_packets(H, W, 3, 1000, seed=21, t_step=1):
             _, frame, _ = evr.process_packet(st, pk, mc, sc, evr.Thresholds())
-        out[eng] = (frame.copy(), st.p.copy(), st.engine())
-    assert out["reg"][2] == "resident_reg"
-    assert np.array_equal(out["reg"][0], out["streaming"][0])
-    assert np.array_equal(out["reg"][1], out["streaming"][1])
+        out[eng] = (frame.copy(), st.p.copy(), st.context().engine_detail())
+    assert "smem frames" in out["resident"][2]
+    assert np.array_equal(out["resident"][0], out["streaming"][0])
+    assert np.array_equal(out["resident"][1], out["streaming"][1])
 
 
 @pytest.mark.parametrize("precision", [0, 1])
@@ -409,3 +410,21 @@ def test_baseline_sizes_streaming_vs_oracle(cfg):
         assert np.abs(np.log(f32) - np.log(ref.u)).max() <= LOG_TOL
     assert np.array_equal(st.p, ref.p) and np.array_equal(st.f, ref.f)
     assert "k_pd_tile" in st.context().engine_detail()
+
+
+@pytest.mark.parametrize("iters", [1, 2, 3, 4, 5, 7, 13])
+@pytest.mark.parametrize("H,W", [(37, 53), (260, 346)])
+def test_rof_and_l1_tiles_bit_exact_vs_oracle(H, W, iters):
+    """rof_manifold_solve (solve.py:264-293) and the L1 data term run on the
+    temporally blocked tiles (K iterations per launch, remainders merged
+    into the last tile): bit-identical to the C oracle for every iteration
+    count, on a steep manifold, at DAVIS346 size too."""
+    rng = np.random.default_rng(iters)
+    yy, xx = np.mgrid[0:H, 0:W]
+    t = 3.0 * np.sin(xx / 6.0) * np.cos(yy / 9.0) ** 2
+    m = evr.compute_metric(t)
+    f = np.clip(1.5 + 0.3 * np.sin(xx / 5.0) + rng.normal(0, 0.05, (H, W)), 1.0, 2.0)
+    got = evr.rof_manifold_solve(f, m, 8.0, iters)
+    assert np.array_equal(got, O.rof_solve(f, m.tx, m.ty, m.G, m.sqrtG, 8.0, iters))
+    got = evr.l1_manifold_solve(f, m, 3.0, iters)
+    assert np.array_equal(got, O.l1_solve(f, m.tx, m.ty, m.G, m.sqrtG, 3.0, iters))
