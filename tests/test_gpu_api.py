@@ -425,3 +425,37 @@ def test_run_stream_solve_ms_is_per_packet_device_time():
                               SolverConfig(), Thresholds(), sink=lambda i, f: None)
     assert stats.packets == 6 and len(stats.solve_ms) == 6
     assert all(0 < ms < 1000 for ms in stats.solve_ms)
+
+
+@pytest.mark.parametrize("H,W,precision", [(400, 300, 0), (360, 640, 0), (360, 640, 1)])
+def test_streaming_engine_device_early_stop(H, W, precision):
+    """convergence_tol > 0 on the fused streaming list (sensors the resident
+    engine does not take): one march launch + rel_change per iteration behind
+    a device stop flag, no host round trip per iteration -- iteration counts
+    and (float64) frames identical to the C oracle, a constant launch count
+    per packet whatever the stop iteration."""
+    from oracle import oracle as O
+
+    rng = np.random.default_rng(H)
+    sc = SolverConfig(lam=2.0, max_iterations=40, convergence_tol=2e-3)
+    mc, th = ManifoldConfig(), Thresholds()
+    st = evr.init_state(SensorGeometry(W, H), sc, precision=precision)
+    ref = O.OracleStream(H, W, O.make_config(lam=2.0, max_iterations=40, convergence_tol=2e-3))
+    n = 6 * 800
+    ev = evr.make_event_array(rng.integers(0, W, n), rng.integers(0, H, n),
+                              rng.choice([-1, 1], n), np.arange(n, dtype=np.int64) * 2)
+    its, per_packet = [], set()
+    for k in range(6):
+        p = ev[k * 800:(k + 1) * 800]
+        n0 = st.context().launch_count()
+        _, frame, res = evr.process_packet_arrays(st, p, mc, sc, th)
+        per_packet.add(st.context().launch_count() - n0)
+        it, rel = ref.process(np.ascontiguousarray(p))
+        assert st.engine() == "streaming"
+        assert res.iterations == it, k
+        if precision == 0:
+            assert np.array_equal(frame, ref.u), k
+            assert res.rel_change == pytest.approx(rel, rel=1e-9)
+        its.append(res.iterations)
+    assert len(per_packet) == 1
+    assert min(its) < 40

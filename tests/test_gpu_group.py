@@ -62,3 +62,41 @@ def test_banded_flat_and_fixed_window_vs_oracle():
             assert res.iterations == it
             assert np.array_equal(frame, ref.u)
         assert np.array_equal(grp.p, ref.p)
+
+
+def _device_count():
+    """Visible CUDA devices via the driver API (no torch import)."""
+    import ctypes
+
+    try:
+        cuda = ctypes.CDLL("libcuda.so.1")
+    except OSError:
+        return 0
+    n = ctypes.c_int(0)
+    if cuda.cuInit(0) != 0 or cuda.cuDeviceGetCount(ctypes.byref(n)) != 0:
+        return 0
+    return n.value
+
+
+@pytest.mark.skipif(_device_count() < 2,
+                    reason="needs >= 2 visible GPUs (the pool's boxes have one): the bands "
+                           "here would share one device, which test_banded_equals_single_"
+                           "context already covers")
+@pytest.mark.parametrize("prec", [0, 1])
+def test_bands_across_real_devices(prec):
+    """configs[4] across GPUs: one band per visible device (peer access over
+    NVLink, the tiles reading the neighbours' halo rows in place), 2048^2,
+    bit-identical to the single-context run."""
+    n = min(_device_count(), 4)
+    H = W = 2048
+    geom = evr.SensorGeometry(W, H)
+    sc = evr.SolverConfig(max_iterations=23)
+    mc = evr.ManifoldConfig(denoise_iterations=11)
+    grp = evr.BandedStream(geom, sc, mc, bands=n, devices=list(range(n)), precision=prec)
+    st = evr.init_state(geom, sc, precision=prec, engine=1)
+    for pk in packets(H, W, 3, 1000, seed=3):
+        frame, res = grp.process_packet(pk)
+        _, ref, rres = evr.process_packet(st, pk, mc, sc, evr.Thresholds())
+        assert res.iterations == rres.iterations
+        assert np.array_equal(frame, ref)
+    assert np.array_equal(grp.p, st.p)

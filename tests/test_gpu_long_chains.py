@@ -81,11 +81,13 @@ def test_c3_float64_chained_bit_exact(gen):
     ref = O.OracleStream(H, W, O.make_config(max_iterations=pd))
     if gen == "steep":
         yy, xx = np.mgrid[0:H, 0:W]
-        raw = (t0 - ((xx % 4) + (yy % 5)) * 1500).astype(np.int64)
+        # ages rising over 16 columns and dropping back: a ramp of slope
+        # ~0.2 per pixel on the surface, then an edge of ~3 that TV-L1 keeps
+        raw = (t0 - (xx % 16) * 400 - (yy % 9) * 100).astype(np.int64)
         st.raw_timestamps = raw.copy()
         ref.raw[...] = raw
-        st.packet_starts.append(t0 - 6000)
-        ref.packet_starts.append(t0 - 6000)
+        st.packet_starts.append(t0 - 6400)
+        ref.packet_starts.append(t0 - 6400)
     gmax = 1.0
     for k, p in enumerate(pk):
         _, frame, res = evr.process_packet_arrays(st, p, mc, sc, th)

@@ -428,3 +428,35 @@ def test_rof_and_l1_tiles_bit_exact_vs_oracle(H, W, iters):
     assert np.array_equal(got, O.rof_solve(f, m.tx, m.ty, m.G, m.sqrtG, 8.0, iters))
     got = evr.l1_manifold_solve(f, m, 3.0, iters)
     assert np.array_equal(got, O.l1_solve(f, m.tx, m.ty, m.G, m.sqrtG, 3.0, iters))
+
+
+@pytest.mark.parametrize("tol", [0.0, 1e-3])
+def test_resident_exchange_repeatable_under_load(tol):
+    """Race evidence without a sanitizer (closed on this pool): the resident
+    kernel's relaxed tagged-word halo exchange and (tol > 0) its per-iteration
+    rel_change fold, replayed 40 times from the same state at the DAVIS346
+    shape, with a concurrent streaming context loading the GPU from another
+    stream -- every replay bit-identical to the oracle."""
+    H, W = 260, 346
+    sc = evr.SolverConfig(max_iterations=30, convergence_tol=tol)
+    mc, th = evr.ManifoldConfig(denoise_iterations=20), evr.Thresholds()
+    pk = uniform_packets(H, W, 2, 500, seed=11, t_step=2)
+    ref = O.OracleStream(H, W, O.make_config(max_iterations=30, denoise_iterations=20,
+                                             convergence_tol=tol))
+    ref.process(np.ascontiguousarray(pk[0]))
+    u0, f0, raw0, p0 = ref.u.copy(), ref.f.copy(), ref.raw.copy(), ref.p.copy()
+    it_ref, _ = ref.process(np.ascontiguousarray(pk[1]))
+    noise = evr.init_state(evr.SensorGeometry(1280, 720), evr.SolverConfig(), engine=1)
+    noise_pk = uniform_packets(720, 1280, 1, 1000, seed=3, t_step=1)[0]
+    st = evr.init_state(evr.SensorGeometry(W, H), sc)
+    for rep in range(40):
+        st.u, st.f, st.raw_timestamps, st.p = u0.copy(), f0.copy(), raw0.copy(), p0.copy()
+        st.packet_starts.clear()
+        st.packet_starts.append(int(pk[0]["t"][0]))
+        noise.context().call("evr_process_packet_async", evr._lib.ptr(noise_pk), len(noise_pk),
+                             1000.0)
+        _, frame, res = evr.process_packet_arrays(st, pk[1], mc, sc, th)
+        assert st.engine() == "resident"
+        assert res.iterations == it_ref
+        assert np.array_equal(frame, ref.u) and np.array_equal(st.p, ref.p), rep
+    noise.context().call("evr_synchronize", None)
