@@ -216,13 +216,23 @@ int main(int argc, char** argv) {
           [&](int a) { kern<<<grid, 32 * G, smem>>>(d_st[a], d_c2, d_st[a ^ 1], H, W, S); }, K); \
     CK(cudaGetLastError());                                                                    \
   }
-  PD2(3, 4, 8, 2, 1);
-  PDP(3, 4, 8, 2);
-  PDS(3, 4, 8, 2, false);
-  TV2(3, 4, 8, 2, 1);
-  TV2(3, 4, 16, 1, 1);
-  TV2(3, 2, 16, 1, 2);
-  TV2(3, 4, 8, 2, 2);
-  TV2(3, 4, 16, 1, 2);
+#define TV1(K, RPT, G, MINB)                                                                   \
+  check("gen1 tv K" #K " RPT" #RPT " G" #G " MINB" #MINB, 1,                                   \
+        [&](int a) {                                                                           \
+          const int TIW = 32 - 2 * K, TIH = G * RPT - 2 * K;                                   \
+          dim3 grid((W + TIW - 1) / TIW, (H + TIH - 1) / TIH);                                 \
+          k_tv_tile<double, K, RPT, G, MINB, false><<<grid, 32 * G>>>(rows(d_tv[a], 1), fr,   \
+                                                                    d_tv[a ^ 1], H, W, tvs,   \
+                                                                    tvs, shrink);             \
+        },                                                                                     \
+        K)
+  TV1(3, 4, 8, 2);
+  TV1(3, 5, 8, 2);
+  TV1(3, 6, 8, 2);
+  TV1(3, 8, 8, 2);
+  TV1(3, 6, 8, 1);
+  TV1(3, 4, 12, 1);
+  TV1(3, 4, 16, 1);
+  TV1(3, 2, 16, 2);
   return 0;
 }
