@@ -340,7 +340,10 @@ def roofline_of(args, ctx, st, H, W, pd, tv, step_ms):
 
     peaks = load_json("MEASURED_PEAKS.json")
     fp64 = load_json("profiles", "fp64_peak.json")
-    peak = float(fp64.get("fp64_tops", 18.37))
+    f32 = args.precision == "f32"
+    # float64: the DADD / DMUL instruction rate (no contraction allowed);
+    # float32: twice the FFMA rate (a*b+c is one FFMA there)
+    peak = float(fp64.get("fp32_ops", 70.28) if f32 else fp64.get("fp64_tops", 18.37))
     hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
     detail = ctx.engine_detail()
     engine = st.engine()
@@ -364,7 +367,8 @@ def roofline_of(args, ctx, st, H, W, pd, tv, step_ms):
     hit = ncu.get(key)
     if hit and hit.get("engine_detail") != detail:
         hit = None  # captured on another kernel shape: not this run's traffic
-    line = {"bound": "fp64", "achieved": round(achieved, 4), "peak": peak, "unit": "TFLOP/s",
+    line = {"bound": "fp32" if f32 else "fp64", "achieved": round(achieved, 4), "peak": peak,
+            "unit": "TFLOP/s",
             "frac": round(achieved / peak, 4),
             "traffic": hit["dram_bytes_per_launch"] if hit else None,
             "kernel": name, "kernel_us": round(kern_us, 3),
@@ -372,8 +376,9 @@ def roofline_of(args, ctx, st, H, W, pd, tv, step_ms):
             "ops_per_launch": ops,
             "ops_note": f"reference IEEE float64 operations, {PD_OPS} per pixel and primal-dual "
                         f"iteration, {TV_OPS} per TV-L1 iteration (div / sqrt = 1)",
-            "peak_source": "profiles/fp64_peak.json (measured DFMA rate, tools/dp_ilp.cu)"
-                           if fp64 else "fallback 18.37 T/s",
+            "peak_source": ("profiles/fp64_peak.json (measured, tools/dp_ilp.cu: "
+                            + ("2 x FFMA rate)" if f32 else "DADD/DMUL/DFMA instruction rate)"))
+                           if fp64 else "fallback",
             "engine_detail": detail}
     if hit:
         gbs = hit["dram_bytes_per_launch"] / (kern_us * 1e-6) / 1e9

@@ -66,19 +66,28 @@ def test_algorithmic_bytes_formula():
     assert abs(bench.algorithmic_bytes(720, 1280, 4, 100, 50) - 5.71e9) < 0.01e9
 
 
-def test_traffic_covers_every_bench_config():
-    """profiles/traffic.json (bench.py's roofline.traffic) has a DRAM figure for
-    every config / precision of bench.py, keyed by the engine AUTO picks, and
-    each figure is below the config's algorithmic bytes (on-chip reuse)."""
+def test_roofline_captures_match_the_bench_kernels():
+    """profiles/roofline_ncu.json (bench.py's roofline.traffic / hbm / ncu
+    fields) holds the ncu capture of the dominant kernel of the headline
+    config and of the resident configs, each naming the engine detail it was
+    captured on, its DRAM bytes below the kernel's algorithmic bytes (the
+    tile keeps 3 iterations on chip, the resident kernel a whole packet),
+    and points at a committed export."""
     import json
 
-    tr = json.load(open(os.path.join(os.path.dirname(bench.__file__), "profiles", "traffic.json")))
-    for name, (H, W, _epp, pd, tv, _rate) in bench.CONFIGS.items():
-        for prec, w in (("f64", 8), ("f32", 4)):
-            hits = [k for k in tr if k.startswith(f"{name}/{prec}/")]
-            assert hits, f"no traffic entry for {name}/{prec}"
-            for k in hits:
-                assert 0 < tr[k]["bytes_per_launch"] < bench.algorithmic_bytes(H, W, w, pd, tv), k
+    root = os.path.dirname(bench.__file__)
+    rn = json.load(open(os.path.join(root, "profiles", "roofline_ncu.json")))
+    N3 = 720 * 1280
+    assert rn["C3/f64/k_pd_tile"]["dram_bytes_per_launch"] < N3 * 8 * 11 * 3
+    assert "K=3" in rn["C3/f64/k_pd_tile"]["engine_detail"]
+    for key, (H, W, _e, pd, tv, _r) in (("C1/f64/k_resident_col", bench.CONFIGS["C1"]),
+                                        ("C2/f64/k_resident_col", bench.CONFIGS["C2"])):
+        assert rn[key]["dram_bytes_per_launch"] < bench.algorithmic_bytes(H, W, 8, pd, tv)
+        assert "k_resident_col" in rn[key]["engine_detail"]
+    for k, v in rn.items():
+        if not k.startswith("_"):
+            assert os.path.exists(os.path.join(root, v["capture"])), v["capture"]
+            assert 0 < v["fp64_pipe_pct"] <= 100 or k.split("/")[1] == "f32"
 
 
 def _free_port():
@@ -105,3 +114,33 @@ def test_multi_rank_max_over_ranks_gloo():
     out = mgr.dict()
     mp.spawn(_rank_main, args=(world, _free_port(), out), nprocs=world, join=True)
     assert out[0] == out[1] == 1.5
+
+
+def test_reference_arm_line_and_same_config():
+    """`bench.py --impl reference` (the reference algorithm on the host
+    cores: the C port, seed 1 = the GPU arm's rank-0 stream) prints the
+    contract's line, and its `config` object is the GPU arm's, key for key."""
+    import json
+    import subprocess
+    import sys
+
+    root = os.path.dirname(bench.__file__)
+    r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--impl", "reference",
+                        "--config", "C1", "--steps", "2", "--warmup", "3"],
+                       capture_output=True, text=True, timeout=600, cwd=root)
+    assert r.returncode == 0, r.stderr[-2000:]
+    line = json.loads(r.stdout.strip().splitlines()[-1])
+    for k in ("impl", "metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step",
+              "higher_is_better", "config", "cpu_baseline", "e2e"):
+        assert k in line, k
+    assert line["impl"] == "reference" and line["metric"] == "events/s" and line["value"] > 0
+    assert line["config"] == bench.workload_config("C1", "f64")
+    assert line["cpu_baseline"]["kind"] == "port" and line["cpu_baseline"]["cores"] >= 1
+    assert line["e2e"]["h2d_bytes_per_step"] == 0
+
+
+def test_algorithmic_ops_counts():
+    """Reference float64 operations per pixel and iteration:
+    47 per primal-dual iteration, 21 per TV-L1 iteration."""
+    assert bench.PD_OPS == 47 and bench.TV_OPS == 21
+    assert bench.algorithmic_ops(720, 1280, 100, 50) == 921_600 * (4700 + 1050)
