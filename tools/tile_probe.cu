@@ -226,13 +226,28 @@ int main(int argc, char** argv) {
                                                                     tvs, shrink);             \
         },                                                                                     \
         K)
+#define PD1(K, RPT, G, MINB)                                                                   \
+  check("gen1 pd K" #K " RPT" #RPT " G" #G " MINB" #MINB, 0,                                   \
+        [&](int a) {                                                                           \
+          const int TIW = 32 - 2 * K, TIH = G * RPT - 2 * K;                                   \
+          dim3 grid((W + TIW - 1) / TIW, (H + TIH - 1) / TIH);                                 \
+          k_pd_tile<double, K, RPT, G, MINB, MetricPackF64, false><<<grid, 32 * G>>>(          \
+              rows(d_st[a], 1), m1, d_st[a ^ 1], H, W, tau, sigma, 1.0, 2.0);                  \
+        },                                                                                     \
+        K)
+  PD1(3, 4, 8, 2);
+  PD1(3, 3, 8, 2);
+  PD1(4, 3, 8, 2);
+  PD1(3, 3, 10, 2);
+  PD1(3, 3, 9, 2);
+  PD1(3, 3, 7, 2);
+  PD1(3, 3, 6, 2);
+  PD1(3, 3, 8, 3);
+  PD1(3, 2, 8, 3);
+  PD1(3, 2, 12, 2);
   TV1(3, 4, 8, 2);
-  TV1(3, 5, 8, 2);
-  TV1(3, 6, 8, 2);
-  TV1(3, 8, 8, 2);
-  TV1(3, 6, 8, 1);
-  TV1(3, 4, 12, 1);
-  TV1(3, 4, 16, 1);
-  TV1(3, 2, 16, 2);
+  TV1(3, 3, 8, 2);
+  TV1(3, 3, 8, 3);
+  TV1(3, 2, 8, 4);
   return 0;
 }
