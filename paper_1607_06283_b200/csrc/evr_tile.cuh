@@ -48,7 +48,7 @@ namespace evr {
 template <class T, int K, int RPT, int G, int MINB, bool BANDED>
 __global__ void __launch_bounds__(32 * G, MINB)
 k_tv_tile(const MarchRows<Q4<T>> in, const MarchRows<T> f0, Q4<T>* __restrict__ out, int H,
-          int W, T sigma, T tau, T shrink) {
+          int W, T sigma, T tau, T shrink, int early) {
   constexpr int RH = G * RPT, TIW = 32 - 2 * K, TIH = RH - 2 * K;
   __shared__ T ub_top[G][32];  // u_bar of each warp's first row
   __shared__ T py_bot[G][32];  // py of each warp's last row
@@ -58,32 +58,42 @@ k_tv_tile(const MarchRows<Q4<T>> in, const MarchRows<T> f0, Q4<T>* __restrict__ 
   const int gj = (int)blockIdx.x * TIW - K + l;
   const int gi0 = y0 + (int)blockIdx.y * TIH - K + g * RPT;
   const int jc = min(max(gj, 0), W - 1);
-  pdl_wait_and_release();
   T u[RPT], ub[RPT], px[RPT], py[RPT], f[RPT];
   // a band's warps whose rows are all its own skip the neighbour selects
   const bool inner = !BANDED || (gi0 >= y0 && gi0 + RPT <= y1);
-  auto load = [&](auto banded) {
+  auto load_f = [&](auto banded) {
+#pragma unroll
+    for (int r = 0; r < RPT; ++r) {
+      const int gr = min(max(gi0 + r, rlo), rhi);
+      if constexpr (decltype(banded)::value) f[r] = f0.template at<true>(gr, jc, W);
+      else f[r] = f0.at_own(gr, jc, W);
+    }
+  };
+  auto load_s = [&](auto banded) {
 #pragma unroll
     for (int r = 0; r < RPT; ++r) {
       const int gr = min(max(gi0 + r, rlo), rhi);
       Q4<T> q;
-      if constexpr (decltype(banded)::value) {
-        q = in.template at<true>(gr, jc, W);
-        f[r] = f0.template at<true>(gr, jc, W);
-      } else {
-        q = in.at_own(gr, jc, W);
-        f[r] = f0.at_own(gr, jc, W);
-      }
+      if constexpr (decltype(banded)::value) q = in.template at<true>(gr, jc, W);
+      else q = in.at_own(gr, jc, W);
       u[r] = q.x;
       ub[r] = q.y;
       px[r] = q.z;
       py[r] = q.w;
     }
   };
-  if (inner)  // warp-uniform: a band's warps away from its edges skip the selects
-    load(std::false_type{});
-  else if constexpr (BANDED)
-    load(std::true_type{});
+  // early: the surface t was written at least two launches ago, so its
+  // loads overlap the previous launch's tail (as k_pd_tile's constants)
+  const bool pre = !BANDED && sizeof(T) == 8 && early;  // float32: measured no gain
+  if (pre) load_f(std::false_type{});
+  pdl_wait_and_release();
+  if (inner) {  // warp-uniform: a band's warps away from its edges skip the selects
+    if (!pre) load_f(std::false_type{});
+    load_s(std::false_type{});
+  } else if constexpr (BANDED) {
+    load_f(std::true_type{});
+    load_s(std::true_type{});
+  }
   // CTA-uniform: a tile whose whole region lies inside the sensor, one pixel
   // away from its edges, runs the iterations without boundary tests (the
   // reference's interior branch at every pixel, div_at's last else: same
@@ -190,7 +200,7 @@ enum : int { DT_KL = 0, DT_ROF = 1, DT_L1 = 2 };
 template <class T, int K, int RPT, int G, int MINB, class M, bool BANDED, int DT = DT_KL>
 __global__ void __launch_bounds__(32 * G, MINB)
 k_pd_tile(const MarchRows<Q4<T>> in, M m, Q4<T>* __restrict__ out, int H, int W, T tau,
-          T sigma, T umin, T umax) {
+          T sigma, T umin, T umax, int early) {
   constexpr int RH = G * RPT, TIW = 32 - 2 * K, TIH = RH - 2 * K;
   __shared__ T qy_bot[G][32];  // qy of each warp's last row
   __shared__ T v_top[G][32];   // v of each warp's first row
@@ -200,37 +210,52 @@ k_pd_tile(const MarchRows<Q4<T>> in, M m, Q4<T>* __restrict__ out, int H, int W,
   const int gj = (int)blockIdx.x * TIW - K + l;
   const int gi0 = y0 + (int)blockIdx.y * TIH - K + g * RPT;
   const int jc = min(max(gj, 0), W - 1);
-  pdl_wait_and_release();
   T p1[RPT], p2[RPT], p3[RPT], u[RPT];
   Coef<T> cf[RPT];
   T sg[RPT], beta[RPT], fb[RPT];
   T ysg[sizeof(T) == 8 ? RPT : 1];  // float64: refined 1 / sqrtG, hoisted
+  typename M::Raw craw[RPT];
   const bool inner = !BANDED || (gi0 >= y0 && gi0 + RPT <= y1);
-  auto load = [&](auto banded) {
+  auto load_c = [&](auto banded) {
+#pragma unroll
+    for (int r = 0; r < RPT; ++r) {
+      const int gr = min(max(gi0 + r, rlo), rhi);
+      if constexpr (decltype(banded)::value) craw[r] = m.template load<true>(gr, y1, jc, W);
+      else craw[r] = m.load_own(gr, in.y0, in.olo, jc, W);
+    }
+  };
+  auto load_s = [&](auto banded) {
 #pragma unroll
     for (int r = 0; r < RPT; ++r) {
       const int gr = min(max(gi0 + r, rlo), rhi);
       Q4<T> q;
-      typename M::Raw c;
-      if constexpr (decltype(banded)::value) {
-        q = in.template at<true>(gr, jc, W);
-        c = m.template load<true>(gr, y1, jc, W);
-      } else {
-        q = in.at_own(gr, jc, W);
-        c = m.load_own(gr, in.y0, in.olo, jc, W);
-      }
+      if constexpr (decltype(banded)::value) q = in.template at<true>(gr, jc, W);
+      else q = in.at_own(gr, jc, W);
       p1[r] = q.x;
       p2[r] = q.y;
       p3[r] = q.z;
       u[r] = q.w;
-      m.finish(c, cf[r], sg[r], beta[r], fb[r]);
-      if constexpr (sizeof(T) == 8) ysg[r] = fdp_recip(sg[r]);
     }
   };
-  if (inner)  // warp-uniform: a band's warps away from its edges skip the selects
-    load(std::false_type{});
-  else if constexpr (BANDED)
-    load(std::true_type{});
+  // early: the constants were packed at least two launches ago (every
+  // launch of the list passes its griddepcontrol.wait before releasing the
+  // next), so their loads go out before this launch's dependency wait and
+  // overlap the previous launch's tail; the state waits for it
+  const bool pre = !BANDED && sizeof(T) == 8 && early;  // float32: measured no gain
+  if (pre) load_c(std::false_type{});
+  pdl_wait_and_release();
+  if (inner) {  // warp-uniform: a band's warps away from its edges skip the selects
+    if (!pre) load_c(std::false_type{});
+    load_s(std::false_type{});
+  } else if constexpr (BANDED) {
+    load_c(std::true_type{});
+    load_s(std::true_type{});
+  }
+#pragma unroll
+  for (int r = 0; r < RPT; ++r) {
+    m.finish(craw[r], cf[r], sg[r], beta[r], fb[r]);
+    if constexpr (sizeof(T) == 8) ysg[r] = fdp_recip(sg[r]);
+  }
   const int ry0 = gi0 - g * RPT, rx0 = (int)blockIdx.x * TIW - K;
   const bool interior = ry0 >= 1 && ry0 + RH <= H - 1 && rx0 >= 1 && rx0 + 32 <= W - 1;
   auto iterate = [&](auto interior_c) {

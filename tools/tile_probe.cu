@@ -128,10 +128,10 @@ int main(int argc, char** argv) {
     dim3 grid((W + TIW - 1) / TIW, (H + TIH - 1) / TIH);
     if (K == 3)
       k_pd_tile<double, 3, RPT, G, 2, MetricPackF64, false><<<grid, 32 * G>>>(
-          rows(d_st[a], 1), m1, d_st[a ^ 1], H, W, tau, sigma, 1.0, 2.0);
+          rows(d_st[a], 1), m1, d_st[a ^ 1], H, W, tau, sigma, 1.0, 2.0, 0);
     else
       k_pd_tile<double, 4, RPT, G, 2, MetricPackF64, false><<<grid, 32 * G>>>(
-          rows(d_st[a], 1), m1, d_st[a ^ 1], H, W, tau, sigma, 1.0, 2.0);
+          rows(d_st[a], 1), m1, d_st[a ^ 1], H, W, tau, sigma, 1.0, 2.0, 0);
   };
   auto gen1_tv = [&](int K, int a) {
     constexpr int G = 8, RPT = 4;
@@ -139,10 +139,10 @@ int main(int argc, char** argv) {
     dim3 grid((W + TIW - 1) / TIW, (H + TIH - 1) / TIH);
     if (K == 3)
       k_tv_tile<double, 3, RPT, G, 2, false><<<grid, 32 * G>>>(rows(d_tv[a], 1), fr, d_tv[a ^ 1], H,
-                                                               W, tvs, tvs, shrink);
+                                                               W, tvs, tvs, shrink, 0);
     else
       k_tv_tile<double, 4, RPT, G, 2, false><<<grid, 32 * G>>>(rows(d_tv[a], 1), fr, d_tv[a ^ 1], H,
-                                                               W, tvs, tvs, shrink);
+                                                               W, tvs, tvs, shrink, 0);
   };
   reset();
   for (int i = 0; i < NL; ++i) gen1_pd(3, i & 1);
@@ -183,7 +183,7 @@ int main(int argc, char** argv) {
           const int TIW = 32 * CPL - 2 * K, TIH = G * RPT - 2 * K;                             \
           dim3 grid((W + TIW - 1) / TIW, (H + TIH - 1) / TIH);                                 \
           k_tv_tile64<K, RPT, G, MINB, CPL, false><<<grid, 32 * G>>>(                          \
-              rows(d_tv[a], 1), fr, d_tv[a ^ 1], H, W, tvs, tvs, shrink);                      \
+              rows(d_tv[a], 1), fr, d_tv[a ^ 1], H, W, tvs, tvs, shrink, 0);                      \
         },                                                                                     \
         K)
 #define PDP(K, RPT, G, MINB)                                                                    \
@@ -223,7 +223,7 @@ int main(int argc, char** argv) {
           dim3 grid((W + TIW - 1) / TIW, (H + TIH - 1) / TIH);                                 \
           k_tv_tile<double, K, RPT, G, MINB, false><<<grid, 32 * G>>>(rows(d_tv[a], 1), fr,   \
                                                                     d_tv[a ^ 1], H, W, tvs,   \
-                                                                    tvs, shrink);             \
+                                                                    tvs, shrink, 0);          \
         },                                                                                     \
         K)
 #define PD1(K, RPT, G, MINB)                                                                   \
@@ -232,22 +232,44 @@ int main(int argc, char** argv) {
           const int TIW = 32 - 2 * K, TIH = G * RPT - 2 * K;                                   \
           dim3 grid((W + TIW - 1) / TIW, (H + TIH - 1) / TIH);                                 \
           k_pd_tile<double, K, RPT, G, MINB, MetricPackF64, false><<<grid, 32 * G>>>(          \
-              rows(d_st[a], 1), m1, d_st[a ^ 1], H, W, tau, sigma, 1.0, 2.0);                  \
+              rows(d_st[a], 1), m1, d_st[a ^ 1], H, W, tau, sigma, 1.0, 2.0, 0);                  \
         },                                                                                     \
         K)
-  PD1(3, 4, 8, 2);
   PD1(3, 3, 8, 2);
-  PD1(4, 3, 8, 2);
-  PD1(3, 3, 10, 2);
-  PD1(3, 3, 9, 2);
-  PD1(3, 3, 7, 2);
-  PD1(3, 3, 6, 2);
-  PD1(3, 3, 8, 3);
-  PD1(3, 2, 8, 3);
-  PD1(3, 2, 12, 2);
-  TV1(3, 4, 8, 2);
-  TV1(3, 3, 8, 2);
-  TV1(3, 3, 8, 3);
-  TV1(3, 2, 8, 4);
+  {
+    // L2 persistence of the constants (set-aside + access-policy window on
+    // the launches), the rest streaming
+    int maxp = 0, maxw = 0;
+    cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, 0);
+    cudaDeviceGetAttribute(&maxw, cudaDevAttrMaxAccessPolicyWindowSize, 0);
+    printf("max persisting L2 %d MB, max window %d MB, constants %lld MB\n", maxp >> 20, maxw >> 20,
+           (long long)(2 * N * sizeof(Q)) >> 20);
+    CK(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, maxp));
+    for (double ratio : {1.0, 0.75, 0.5}) {
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeAccessPolicyWindow;
+      at[0].val.accessPolicyWindow.base_ptr = d_c;
+      at[0].val.accessPolicyWindow.num_bytes = std::min<size_t>(2 * N * sizeof(Q), maxw);
+      at[0].val.accessPolicyWindow.hitRatio = (float)ratio;
+      at[0].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+      at[0].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+      char name[80];
+      snprintf(name, sizeof name, "gen1 pd K3 RPT3 + L2 persist ratio %.2f", ratio);
+      check(name, 0,
+            [&](int a) {
+              constexpr int K = 3, RPT = 3, G = 8;
+              const int TIW = 32 - 2 * K, TIH = G * RPT - 2 * K;
+              cudaLaunchConfig_t lc{};
+              lc.gridDim = dim3((W + TIW - 1) / TIW, (H + TIH - 1) / TIH);
+              lc.blockDim = dim3(32 * G);
+              lc.attrs = at;
+              lc.numAttrs = 1;
+              cudaLaunchKernelEx(&lc, k_pd_tile<double, K, RPT, G, 2, MetricPackF64, false>,
+                                 rows(d_st[a], 1), m1, d_st[a ^ 1], H, W, tau, sigma, 1.0, 2.0, 0);
+            },
+            3);
+      cudaCtxResetPersistingL2Cache();
+    }
+  }
   return 0;
 }
