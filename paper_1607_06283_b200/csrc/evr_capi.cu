@@ -194,7 +194,10 @@ void launch_ingest(evr_ctx* ctx) {
 enum StepKind {
   ST_INGEST, ST_NORM, ST_TVD, ST_TVP, ST_TVFIN, ST_METRIC, ST_PDP, ST_REL, ST_PDD, ST_EPI,
   // fused list (whole-sensor contexts): packed state, one launch per iteration
-  ST_NORMF, ST_TVF, ST_TVFINF, ST_PACK, ST_PDF, ST_RELF, ST_UNPACK
+  ST_NORMF, ST_TVF, ST_TVFINF, ST_PACK, ST_PDF, ST_RELF, ST_UNPACK,
+  // whole-sensor fused list: TV-L1 end + metric + pack in one launch, the
+  // final tile leaving u_{M-1}, epilogue + rel_change in one launch
+  ST_MPACK, ST_PDFIN, ST_UNREL
 };
 struct Step {
   int kind, it;
@@ -210,10 +213,58 @@ struct Step {
 // -> 2 tiles); the last primal-dual iteration always runs alone, so
 // rel_change sees the u of the two last iterations.  Split list (bands with EVR_GROUP_SPLIT): one launch
 // per half-step with halo rows exchanged between half-steps.
-std::vector<Step> packet_steps(const evr_config& g, int which, bool fused, int tk = 1) {
+std::vector<Step> packet_steps(const evr_config& g, int which, bool fused, int tk = 1,
+                               bool whole = false) {
   std::vector<Step> v;
   const int D = g.denoise_iterations, M = g.max_iterations;
   tk = std::max(tk, 1);
+  static const int fuse = [] {  // A/B switch of the whole-sensor fusions (bit 0 MPACK, bit 1 PDFIN/UNREL)
+    const char* e = getenv("EVR_FUSE");
+    return e ? atoi(e) : 3;
+  }();
+  if (whole && fused && which == 2 && tk > 1 && M >= 2 && g.convergence_tol <= 0 && fuse) {
+    // whole-sensor packet: up to 4 launches fewer than the general list below
+    v.push_back({ST_INGEST, 0});
+    int b = 0;
+    if (g.manifold_enabled) {
+      v.push_back({ST_NORMF, 0});
+      for (int k = 0; k < D;) {
+        const int kk = std::min(tk, D - k);
+        v.push_back({ST_TVF, k, b, kk});
+        b ^= 1;
+        k += kk;
+      }
+    }
+    if (fuse & 1) {
+      v.push_back({ST_MPACK, 0, b});  // b: the TV set holding the last iteration
+    } else {
+      if (g.manifold_enabled) v.push_back({ST_TVFINF, D, b});
+      v.push_back({ST_METRIC, 0});
+      v.push_back({ST_PACK, 0});
+    }
+    b = 0;
+    if (fuse & 2) {
+      for (int k = 0, rem = M; rem > 0;) {  // every launch 2..4 iterations (the built tiles)
+        int kk = std::min(tk, rem);
+        if (rem - kk == 1) kk = kk < 4 ? kk + 1 : kk - 1;
+        v.push_back({rem == kk ? ST_PDFIN : ST_PDF, k, b, kk});
+        b ^= 1;
+        k += kk;
+        rem -= kk;
+      }
+      v.push_back({ST_UNREL, M, b});
+    } else {
+      for (int k = 0; k < M;) {
+        const int kk = std::max(1, std::min(tk, M - 1 - k));
+        v.push_back({ST_PDF, k, b, kk});
+        if (k == M - 1) v.push_back({ST_RELF, k, b});
+        b ^= 1;
+        k += kk;
+      }
+      v.push_back({ST_UNPACK, M, b});
+    }
+    return v;
+  }
   if (which != 1) {
     v.push_back({ST_INGEST, 0});
     if (g.manifold_enabled) {
@@ -503,7 +554,7 @@ int launch_tv_tile(evr_ctx* ctx, int K, const MarchRows<Q4<T>>& in, const MarchR
 // step: tau = sigma for operator solves (no context config); < 0 = the config's
 template <class T, int RPT, bool B, class M, int DT = DT_KL>
 void pd_tile_rpt(evr_ctx* ctx, int K, const MarchRows<Q4<T>>& in, const M& m, Q4<T>* out,
-                 double step = -1.0, int early = 0) {
+                 double step = -1.0, int early = 0, T* prev = nullptr) {
   constexpr int G = TileShape<T>::G, MB = TileShape<T>::MINB;
   const evr_config& g = ctx->cfg;
   const int H = ctx->Htot, W = ctx->W;
@@ -511,33 +562,36 @@ void pd_tile_rpt(evr_ctx* ctx, int K, const MarchRows<Q4<T>>& in, const M& m, Q4
   const T tau = (T)(step < 0 ? g.tau : step), sigma = (T)(step < 0 ? g.sigma : step);
   const T lo = (T)g.u_min, hi = (T)g.u_max;
   if (K == 2)
-    launch_pdl2(k_pd_tile<T, 2, RPT, G, MB, M, B, DT>, tile_grid<T, 2, RPT>(ctx), 32 * G, s, in, m,
-                out, H, W, tau, sigma, lo, hi, early);
+    launch_pdl2(prev ? k_pd_tile<T, 2, RPT, G, MB, M, B, DT, !B> : k_pd_tile<T, 2, RPT, G, MB, M, B, DT>,
+                tile_grid<T, 2, RPT>(ctx), 32 * G, s, in, m, out, H, W, tau, sigma, lo, hi, early,
+                prev);
   else if (K == 3)
-    launch_pdl2(k_pd_tile<T, 3, RPT, G, MB, M, B, DT>, tile_grid<T, 3, RPT>(ctx), 32 * G, s, in, m,
-                out, H, W, tau, sigma, lo, hi, early);
+    launch_pdl2(prev ? k_pd_tile<T, 3, RPT, G, MB, M, B, DT, !B> : k_pd_tile<T, 3, RPT, G, MB, M, B, DT>,
+                tile_grid<T, 3, RPT>(ctx), 32 * G, s, in, m, out, H, W, tau, sigma, lo, hi, early,
+                prev);
   else
-    launch_pdl2(k_pd_tile<T, 4, RPT, G, MB, M, B, DT>, tile_grid<T, 4, RPT>(ctx), 32 * G, s, in, m,
-                out, H, W, tau, sigma, lo, hi, early);
+    launch_pdl2(prev ? k_pd_tile<T, 4, RPT, G, MB, M, B, DT, !B> : k_pd_tile<T, 4, RPT, G, MB, M, B, DT>,
+                tile_grid<T, 4, RPT>(ctx), 32 * G, s, in, m, out, H, W, tau, sigma, lo, hi, early,
+                prev);
 }
 template <class T, bool B, class M>
 void pd_tile_shape(evr_ctx* ctx, int K, const MarchRows<Q4<T>>& in, const M& m, Q4<T>* out,
-                   int early) {
+                   int early, T* prev = nullptr) {
   constexpr int R0 = TileShape<T>::RPT;
   const int rpt = tile_rpt<T>(ctx, K);
   if constexpr (std::is_same<T, float>::value && R0 == 8) {
-    if (rpt == 7) return pd_tile_rpt<T, 7, B>(ctx, K, in, m, out, -1.0, early);
-    if (rpt == 6) return pd_tile_rpt<T, 6, B>(ctx, K, in, m, out, -1.0, early);
+    if (rpt == 7) return pd_tile_rpt<T, 7, B>(ctx, K, in, m, out, -1.0, early, prev);
+    if (rpt == 6) return pd_tile_rpt<T, 6, B>(ctx, K, in, m, out, -1.0, early, prev);
   }
-  pd_tile_rpt<T, R0, B>(ctx, K, in, m, out, -1.0, early);
+  pd_tile_rpt<T, R0, B>(ctx, K, in, m, out, -1.0, early, prev);
 }
 template <class T, class M>
 int launch_pd_tile(evr_ctx* ctx, int K, const MarchRows<Q4<T>>& in, const M& m, Q4<T>* out,
-                   int early) {
+                   int early, T* prev = nullptr) {
   if (ctx->banded)
     pd_tile_shape<T, true>(ctx, K, in, m, out, 0);
   else
-    pd_tile_shape<T, false>(ctx, K, in, m, out, early);
+    pd_tile_shape<T, false>(ctx, K, in, m, out, early, prev);
   return 1;
 }
 
@@ -637,7 +691,8 @@ template <class T> int launch_step(evr_ctx* ctx, const Step& st) {
           P.pd[0] + off, P.cst + off * E, n);
       return 1;
     }
-    case ST_PDF: {
+    case ST_PDF:
+    case ST_PDFIN: {
       const int a = st.buf;
       constexpr int E = sizeof(T) == 8 ? 2 : 1;
       using M = typename MetricPack<T>::type;
@@ -650,7 +705,9 @@ template <class T> int launch_step(evr_ctx* ctx, const Step& st) {
         m = M{cr.own, cr};
       Q4<T>* out = packed<T>(ctx).pd[a ^ 1];
       // not the first iteration launch after the pack: constants loaded early
-      if (st.k > 1) return launch_pd_tile<T>(ctx, st.k, in, m, out, st.it > 0 ? 1 : 0);
+      if (st.k > 1)
+        return launch_pd_tile<T>(ctx, st.k, in, m, out, st.it > 0 ? 1 : 0,
+                                 st.kind == ST_PDFIN ? ctx->fld<T>(F_UN) : (T*)nullptr);
       if (ctx->banded)
         launch_pdl(k_pd_march<T, kMarchRY, MarchDepth<T>::pd, M, true>, march_grid(ctx), kMarchNT,
                    s, in.own, in, m, out, ctx->Htot, ctx->W, (T)g.tau, (T)g.sigma, (T)g.u_min,
@@ -659,6 +716,23 @@ template <class T> int launch_step(evr_ctx* ctx, const Step& st) {
         launch_pdl(k_pd_march<T, kMarchRY, MarchDepth<T>::pd, M, false>, march_grid(ctx), kMarchNT,
                    s, in.own, in, m, out, ctx->Htot, ctx->W, (T)g.tau, (T)g.sigma, (T)g.u_min,
                    (T)g.u_max, (const int*)(g.convergence_tol > 0 ? ctx->d_stop : nullptr));
+      return 1;
+    }
+    case ST_MPACK: {  // st.buf: the TV set holding the last iteration
+      const Packed<T> P = packed<T>(ctx);
+      k_metric_pack<T><<<grid2d(ctx), block2d(), 0, s>>>(
+          P.tv[st.buf], ctx->f, ctx->fld<T>(F_P1), ctx->fld<T>(F_P2), ctx->fld<T>(F_P3),
+          ctx->fld<T>(F_U), t, ctx->fld<T>(F_TX), ctx->fld<T>(F_TY), ctx->fld<T>(F_G),
+          ctx->fld<T>(F_SG), P.pd[0], P.cst, ctx->H, ctx->W, (T)g.t_scale, (T)(g.tau * g.lam),
+          g.manifold_enabled ? 0 : 1);
+      return 1;
+    }
+    case ST_UNREL: {  // st.buf: the set holding the last iteration, F_UN: u_{M-1}
+      const Packed<T> P = packed<T>(ctx);
+      launch_pdl(k_unpack_rel<T, kNT>, red_blocks(n), kNT, s, (const Q4<T>*)P.pd[st.buf],
+                 (const T*)ctx->fld<T>(F_UN), ctx->fld<T>(F_P1), ctx->fld<T>(F_P2),
+                 ctx->fld<T>(F_P3), ctx->fld<T>(F_U), ctx->f, n, ctx->part, ctx->rticket,
+                 ctx->d_info, st.it);
       return 1;
     }
     case ST_RELF: {  // u of the last two iterations, the w of the packed quads
@@ -686,7 +760,7 @@ template <class T> int launch_step(evr_ctx* ctx, const Step& st) {
 template <class T> int enqueue_packet(evr_ctx* ctx, int which) {
   int n = 0;
   const int tk = ctx->banded ? 1 : ctx_tile_k(ctx);
-  for (const Step& st : packet_steps(ctx->cfg, which, !ctx->banded, tk))
+  for (const Step& st : packet_steps(ctx->cfg, which, !ctx->banded, tk, !ctx->banded))
     n += launch_step<T>(ctx, st);
   int rc = launch_err(ctx, "packet");
   return rc ? rc : n;
@@ -1478,11 +1552,14 @@ int evr_engine_detail(evr_ctx* ctx, char* buf, int len) {
         const int rpt = d ? tile_rpt<double>(ctx, tk) : tile_rpt<float>(ctx, tk);
         const int G = d ? TileShape<double>::G : TileShape<float>::G;
         const int tiw = 32 - 2 * tk, tih = G * rpt - 2 * tk;
+        const bool whole = ctx->cfg.convergence_tol <= 0 && ctx->cfg.max_iterations >= 2;
         snprintf(buf, len,
                  "streaming k_tv_tile/k_pd_tile<%s,K=%d> %d iterations per launch, %dx%d tiles, "
-                 "%d CTAs x %d (+ k_pd_march<RY=%d> for the last iteration)",
+                 "%d CTAs x %d%s",
                  ty, tk, tk, tiw, tih, ((ctx->W + tiw - 1) / tiw) * ((ctx->H + tih - 1) / tih),
-                 32 * G, kMarchRY);
+                 32 * G,
+                 whole ? ", fused metric+pack and epilogue+rel_change"
+                       : " (+ k_pd_march per iteration with a convergence_tol)");
       } else {
         snprintf(buf, len, "streaming k_tv_march/k_pd_march<%s,RY=%d> %u CTAs x %d", ty,
                  kMarchRY, march_grid(ctx), kMarchNT);

@@ -672,6 +672,50 @@ __global__ void k_tv_finish_packed(const Q4<T>* __restrict__ q, T* __restrict__ 
   t[k] = vclip(q[k].x, T(0), t_scale);
 }
 
+// Whole-sensor fused list, one launch instead of three: the end of TV-L1
+// (np.clip(u, 0, t_scale), surface.py:195) on the packed TV state, the
+// metric (compute_metric + coeffs, surface.py:81-90, :199-205, exactly
+// k_metric_setup's operations: a pixel's slopes read its right / lower
+// neighbours' clipped u) and the packing of the solver state and
+// constants.  Writes the t, tx, ty, G, sqrtG planes (state views); the
+// coefficient planes stay unwritten -- only the packed constants feed the
+// tiles.  flat: the metric of a disabled manifold (tx = ty = 0).
+template <class T>
+__global__ void k_metric_pack(const Q4<T>* __restrict__ tvq, const double* __restrict__ f,
+                              const T* __restrict__ p1, const T* __restrict__ p2,
+                              const T* __restrict__ p3, const T* __restrict__ u,
+                              T* __restrict__ t, T* __restrict__ tx, T* __restrict__ ty,
+                              T* __restrict__ G, T* __restrict__ sgp, Q4<T>* __restrict__ st,
+                              Q4<T>* __restrict__ cst, int H, int W, T t_scale, T tl, int flat) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  const int i = blockIdx.y * blockDim.y + threadIdx.y;
+  if (i >= H || j >= W) return;
+  const int64_t k = (int64_t)i * W + j;
+  T gx = T(0), gy = T(0);
+  if (!flat) {
+    const T tk = vclip(tvq[k].x, T(0), t_scale);
+    t[k] = tk;
+    gx = j < W - 1 ? vclip(tvq[k + 1].x, T(0), t_scale) - tk : T(0);
+    gy = i < H - 1 ? vclip(tvq[k + W].x, T(0), t_scale) - tk : T(0);
+  }
+  const T det = metric_G(gx, gy);
+  const T s = Arith<T>::sqrt(det);
+  tx[k] = gx;
+  ty[k] = gy;
+  G[k] = det;
+  sgp[k] = s;
+  const T b = tl * s;
+  const T fb = T(4) * b * (T)f[k];
+  st[k] = Q4<T>{p1[k], p2[k], p3[k], u[k]};
+  if constexpr (sizeof(T) == 4) {
+    cst[k] = Q4<T>{gx, gy, fb, T(0)};
+  } else {
+    const Coef<T> a = coeffs_of(gx, gy, det);
+    cst[2 * k] = Q4<T>{a.a11, a.a12, a.a22, a.a31};
+    cst[2 * k + 1] = Q4<T>{a.a32, s, b, fb};
+  }
+}
+
 // planes -> packed solver state + constants (after k_metric_setup)
 template <class T>
 __global__ void k_pack_solver(const T* __restrict__ p1, const T* __restrict__ p2,
@@ -780,6 +824,61 @@ k_relchange(const T* __restrict__ un, const T* __restrict__ u, int64_t N, double
     sums[1] = o;
     *ticket = 0u;
     if (stop && rel < tol) *stop = 1;
+  }
+}
+
+// Whole-sensor fused list: the epilogue (state.u = u, state.p, state.f =
+// copy(u), pipeline.py:167-170) from the packed set holding the last
+// iteration, fused with rel_change of that iteration (solve.py:246-249:
+// |u_M - u_{M-1}| / max(|u_{M-1}|, 1e-30)) against the u_{M-1} plane the
+// final tile left (k_pd_tile's `prev`); per-CTA partials, the last CTA
+// folds them in index order (as k_relchange).
+template <class T, int NT>
+__global__ void __launch_bounds__(NT)
+k_unpack_rel(const Q4<T>* __restrict__ q, const T* __restrict__ uprev, T* __restrict__ p1,
+             T* __restrict__ p2, T* __restrict__ p3, T* __restrict__ u,
+             double* __restrict__ f, int64_t N, double* part, unsigned* ticket,
+             evr_solve_info* info, int iterations) {
+  __shared__ double sh[NT / 32];
+  __shared__ bool last;
+  pdl_wait_and_release();
+  double d = 0.0, o = 0.0;
+  for (int64_t k = (int64_t)blockIdx.x * NT + threadIdx.x; k < N; k += (int64_t)gridDim.x * NT) {
+    const Q4<T> v = q[k];
+    p1[k] = v.x;
+    p2[k] = v.y;
+    p3[k] = v.z;
+    u[k] = v.w;
+    f[k] = (double)v.w;
+    const double a = (double)v.w, b = (double)uprev[k];
+    d += (a - b) * (a - b);
+    o += b * b;
+  }
+  d = block_sum<NT>(d, sh);
+  o = block_sum<NT>(o, sh);
+  if (threadIdx.x == 0) {
+    part[2 * blockIdx.x] = d;
+    part[2 * blockIdx.x + 1] = o;
+    __threadfence();
+    last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  const int nb = (int)gridDim.x;
+  d = 0.0;
+  o = 0.0;
+  for (int b = threadIdx.x; b < nb; b += NT) {
+    d += __ldcg(part + 2 * b);
+    o += __ldcg(part + 2 * b + 1);
+  }
+  d = block_sum<NT>(d, sh);
+  o = block_sum<NT>(o, sh);
+  if (threadIdx.x == 0) {
+    const double den = sqrt(o);
+    info->rel_change = sqrt(d) / (den > 1e-30 ? den : 1e-30);
+    info->iterations = iterations;
+    *ticket = 0u;
   }
 }
 

@@ -197,10 +197,11 @@ k_tv_tile(const MarchRows<Q4<T>> in, const MarchRows<T> f0, Q4<T>* __restrict__ 
 // (rof_manifold_solve, solve.py:285-287: slots 1 / (1 + w), w f), 2 = L1
 // (slots w = tau lam sqrtG, f; the soft shrink of k_l1_primal).
 enum : int { DT_KL = 0, DT_ROF = 1, DT_L1 = 2 };
-template <class T, int K, int RPT, int G, int MINB, class M, bool BANDED, int DT = DT_KL>
+template <class T, int K, int RPT, int G, int MINB, class M, bool BANDED, int DT = DT_KL,
+          bool PREV = false>
 __global__ void __launch_bounds__(32 * G, MINB)
 k_pd_tile(const MarchRows<Q4<T>> in, M m, Q4<T>* __restrict__ out, int H, int W, T tau,
-          T sigma, T umin, T umax, int early) {
+          T sigma, T umin, T umax, int early, T* __restrict__ prev) {
   constexpr int RH = G * RPT, TIW = 32 - 2 * K, TIH = RH - 2 * K;
   __shared__ T qy_bot[G][32];  // qy of each warp's last row
   __shared__ T v_top[G][32];   // v of each warp's first row
@@ -268,6 +269,16 @@ k_pd_tile(const MarchRows<Q4<T>> in, M m, Q4<T>* __restrict__ out, int H, int W,
     };
 #pragma unroll 1
     for (int it = 0; it < K; ++it) {
+      if (PREV && it == K - 1) {  // the final launch: u before the last iteration
+        if (l >= K && l < 32 - K && gj < W) {  // (k_unpack_rel's rel_change)
+  #pragma unroll
+          for (int r = 0; r < RPT; ++r) {
+            const int R = g * RPT + r, gi = gi0 + r;
+            if (R >= K && R < RH - K && gi < y1)
+              prev[(int64_t)(gi - y0 + (BANDED ? in.olo : 0)) * W + gj] = u[r];
+          }
+        }
+      }
       T qx[RPT], qy[RPT], v[RPT];
   #pragma unroll
       for (int r = 0; r < RPT; ++r) q_of(cf[r], p1[r], p2[r], p3[r], qx[r], qy[r]);

@@ -235,41 +235,10 @@ int main(int argc, char** argv) {
               rows(d_st[a], 1), m1, d_st[a ^ 1], H, W, tau, sigma, 1.0, 2.0, 0);                  \
         },                                                                                     \
         K)
-  PD1(3, 3, 8, 2);
-  {
-    // L2 persistence of the constants (set-aside + access-policy window on
-    // the launches), the rest streaming
-    int maxp = 0, maxw = 0;
-    cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, 0);
-    cudaDeviceGetAttribute(&maxw, cudaDevAttrMaxAccessPolicyWindowSize, 0);
-    printf("max persisting L2 %d MB, max window %d MB, constants %lld MB\n", maxp >> 20, maxw >> 20,
-           (long long)(2 * N * sizeof(Q)) >> 20);
-    CK(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, maxp));
-    for (double ratio : {1.0, 0.75, 0.5}) {
-      cudaLaunchAttribute at[1];
-      at[0].id = cudaLaunchAttributeAccessPolicyWindow;
-      at[0].val.accessPolicyWindow.base_ptr = d_c;
-      at[0].val.accessPolicyWindow.num_bytes = std::min<size_t>(2 * N * sizeof(Q), maxw);
-      at[0].val.accessPolicyWindow.hitRatio = (float)ratio;
-      at[0].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
-      at[0].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
-      char name[80];
-      snprintf(name, sizeof name, "gen1 pd K3 RPT3 + L2 persist ratio %.2f", ratio);
-      check(name, 0,
-            [&](int a) {
-              constexpr int K = 3, RPT = 3, G = 8;
-              const int TIW = 32 - 2 * K, TIH = G * RPT - 2 * K;
-              cudaLaunchConfig_t lc{};
-              lc.gridDim = dim3((W + TIW - 1) / TIW, (H + TIH - 1) / TIH);
-              lc.blockDim = dim3(32 * G);
-              lc.attrs = at;
-              lc.numAttrs = 1;
-              cudaLaunchKernelEx(&lc, k_pd_tile<double, K, RPT, G, 2, MetricPackF64, false>,
-                                 rows(d_st[a], 1), m1, d_st[a ^ 1], H, W, tau, sigma, 1.0, 2.0, 0);
-            },
-            3);
-      cudaCtxResetPersistingL2Cache();
-    }
-  }
+  TV1(3, 3, 8, 2);
+  TV1(2, 3, 8, 2);
+  TV1(2, 4, 8, 2);
+  TV1(4, 4, 8, 2);
+  TV1(2, 2, 8, 3);
   return 0;
 }
