@@ -19,6 +19,7 @@ for v in rof l1 tgv; do
   python bench.py --config C2 --variant $v --steps 50 --warmup 5 > $O/bench_C2_$v.json 2>&1
 done
 python bench.py --config C5 --bands 2 --steps 20 --warmup 3 > $O/bench_C5_bands2_1gpu.json 2>&1
+for fz in 0 3; do EVR_FUSE=$fz python bench.py --steps 200 --warmup 10 --no-cpu-baseline > $O/bench_C3_f64_fuse$fz.json 2>&1; done
 ncu --metrics gpu__time_duration.sum --clock-control none --csv -c 300 --log-file $O/launches_C3_f64.csv \
     python bench.py --steps 2 --warmup 3 --no-cpu-baseline > /dev/null 2>&1
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches_C2_f64.csv \
@@ -31,6 +32,8 @@ ncu --set full --import-source on --clock-control none -k regex:k_resident -s 5 
     -o $O/full_k_resident_col_C2_f64 python bench.py --config C2 --steps 2 --warmup 3 --no-cpu-baseline > /dev/null 2>&1
 ncu --set full --import-source on --clock-control none -k regex:k_resident -s 5 -c 1 \
     -o $O/full_k_resident_col_C1_f64 python bench.py --config C1 --steps 2 --warmup 3 --no-cpu-baseline > /dev/null 2>&1
+ncu --set full --import-source on --clock-control none -k regex:"k_metric_pack|k_unpack_rel" -s 2 -c 2 \
+    -o $O/full_k_fused_C3_f64 python bench.py --steps 1 --warmup 3 --no-cpu-baseline > /dev/null 2>&1
 ncu --set full --import-source on --clock-control none -k regex:k_pd_tile -s 40 -c 1 \
     -o $O/full_k_pd_tile_C3_f32 python bench.py --precision f32 --steps 1 --warmup 3 --no-cpu-baseline > /dev/null 2>&1
 for r in $O/*.ncu-rep; do
