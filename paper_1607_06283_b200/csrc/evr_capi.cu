@@ -2257,43 +2257,42 @@ int evr_op_tgv_solve(evr_ctx* ctx, const double* f, const double* tx, const doub
   if (data_term == 0 && !(u_min < u_max))
     return fail(ctx, EVR_ERR_INVALID, "box must satisfy u_min < u_max");
   int rc;
-  if (!ctx->tgv) CK(cudaMalloc(&ctx->tgv, 9 * B));
+  // the ping-pong sets of k_tgv_iter: w1, w2 and q11, q22, q12 twice, plus
+  // the second dual set (the first is F_P1..F_P3)
+  if (!ctx->tgv) CK(cudaMalloc(&ctx->tgv, 13 * B));
   if ((rc = upload_metric(ctx, tx, ty, G, sqrtG))) return rc;
   double* fdev = ctx->aos_b;
   if ((rc = h2d(ctx, fdev, f, B))) return rc;
   CK(cudaMemcpyAsync(ctx->fld<double>(F_U), fdev, B, cudaMemcpyDeviceToDevice, s));
   for (int k : {F_P1, F_P2, F_P3}) CK(cudaMemsetAsync(ctx->fld<double>(k), 0, B, s));
   double* t = ctx->tgv;
-  CK(cudaMemsetAsync(t, 0, 9 * B, s));
+  CK(cudaMemsetAsync(t, 0, 13 * B, s));
   const double step = 1.0 / std::sqrt(17.0 + 4.0 * std::sqrt(2.0));
   k_solver_setup<double><<<grid1d(N), kNT, 0, s>>>(
       ctx->fld<double>(F_TX), ctx->fld<double>(F_TY), ctx->fld<double>(F_G), ctx->fld<double>(F_SG),
       fdev, coefs<double>(ctx), ctx->fld<double>(F_BETA), ctx->fld<double>(F_FB), N, step * lam, 0);
-  double* ub[2] = {ctx->fld<double>(F_U), ctx->fld<double>(F_UN)};
-  double* w[2][2] = {{t, t + N}, {t + 2 * N, t + 3 * N}};
+  const TgvSet<double> sets[2] = {
+      {ctx->fld<double>(F_U), t, t + N, ctx->fld<double>(F_P1), ctx->fld<double>(F_P2),
+       ctx->fld<double>(F_P3), t + 4 * N, t + 5 * N, t + 6 * N},
+      {ctx->fld<double>(F_UN), t + 2 * N, t + 3 * N, t + 10 * N, t + 11 * N, t + 12 * N,
+       t + 7 * N, t + 8 * N, t + 9 * N}};
   for (int it = 0; it < iterations; ++it) {
     const int a = it & 1;
-    TgvPlanes<double> tp{w[a][0], w[a][1], w[a ^ 1][0], w[a ^ 1][1], t + 4 * N, t + 5 * N,
-                         t + 6 * N, t + 7 * N, t + 8 * N};
-    double* v = ctx->fld<double>(F_V);
-    k_tgv_primal<double><<<grid2d(ctx), block2d(), 0, s>>>(
-        ctx->fld<double>(F_P1), ctx->fld<double>(F_P2), ctx->fld<double>(F_P3), coefs<double>(ctx),
-        ub[a], ctx->fld<double>(F_SG), fdev, ub[a ^ 1], v, tp, ctx->geo_own(), step, step * lam,
-        data_term, u_min, u_max);
-    k_tgv_dual<double><<<grid2d(ctx), block2d(), 0, s>>>(
-        v, tp, ctx->fld<double>(F_P1), ctx->fld<double>(F_P2), ctx->fld<double>(F_P3),
-        coefs<double>(ctx), ctx->fld<double>(F_SG), ctx->geo_own(), step, alpha0, alpha1);
+    k_tgv_iter<double><<<grid2d(ctx), block2d(), 0, s>>>(
+        sets[a], sets[a ^ 1], coefs<double>(ctx), ctx->fld<double>(F_SG), fdev, ctx->geo_own(),
+        step, step, step * lam, data_term, u_min, u_max, alpha0, alpha1);
   }
-  ctx->launches += 1 + 2 * (int64_t)iterations;
+  ctx->launches += 1 + (int64_t)iterations;
   if ((rc = launch_err(ctx, "tgv"))) return rc;
+  double* wfin[2] = {sets[iterations & 1].w1, sets[iterations & 1].w2};
+  double* ufin = sets[iterations & 1].u;
   if (w_out) {  // (H, W, 2) interleaved
-    double* wl = w[iterations & 1][0];
-    CK(cudaMemcpy2DAsync(w_out, 2 * sizeof(double), wl, sizeof(double), sizeof(double), N,
+    CK(cudaMemcpy2DAsync(w_out, 2 * sizeof(double), wfin[0], sizeof(double), sizeof(double), N,
                          cudaMemcpyDeviceToHost, s));
-    CK(cudaMemcpy2DAsync(w_out + 1, 2 * sizeof(double), wl + N, sizeof(double), sizeof(double),
+    CK(cudaMemcpy2DAsync(w_out + 1, 2 * sizeof(double), wfin[1], sizeof(double), sizeof(double),
                          N, cudaMemcpyDeviceToHost, s));
   }
-  return d2h_sync(ctx, u_out, ub[iterations & 1], B);
+  return d2h_sync(ctx, u_out, ufin, B);
 }
 
 }  // extern "C"

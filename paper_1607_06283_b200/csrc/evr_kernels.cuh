@@ -272,78 +272,104 @@ __global__ void k_l1_primal(const T* __restrict__ p1, const T* __restrict__ p2,
   v[k] = Arith<T>::mad(nu, T(2), -uk);
 }
 
-// TGV state planes: w (in), w+ (out), w_bar (out), symmetric dual Q
-template <class T> struct TgvPlanes {
-  T *w1, *w2, *w1n, *w2n, *b1, *b2, *q11, *q22, *q12;
+// One TGV iteration in one launch.  Primal half-step: u+ = prox_D(div(A^T p)
+// tau + u), w+ = w + (A^T p + div_sym Q) tau, over-relaxed u_bar = v and
+// w_bar = b, on the pixel and, recomputed bit-identically, on its right and
+// lower neighbours (the values the dual reads there).  Dual half-step on the
+// pixel: p = proj_{alpha1 sqrtG}(p + sigma A (grad u_bar - w_bar)), Q =
+// proj_{alpha0}(Q + sigma E w_bar), |Q|^2 = q11^2 + q22^2 + 2 q12^2.  Every field is ping-ponged (set in
+// -> set out), so the neighbours' reads of set `in` never race this launch's
+// writes; the intermediate planes v, w_bar of the split form disappear.
+template <class T> struct TgvSet {
+  T *u, *w1, *w2, *p1, *p2, *p3, *q11, *q22, *q12;
 };
-
-// TGV primal: u+ = prox_D(div(A^T p)*tau + u), w+ = w + (A^T p + div_sym Q)*tau,
-// over-relaxed u_bar (v) and w_bar
+// Block (32, 8): the primal runs once per pixel of the block's 32 x 8 tile
+// plus its right column and lower row (33 x 9, the halo recomputed), into
+// shared memory; the dual then reads its right / lower neighbours there.
 template <class T>
-__global__ void k_tgv_primal(const T* __restrict__ p1, const T* __restrict__ p2,
-                             const T* __restrict__ p3, CoefPlanes<T> c,
-                             const T* __restrict__ u, const T* __restrict__ sg,
-                             const double* __restrict__ f, T* __restrict__ un,
-                             T* __restrict__ v, TgvPlanes<T> tp, Geo g, T tau, T tl, int kind,
-                             T umin, T umax) {
-  EVR_GEO_INDEX
-  const int H = g.Htot;
-  T qx, qy, qxl = T(0), qyu = T(0), dummy;
-  q_at(c, p1, p2, p3, k, qx, qy);
-  if (j > 0) q_at(c, p1, p2, p3, k - 1, qxl, dummy);
-  if (gi > 0) q_at(c, p1, p2, p3, k - W, dummy, qyu);
-  const T d = div_at(qx, qxl, qy, qyu, gi, j, H, W);
-  const T uk = u[k];
-  const T nu = data_prox(kind, Arith<T>::mad(d, tau, uk), (T)f[k], tl * sg[k], umin, umax);
-  un[k] = nu;
-  v[k] = Arith<T>::mad(nu, T(2), -uk);
-  const T e1 = div_at(tp.q11[k], j > 0 ? tp.q11[k - 1] : T(0), tp.q12[k],
-                      gi > 0 ? tp.q12[k - W] : T(0), gi, j, H, W);
-  const T e2 = div_at(tp.q12[k], j > 0 ? tp.q12[k - 1] : T(0), tp.q22[k],
-                      gi > 0 ? tp.q22[k - W] : T(0), gi, j, H, W);
-  const T w1 = tp.w1[k], w2 = tp.w2[k];
-  const T n1 = Arith<T>::mad(qx + e1, tau, w1), n2 = Arith<T>::mad(qy + e2, tau, w2);
-  tp.w1n[k] = n1;
-  tp.w2n[k] = n2;
-  tp.b1[k] = Arith<T>::mad(n1, T(2), -w1);
-  tp.b2[k] = Arith<T>::mad(n2, T(2), -w2);
-}
-
-// TGV dual: p = proj_{alpha1 sqrtG}(p + sigma A (grad u_bar - w_bar)),
-// Q = proj_{alpha0}(Q + sigma E w_bar), |Q|^2 = q11^2 + q22^2 + 2 q12^2
-template <class T>
-__global__ void k_tgv_dual(const T* __restrict__ v, TgvPlanes<T> tp, T* __restrict__ p1,
-                           T* __restrict__ p2, T* __restrict__ p3, CoefPlanes<T> c,
-                           const T* __restrict__ sg, Geo g, T sigma, T alpha0, T alpha1) {
-  EVR_GEO_INDEX
-  const int H = g.Htot;
+__global__ void __launch_bounds__(256) k_tgv_iter(const TgvSet<T> in, TgvSet<T> out,
+                                                  CoefPlanes<T> c, const T* __restrict__ sg,
+                                                  const double* __restrict__ f, Geo g, T tau,
+                                                  T sigma, T tl, int kind, T umin, T umax,
+                                                  T alpha0, T alpha1) {
+  __shared__ T sv[9][33], sb1[9][33], sb2[9][33];
+  const int W = g.W, H = g.Htot;
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  const int j0 = blockIdx.x * 32, i0 = g.ilo + (int)blockIdx.y * 8;
+  // primal at local row ii, column jj (inside the sensor)
+  auto primal = [&](int ii, int jj, T& nu, T& vv, T& n1, T& n2, T& b1, T& b2) {
+    const int64_t kk = (int64_t)ii * W + jj;
+    const int gii = g.row0 + ii;
+    T qx, qy, qxl = T(0), qyu = T(0), dummy;
+    q_at(c, in.p1, in.p2, in.p3, kk, qx, qy);
+    if (jj > 0) q_at(c, in.p1, in.p2, in.p3, kk - 1, qxl, dummy);
+    if (gii > 0) q_at(c, in.p1, in.p2, in.p3, kk - W, dummy, qyu);
+    const T d = div_at(qx, qxl, qy, qyu, gii, jj, H, W);
+    const T uk = in.u[kk];
+    nu = data_prox(kind, Arith<T>::mad(d, tau, uk), (T)f[kk], tl * sg[kk], umin, umax);
+    vv = Arith<T>::mad(nu, T(2), -uk);
+    const T e1 = div_at(in.q11[kk], jj > 0 ? in.q11[kk - 1] : T(0), in.q12[kk],
+                        gii > 0 ? in.q12[kk - W] : T(0), gii, jj, H, W);
+    const T e2 = div_at(in.q12[kk], jj > 0 ? in.q12[kk - 1] : T(0), in.q22[kk],
+                        gii > 0 ? in.q22[kk - W] : T(0), gii, jj, H, W);
+    const T w1 = in.w1[kk], w2 = in.w2[kk];
+    n1 = Arith<T>::mad(qx + e1, tau, w1);
+    n2 = Arith<T>::mad(qy + e2, tau, w2);
+    b1 = Arith<T>::mad(n1, T(2), -w1);
+    b2 = Arith<T>::mad(n2, T(2), -w2);
+  };
+  const int i = i0 + ty, j = j0 + tx;
+  const bool own = i <= g.ihi && j < W;
+  T nu = T(0), n1 = T(0), n2 = T(0), t0, t1, t2;
+  if (own) primal(i, j, nu, sv[ty][tx], n1, n2, sb1[ty][tx], sb2[ty][tx]);
+  if (tx < 8) {  // the column right of the tile
+    const int ii = i0 + tx, jj = j0 + 32;
+    if (ty == 0 && ii <= g.ihi && jj < W && g.row0 + ii < H)
+      primal(ii, jj, t0, sv[tx][32], t1, t2, sb1[tx][32], sb2[tx][32]);
+  }
+  if (ty == 7) {  // the row below the tile (the corner is never read)
+    const int ii = i0 + 8;
+    if (ii <= g.ihi && g.row0 + ii < H && j < W)
+      primal(ii, j, t0, sv[8][tx], t1, t2, sb1[8][tx], sb2[8][tx]);
+  }
+  __syncthreads();
+  if (!own) return;
+  const int64_t k = (int64_t)i * W + j;
+  const int gi = g.row0 + i;
   const bool xr = j < W - 1, yd = gi < H - 1;
-  const T* b1 = tp.b1;
-  const T* b2 = tp.b2;
-  const T gx = (xr ? v[k + 1] - v[k] : T(0)) - b1[k];
-  const T gy = (yd ? v[k + W] - v[k] : T(0)) - b2[k];
+  out.u[k] = nu;
+  out.w1[k] = n1;
+  out.w2[k] = n2;
+  const T v = sv[ty][tx], b1 = sb1[ty][tx], b2 = sb2[ty][tx];
+  const T vr = xr ? sv[ty][tx + 1] : T(0), b1r = xr ? sb1[ty][tx + 1] : T(0);
+  const T b2r = xr ? sb2[ty][tx + 1] : T(0);
+  const T vd = yd ? sv[ty + 1][tx] : T(0), b1d = yd ? sb1[ty + 1][tx] : T(0);
+  const T b2d = yd ? sb2[ty + 1][tx] : T(0);
+  // dual
+  const T gx = (xr ? vr - v : T(0)) - b1;
+  const T gy = (yd ? vd - v : T(0)) - b2;
   const Coef<T> a = c.at(k);
   const T s11 = sigma * a.a11, s12 = sigma * a.a12, s22 = sigma * a.a22;
   const T s31 = sigma * a.a31, s32 = sigma * a.a32;
-  const T q1 = Arith<T>::mad(s12, gy, Arith<T>::mad(s11, gx, p1[k]));
-  const T q2 = Arith<T>::mad(s22, gy, Arith<T>::mad(s12, gx, p2[k]));
-  const T q3 = Arith<T>::mad(s32, gy, Arith<T>::mad(s31, gx, p3[k]));
+  const T q1 = Arith<T>::mad(s12, gy, Arith<T>::mad(s11, gx, in.p1[k]));
+  const T q2 = Arith<T>::mad(s22, gy, Arith<T>::mad(s12, gx, in.p2[k]));
+  const T q3 = Arith<T>::mad(s32, gy, Arith<T>::mad(s31, gx, in.p3[k]));
   T n = Arith<T>::sqrt(Arith<T>::mad(q3, q3, Arith<T>::mad(q2, q2, q1 * q1)));
   n = vmax(Arith<T>::div(n, alpha1 * sg[k]), T(1));
-  p1[k] = Arith<T>::div(q1, n);
-  p2[k] = Arith<T>::div(q2, n);
-  p3[k] = Arith<T>::div(q3, n);
-  const T e11 = xr ? b1[k + 1] - b1[k] : T(0);
-  const T e22 = yd ? b2[k + W] - b2[k] : T(0);
-  const T e12 = ((yd ? b1[k + W] - b1[k] : T(0)) + (xr ? b2[k + 1] - b2[k] : T(0))) * T(0.5);
-  const T qa = Arith<T>::mad(sigma, e11, tp.q11[k]);
-  const T qb = Arith<T>::mad(sigma, e22, tp.q22[k]);
-  const T qd = Arith<T>::mad(sigma, e12, tp.q12[k]);
-  T m = Arith<T>::sqrt(Arith<T>::mad(qd * qd, T(2), Arith<T>::mad(qb, qb, qa * qa)));
-  m = vmax(Arith<T>::div(m, alpha0), T(1));
-  tp.q11[k] = Arith<T>::div(qa, m);
-  tp.q22[k] = Arith<T>::div(qb, m);
-  tp.q12[k] = Arith<T>::div(qd, m);
+  out.p1[k] = Arith<T>::div(q1, n);
+  out.p2[k] = Arith<T>::div(q2, n);
+  out.p3[k] = Arith<T>::div(q3, n);
+  const T e11 = xr ? b1r - b1 : T(0);
+  const T e22 = yd ? b2d - b2 : T(0);
+  const T e12 = ((yd ? b1d - b1 : T(0)) + (xr ? b2r - b2 : T(0))) * T(0.5);
+  const T qa = Arith<T>::mad(sigma, e11, in.q11[k]);
+  const T qb = Arith<T>::mad(sigma, e22, in.q22[k]);
+  const T qd = Arith<T>::mad(sigma, e12, in.q12[k]);
+  T mq = Arith<T>::sqrt(Arith<T>::mad(qd * qd, T(2), Arith<T>::mad(qb, qb, qa * qa)));
+  mq = vmax(Arith<T>::div(mq, alpha0), T(1));
+  out.q11[k] = Arith<T>::div(qa, mq);
+  out.q22[k] = Arith<T>::div(qb, mq);
+  out.q12[k] = Arith<T>::div(qd, mq);
 }
 
 // dual ascent + ball projection (solve.py:170-201)

@@ -128,10 +128,10 @@ int main(int argc, char** argv) {
     dim3 grid((W + TIW - 1) / TIW, (H + TIH - 1) / TIH);
     if (K == 3)
       k_pd_tile<double, 3, RPT, G, 2, MetricPackF64, false><<<grid, 32 * G>>>(
-          rows(d_st[a], 1), m1, d_st[a ^ 1], H, W, tau, sigma, 1.0, 2.0, 0);
+          rows(d_st[a], 1), m1, d_st[a ^ 1], H, W, tau, sigma, 1.0, 2.0, 0, (double*)nullptr);
     else
       k_pd_tile<double, 4, RPT, G, 2, MetricPackF64, false><<<grid, 32 * G>>>(
-          rows(d_st[a], 1), m1, d_st[a ^ 1], H, W, tau, sigma, 1.0, 2.0, 0);
+          rows(d_st[a], 1), m1, d_st[a ^ 1], H, W, tau, sigma, 1.0, 2.0, 0, (double*)nullptr);
   };
   auto gen1_tv = [&](int K, int a) {
     constexpr int G = 8, RPT = 4;
@@ -232,13 +232,13 @@ int main(int argc, char** argv) {
           const int TIW = 32 - 2 * K, TIH = G * RPT - 2 * K;                                   \
           dim3 grid((W + TIW - 1) / TIW, (H + TIH - 1) / TIH);                                 \
           k_pd_tile<double, K, RPT, G, MINB, MetricPackF64, false><<<grid, 32 * G>>>(          \
-              rows(d_st[a], 1), m1, d_st[a ^ 1], H, W, tau, sigma, 1.0, 2.0, 0);                  \
+              rows(d_st[a], 1), m1, d_st[a ^ 1], H, W, tau, sigma, 1.0, 2.0, 0, (double*)nullptr);                  \
         },                                                                                     \
         K)
-  TV1(3, 3, 8, 2);
-  TV1(2, 3, 8, 2);
-  TV1(2, 4, 8, 2);
-  TV1(4, 4, 8, 2);
-  TV1(2, 2, 8, 3);
+  PD1(3, 3, 8, 2);
+  PD1(2, 3, 8, 2);
+  PD1(2, 4, 8, 2);
+  PD1(2, 2, 8, 3);
+  PD1(2, 2, 12, 2);
   return 0;
 }
