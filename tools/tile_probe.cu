@@ -236,9 +236,22 @@ int main(int argc, char** argv) {
         },                                                                                     \
         K)
   PD1(3, 3, 8, 2);
-  PD1(2, 3, 8, 2);
-  PD1(2, 4, 8, 2);
-  PD1(2, 2, 8, 3);
-  PD1(2, 2, 12, 2);
+#define PDG(K, RPT, OFF)                                                                       \
+  {                                                                                            \
+    auto kern = k_pd_tile64pg<K, RPT>;                                                         \
+    const int smem = 2 * 8 * RPT * 32 * 96;                                                    \
+    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));         \
+    const int TIW = 32 - 2 * K, TIH = 8 * RPT - 2 * K;                                         \
+    const int ntx = (W + TIW - 1) / TIW, nt = ntx * ((H + TIH - 1) / TIH);                     \
+    check("gen2pg pd K" #K " RPT" #RPT " offset " #OFF, 0,                                     \
+          [&](int a) { kern<<<sms, 512, smem>>>(d_st[a], d_c2, d_st[a ^ 1], H, W, ntx, nt, S, OFF); }, \
+          K);                                                                                  \
+    CK(cudaGetLastError());                                                                    \
+  }
+  PDG(3, 3, 0);
+  PDG(3, 3, 1);
+  PDG(3, 3, 2);
+  PDG(3, 3, 3);
+  PDG(3, 4, 1);
   return 0;
 }
