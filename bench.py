@@ -181,6 +181,9 @@ class ClockSampler:
 
 
 def dist_init():
+    """One process per GPU (torchrun): NCCL for the barrier and the
+    max-over-ranks reduction.  EVR_DIST_BACKEND=gloo exercises the same code
+    path where NCCL cannot run (ranks sharing one device in a smoke test)."""
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
@@ -188,8 +191,13 @@ def dist_init():
         import torch
         import torch.distributed as dist
 
+        local = local % max(torch.cuda.device_count(), 1)
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        backend = os.environ.get("EVR_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     return world, rank, local
 
 
@@ -200,6 +208,8 @@ def allmax(x, world, device="cuda"):
     import torch
     import torch.distributed as dist
 
+    if dist.get_backend() != "nccl":
+        device = "cpu"
     t = torch.tensor([x], dtype=torch.float64, device=device)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
@@ -300,7 +310,9 @@ def run_reference(args):
     if int(os.environ.get("RANK", "0")) != 0:
         return 0
     H, W, epp, pd, tv, rate = CONFIGS[args.config]
-    os.environ.setdefault("OMP_NUM_THREADS", str(len(os.sched_getaffinity(0))))
+    # every host core (torchrun presets OMP_NUM_THREADS=1 for its ranks; rank
+    # 0 is the only process of this arm), set before the oracle library loads
+    os.environ["OMP_NUM_THREADS"] = str(len(os.sched_getaffinity(0)))
     n = args.warmup + args.steps
     times, threads = cpu_port_run(H, W, epp, pd, tv, rate, n, seed=1, budget_s=args.ref_budget)
     timed = times[args.warmup:] if len(times) > args.warmup else times[-1:]
@@ -503,7 +515,7 @@ def run_gpu(args):
 
     cpu = numpy_ref = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        os.environ.setdefault("OMP_NUM_THREADS", str(len(os.sched_getaffinity(0))))
+        os.environ["OMP_NUM_THREADS"] = str(len(os.sched_getaffinity(0)))
         times, threads = cpu_port_run(H, W, epp, pd, tv, rate, 400, seed=1,
                                       budget_s=args.cpu_budget)
         times = times[1:] if len(times) > 1 else times
