@@ -459,3 +459,32 @@ def test_streaming_engine_device_early_stop(H, W, precision):
         its.append(res.iterations)
     assert len(per_packet) == 1
     assert min(its) < 40
+
+
+def test_time_iteration_kernel_hook_leaves_state_alone():
+    """evr_time_iteration_kernel (bench.py's live roofline timing) runs the
+    streaming list's tiles on the packed scratch sets only: the next packet
+    gives the same frame as without the timing call."""
+    import ctypes
+
+    from paper_1607_06283_b200 import _lib
+
+    geom = SensorGeometry(width=300, height=400)
+    ev = evr.events_to_array(make_events(2000, geom, seed=12))
+    pk = [ev[:1000], ev[1000:]]
+    mc, sc, th = ManifoldConfig(), SolverConfig(max_iterations=12), Thresholds()
+    a = evr.init_state(geom, sc, engine=1)
+    b = evr.init_state(geom, sc, engine=1)
+    evr.process_packet_arrays(a, pk[0], mc, sc, th)
+    evr.process_packet_arrays(b, pk[0], mc, sc, th)
+    us, k = ctypes.c_float(0), ctypes.c_int(0)
+    for which in (0, 1):
+        b.context().call("evr_time_iteration_kernel", which, 5, ctypes.byref(us), ctypes.byref(k))
+        assert us.value > 0 and k.value >= 2
+    _, fa, _ = evr.process_packet_arrays(a, pk[1], mc, sc, th)
+    _, fb, _ = evr.process_packet_arrays(b, pk[1], mc, sc, th)
+    assert np.array_equal(fa, fb) and np.array_equal(a.p, b.p)
+    with pytest.raises(Exception):  # the resident engine has no iteration kernels
+        st = evr.init_state(GEOM, SolverConfig())
+        evr.process_packet(st, make_events(30), ManifoldConfig(), SolverConfig(), Thresholds())
+        st.context().call("evr_time_iteration_kernel", 0, 5, ctypes.byref(us), None)
