@@ -442,6 +442,22 @@ __device__ __forceinline__ double ldg(const double* p) { return __ldg(p); }
 // row of the band below (y1) -- in place from the neighbours' buffers: peer
 // memory over NVLink when the bands sit on different GPUs, so the halo
 // exchange is part of the iteration kernel itself.
+// Bounds-checked builds (-DEVR_CHECKS=1, tools/build_variants.sh): device
+// asserts on the indices every iteration kernel reads through MarchRows and
+// on the resident engine's exchange slots; a failing check traps the
+// context (the stand-in for compute-sanitizer, closed on this GPU pool)
+#ifndef EVR_CHECKS
+#define EVR_CHECKS 0
+#endif
+#define EVR_ASSERT(c)                                                                  \
+  do {                                                                                 \
+    if (EVR_CHECKS && !(c)) {                                                          \
+      printf("EVR_CHECKS failed: %s (%s:%d) block %d thread %d\n", #c, __FILE__,        \
+             __LINE__, (int)blockIdx.x, (int)threadIdx.x);                             \
+      __trap();                                                                        \
+    }                                                                                  \
+  } while (0)
+
 template <class Q> struct MarchRows {
   const Q* own;
   const Q* up;  // row y0 - 1 of the band above (BANDED only; the tile kernels
@@ -451,15 +467,21 @@ template <class Q> struct MarchRows {
   // element of global row gr (a band's own rows or K rows either side)
   // own row gr (32-bit offsets; the caller knows gr is in [y0, y1))
   __device__ __forceinline__ Q at_own(int gr, int jc, int W) const {
+    EVR_ASSERT(gr >= y0 && gr < y1 && jc >= 0 && jc < W);
     return ldg(own + ((gr - y0 + olo) * W + jc));
   }
   template <bool BANDED> __device__ __forceinline__ Q at(int gr, int jc, int W) const {
-    if constexpr (BANDED)
+    EVR_ASSERT(jc >= 0 && jc < W);
+    if constexpr (BANDED) {
+      // up to 4 rows (the largest tile K) either side, from a neighbour that exists
+      EVR_ASSERT(gr >= y0 - 4 && gr < y1 + 4 && (gr >= y0 || up) && (gr < y1 || dn));
       return ldg(gr < y0   ? up + ((int64_t)(gr - y0 + 1) * W + jc)
                  : gr >= y1 ? dn + ((int64_t)(gr - y1) * W + jc)
                             : own + ((int64_t)(gr - y0 + olo) * W + jc));
-    else
+    } else {
+      EVR_ASSERT(gr >= y0 && gr < y1);
       return ldg(own + (gr * W + jc));
+    }
   }
 };
 

@@ -151,6 +151,7 @@ __global__ void __launch_bounds__(NT, 1) k_resident_col(const ResArgs<T> a) {
   // Rb = last own row -> the band below) as tagged words: nv = 1 (u_bar) or
   // 3 (p1, p2, p3) values in the column's slots
   auto ll_put = [&](int step, int r, int nv, T v0, T v1, T v2) {
+    EVR_ASSERT(col && b < a.nb && (r == 1 || r == Rb));
     unsigned long long w[NCW];
     const unsigned tag = tag_base + (unsigned)step;
     LLWords<T>::pack(v0, tag, w);
@@ -176,6 +177,7 @@ __global__ void __launch_bounds__(NT, 1) k_resident_col(const ResArgs<T> a) {
     const unsigned long long* src[2] = {slot + (size_t)(b - 1) * 2 * xside + xside + jw,
                                         slot + (size_t)(b + 1) * 2 * xside + jw};
     const bool on[2] = {has_up, has_dn};
+    EVR_ASSERT((!has_up || b >= 1) && (!has_dn || b + 1 < a.nb));
     unsigned long long w[2][NCW];
     bool ready;
     if (!col) {
