@@ -2139,8 +2139,30 @@ int evr_op_pd_solve(evr_ctx* ctx, const evr_config* cfg, const double* f, const 
   ctx->launches += 2;
   if ((rc = launch_err(ctx, "pd setup"))) return rc;
   double* saved_f = ctx->f;
-  ctx->f = fdev;  // energy trace reads f
-  rc = solve_host_loop<double>(ctx, *cfg, info, energy_trace, rel_trace, false);
+  ctx->f = fdev;  // energy trace reads f; the fused list's epilogue writes f = u there
+  if (!energy_trace && !rel_trace && !ctx->banded) {
+    // no per-iteration trace: the streaming engine's solve list on this
+    // context's planes -- temporally blocked tiles (rel_change of the last
+    // iteration folded on the device) or, with a tolerance, one march launch
+    // + rel_change per iteration behind the device stop flag; no host round
+    // trip per iteration either way
+    const evr_config saved_cfg = ctx->cfg;
+    ctx->cfg = *cfg;
+    int n = 0;
+    for (const Step& st : packet_steps(ctx->cfg, 1, true, ctx_tile_k(ctx), false))
+      n += launch_step<double>(ctx, st);
+    ctx->cfg = saved_cfg;
+    ctx->launches += n;
+    rc = launch_err(ctx, "pd solve");
+    if (!rc && info) {
+      CK(cudaMemcpyAsync(ctx->h_info, ctx->d_info, sizeof(evr_solve_info), cudaMemcpyDeviceToHost,
+                         s));
+      CK(cudaStreamSynchronize(s));
+      *info = *ctx->h_info;
+    }
+  } else {
+    rc = solve_host_loop<double>(ctx, *cfg, info, energy_trace, rel_trace, false);
+  }
   ctx->f = saved_f;
   if (rc) return rc;
   k_planes_to_aos<double><<<grid1d(N), kNT, 0, s>>>(ctx->fld<double>(F_P1), ctx->fld<double>(F_P2),
