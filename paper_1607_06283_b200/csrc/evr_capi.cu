@@ -65,6 +65,8 @@ struct evr_ctx {
   double* part = nullptr;   // reduction partials
   unsigned* rticket = nullptr;  // k_relchange's last-CTA ticket
   int* d_stop = nullptr;         // fused list, convergence_tol > 0: the stop flag
+  double* d_hist = nullptr;      // traced host-driven solve: per-iteration rel_change | energy
+  int hist_cap = 0;
   double* d_scalar = nullptr;
   int* d_err = nullptr;
   evr_solve_info* d_info = nullptr;
@@ -412,12 +414,12 @@ void launch_pdl(void (*k)(KArgs...), unsigned grid, unsigned block, cudaStream_t
 
 template <class T>
 void relchange(evr_ctx* ctx, const T* un, const T* u, int iterations, int stride = 1,
-               bool early_stop = false) {
+               bool early_stop = false, double* hist = nullptr) {
   const int nb = red_blocks(ctx->own_n());
   launch_pdl(k_relchange<T, kNT>, nb, kNT, ctx->stream, un + ctx->own_off() * stride,
              u + ctx->own_off() * stride, ctx->own_n(), ctx->part, stride, ctx->rticket,
              ctx->d_info, iterations, ctx->d_scalar + 2, early_stop ? ctx->cfg.convergence_tol : 0.0,
-             early_stop ? ctx->d_stop : nullptr);
+             early_stop ? ctx->d_stop : nullptr, hist);
 }
 
 // temporally blocked tiles (evr_tile.cuh): a CTA of G warps covers 32 x
@@ -1132,6 +1134,19 @@ template <class T>
 int solve_host_loop(evr_ctx* ctx, const evr_config& g, evr_solve_info* info, double* etrace,
                     double* rtrace, bool write_state) {
   const bool track = g.convergence_tol > 0 || etrace || rtrace;
+  // without a tolerance the iteration count is fixed: the traces go to a
+  // device history read back once, no host round trip per iteration
+  const bool sync_each = g.convergence_tol > 0;
+  double* hist = nullptr;
+  if (!sync_each && (etrace || rtrace)) {
+    if (ctx->hist_cap < g.max_iterations) {
+      cudaFree(ctx->d_hist);
+      ctx->d_hist = nullptr;
+      CK(cudaMalloc(&ctx->d_hist, sizeof(double) * 2 * g.max_iterations));
+      ctx->hist_cap = g.max_iterations;
+    }
+    hist = ctx->d_hist;  // [rel_change x hist_cap | energy x hist_cap]
+  }
   T* bufs[2] = {ctx->fld<T>(F_U), ctx->fld<T>(F_UN)};
   int iterations = 0, cur_i = 0;
   double rel = INFINITY;
@@ -1146,7 +1161,7 @@ int solve_host_loop(evr_ctx* ctx, const evr_config& g, evr_solve_info* info, dou
     iterations = it + 1;
     ctx->launches += 1;
     if (track || it == g.max_iterations - 1) {
-      relchange<T>(ctx, nxt, cur, iterations);
+      relchange<T>(ctx, nxt, cur, iterations, 1, false, hist);
       ctx->launches += 1;
     }
     k_pd_dual<T><<<grid_geo(own), block2d(), 0, ctx->stream>>>(
@@ -1159,12 +1174,14 @@ int solve_host_loop(evr_ctx* ctx, const evr_config& g, evr_solve_info* info, dou
       k_energy_partial<T, kNT><<<nb, kNT, 0, ctx->stream>>>(nxt, ctx->f, coefs<T>(ctx),
                                                            ctx->fld<T>(F_G), ctx->fld<T>(F_SG),
                                                            ctx->H, ctx->W, ctx->part);
-      k_energy_final<kNT><<<1, kNT, 0, ctx->stream>>>(ctx->part, nb, g.lam, ctx->d_scalar);
+      k_energy_final<kNT><<<1, kNT, 0, ctx->stream>>>(
+          ctx->part, nb, g.lam, hist ? hist + ctx->hist_cap + it : ctx->d_scalar);
       ctx->launches += 2;
-      CK(cudaMemcpyAsync(&etrace[it], ctx->d_scalar, sizeof(double), cudaMemcpyDeviceToHost,
-                         ctx->stream));
+      if (!hist)
+        CK(cudaMemcpyAsync(&etrace[it], ctx->d_scalar, sizeof(double), cudaMemcpyDeviceToHost,
+                           ctx->stream));
     }
-    if (track) {
+    if (sync_each) {
       CK(cudaMemcpyAsync(ctx->h_info, ctx->d_info, sizeof(evr_solve_info),
                          cudaMemcpyDeviceToHost, ctx->stream));
       CK(cudaStreamSynchronize(ctx->stream));
@@ -1184,12 +1201,20 @@ int solve_host_loop(evr_ctx* ctx, const evr_config& g, evr_solve_info* info, dou
   }
   int rc = launch_err(ctx, "solve loop");
   if (rc) return rc;
+  if (hist) {
+    if (rtrace)
+      CK(cudaMemcpyAsync(rtrace, hist, sizeof(double) * iterations, cudaMemcpyDeviceToHost,
+                         ctx->stream));
+    if (etrace)
+      CK(cudaMemcpyAsync(etrace, hist + ctx->hist_cap, sizeof(double) * iterations,
+                         cudaMemcpyDeviceToHost, ctx->stream));
+  }
   CK(cudaMemcpyAsync(ctx->h_info, ctx->d_info, sizeof(evr_solve_info), cudaMemcpyDeviceToHost,
                      ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
   if (info) {
     info->iterations = iterations;
-    info->rel_change = track ? rel : ctx->h_info->rel_change;
+    info->rel_change = sync_each ? rel : ctx->h_info->rel_change;
   }
   return EVR_OK;
 }
@@ -1461,6 +1486,7 @@ void evr_destroy(evr_ctx* ctx) {
   drop_graphs(ctx);
   cudaFree(ctx->slab);
   cudaFree(ctx->d_stop);
+  cudaFree(ctx->d_hist);
   cudaFree(ctx->d_pack);
   cudaFree(ctx->f);
   cudaFree(ctx->raw);

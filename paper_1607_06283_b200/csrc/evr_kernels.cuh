@@ -828,7 +828,7 @@ template <class T, int NT>
 __global__ void __launch_bounds__(NT)
 k_relchange(const T* __restrict__ un, const T* __restrict__ u, int64_t N, double* part,
             int stride, unsigned* ticket, evr_solve_info* info, int iterations, double* sums,
-            double tol = 0.0, int* stop = nullptr) {
+            double tol = 0.0, int* stop = nullptr, double* hist = nullptr) {
   __shared__ double sh[NT / 32];
   __shared__ bool last;
   pdl_wait_and_release();
@@ -868,6 +868,7 @@ k_relchange(const T* __restrict__ un, const T* __restrict__ u, int64_t N, double
     const double rel = sqrt(d) / (den > 1e-30 ? den : 1e-30);
     info->rel_change = rel;
     info->iterations = iterations;
+    if (hist) hist[iterations - 1] = rel;  // per-iteration trace, read back once
     sums[0] = d;  // evr_group folds the bands' sums
     sums[1] = o;
     *ticket = 0u;
