@@ -553,6 +553,58 @@ int launch_tv_tile(evr_ctx* ctx, int K, const MarchRows<Q4<T>>& in, const MarchR
     tv_tile_shape<T, false>(ctx, K, in, f0, out, sigma, tau, shrink, early);
   return 1;
 }
+// Clustered primal-dual tiles (k_pd_tile<..., CX, CY>): EVR_TILE_CLUSTER
+// = "CXxCY" (2x2, 4x2, 2x4; unset or 1x1 = the one-CTA regions).
+int env_tile_cluster() {
+  static const int env = [] {
+    const char* e = getenv("EVR_TILE_CLUSTER");
+    if (!e) return 0;
+    if (!strcmp(e, "2x2")) return 22;
+    if (!strcmp(e, "4x2")) return 42;
+    if (!strcmp(e, "2x4")) return 24;
+    return 0;
+  }();
+  return env;
+}
+template <class... KArgs, class... Args>
+void launch_cluster(void (*k)(KArgs...), dim3 grid, unsigned block, int cx, int cy,
+                    cudaStream_t s, Args&&... args) {
+  cudaLaunchConfig_t lc{};
+  lc.gridDim = grid;
+  lc.blockDim = dim3(block);
+  lc.stream = s;
+  cudaLaunchAttribute at[2];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = cx;
+  at[0].val.clusterDim.y = cy;
+  at[0].val.clusterDim.z = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[1].val.programmaticStreamSerializationAllowed = 1;
+  lc.attrs = at;
+  lc.numAttrs = pdl_enabled() ? 2 : 1;
+  cudaLaunchKernelEx(&lc, k, std::forward<Args>(args)...);
+}
+template <class T, int K, int RPT, int CX, int CY, class M>
+void pd_tile_cl(evr_ctx* ctx, const MarchRows<Q4<T>>& in, const M& m, Q4<T>* out, T tau,
+                T sigma, T lo, T hi, int early, T* prev) {
+  constexpr int G = TileShape<T>::G, MB = TileShape<T>::MINB;
+  constexpr int TIW = 32 * CX - 2 * K, TIH = G * RPT * CY - 2 * K;
+  const int rows = ctx->own_hi - ctx->own_lo + 1;
+  const dim3 grid(CX * ((ctx->W + TIW - 1) / TIW), CY * ((rows + TIH - 1) / TIH));
+  launch_cluster(prev ? k_pd_tile<T, K, RPT, G, MB, M, false, DT_KL, true, CX, CY>
+                      : k_pd_tile<T, K, RPT, G, MB, M, false, DT_KL, false, CX, CY>,
+                 grid, 32 * G, CX, CY, ctx->stream, in, m, out, ctx->Htot, ctx->W, tau, sigma, lo,
+                 hi, early, prev);
+}
+template <class T, int K, int RPT, class M>
+bool pd_tile_cluster(evr_ctx* ctx, int shape, const MarchRows<Q4<T>>& in, const M& m,
+                     Q4<T>* out, T tau, T sigma, T lo, T hi, int early, T* prev) {
+  if (shape == 22) pd_tile_cl<T, K, RPT, 2, 2>(ctx, in, m, out, tau, sigma, lo, hi, early, prev);
+  else if (shape == 42) pd_tile_cl<T, K, RPT, 4, 2>(ctx, in, m, out, tau, sigma, lo, hi, early, prev);
+  else if (shape == 24) pd_tile_cl<T, K, RPT, 2, 4>(ctx, in, m, out, tau, sigma, lo, hi, early, prev);
+  else return false;
+  return true;
+}
 // step: tau = sigma for operator solves (no context config); < 0 = the config's
 template <class T, int RPT, bool B, class M, int DT = DT_KL>
 void pd_tile_rpt(evr_ctx* ctx, int K, const MarchRows<Q4<T>>& in, const M& m, Q4<T>* out,
@@ -563,6 +615,13 @@ void pd_tile_rpt(evr_ctx* ctx, int K, const MarchRows<Q4<T>>& in, const M& m, Q4
   cudaStream_t s = ctx->stream;
   const T tau = (T)(step < 0 ? g.tau : step), sigma = (T)(step < 0 ? g.sigma : step);
   const T lo = (T)g.u_min, hi = (T)g.u_max;
+  if constexpr (!B && DT == DT_KL && std::is_same<T, double>::value) {
+    const int cl = env_tile_cluster();
+    if (cl && K == 3 && pd_tile_cluster<T, 3, RPT>(ctx, cl, in, m, out, tau, sigma, lo, hi, early, prev))
+      return;
+    if (cl && K == 4 && pd_tile_cluster<T, 4, RPT>(ctx, cl, in, m, out, tau, sigma, lo, hi, early, prev))
+      return;
+  }
   if (K == 2)
     launch_pdl2(prev ? k_pd_tile<T, 2, RPT, G, MB, M, B, DT, !B> : k_pd_tile<T, 2, RPT, G, MB, M, B, DT>,
                 tile_grid<T, 2, RPT>(ctx), 32 * G, s, in, m, out, H, W, tau, sigma, lo, hi, early,

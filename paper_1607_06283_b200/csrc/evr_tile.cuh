@@ -30,6 +30,7 @@
 
 #include <type_traits>
 
+#include "evr_cluster.cuh"
 #include "evr_fastdp.cuh"
 #include "evr_kernels.cuh"
 
@@ -196,20 +197,54 @@ k_tv_tile(const MarchRows<Q4<T>> in, const MarchRows<T> f0, Q4<T>* __restrict__ 
 // (float64 operator solves): 0 = KL (packed slots beta, 4 beta f), 1 = ROF
 // (rof_manifold_solve, solve.py:285-287: slots 1 / (1 + w), w f), 2 = L1
 // (slots w = tau lam sqrtG, f; the soft shrink of k_l1_primal).
+//
+// Clustered form (CX x CY > 1, launched with cluster dims {CX, CY}): the
+// region is the cluster's, CX*32 columns x CY*G*RPT rows, one 32 x G*RPT
+// block per CTA, and only its outer edge is halo.  Inside the cluster a
+// half-step's one missing neighbour value crosses to the adjacent CTA
+// through DSMEM: q of the right / lower edge into the right / lower CTA
+// before the primal, v of the left / upper edge into the left / upper CTA
+// before the dual, each st.async counting its bytes off the receiver's
+// mbarrier.  One buffer per direction suffices: a CTA sends its next value
+// into a neighbour only after receiving the neighbour's reply to the last.
 enum : int { DT_KL = 0, DT_ROF = 1, DT_L1 = 2 };
 template <class T, int K, int RPT, int G, int MINB, class M, bool BANDED, int DT = DT_KL,
-          bool PREV = false>
+          bool PREV = false, int CX = 1, int CY = 1>
 __global__ void __launch_bounds__(32 * G, MINB)
 k_pd_tile(const MarchRows<Q4<T>> in, M m, Q4<T>* __restrict__ out, int H, int W, T tau,
           T sigma, T umin, T umax, int early, T* __restrict__ prev) {
-  constexpr int RH = G * RPT, TIW = 32 - 2 * K, TIH = RH - 2 * K;
+  constexpr bool CL = CX * CY > 1;
+  constexpr int RH = G * RPT, CW = 32 * CX, CH = RH * CY, TIW = CW - 2 * K, TIH = CH - 2 * K;
   __shared__ T qy_bot[G][32];  // qy of each warp's last row
   __shared__ T v_top[G][32];   // v of each warp's first row
+  __shared__ T x_qx[CL ? RH : 1], x_qy[CL ? 32 : 1];  // from the left / upper CTA
+  __shared__ T x_vr[CL ? RH : 1], x_vb[CL ? 32 : 1];  // from the right / lower CTA
+  __shared__ uint64_t x_bar[2];                       // primal-in, dual-in
   const int l = threadIdx.x & 31, g = threadIdx.x >> 5;
+  const int cx = CL ? (int)blockIdx.x % CX : 0, cy = CL ? (int)blockIdx.y % CY : 0;
   const int y0 = BANDED ? in.y0 : 0, y1 = BANDED ? in.y1 : H;
   const int rlo = max(y0 - K, 0), rhi = min(y1 + K, H) - 1;
-  const int gj = (int)blockIdx.x * TIW - K + l;
-  const int gi0 = y0 + (int)blockIdx.y * TIH - K + g * RPT;
+  const int gj = (int)blockIdx.x / CX * TIW - K + cx * 32 + l;
+  const int gi0 = y0 + (int)blockIdx.y / CY * TIH - K + cy * RH + g * RPT;
+  // bytes each half-step receives (0: an outer side of the cluster)
+  const unsigned in_p = (cx > 0 ? RH * sizeof(T) : 0) + (cy > 0 ? 32 * sizeof(T) : 0);
+  const unsigned in_d = (cx < CX - 1 ? RH * sizeof(T) : 0) + (cy < CY - 1 ? 32 * sizeof(T) : 0);
+  unsigned to_r = 0, to_b = 0, to_l = 0, to_a = 0;  // mapped slot bases in the neighbours
+  unsigned me = 0;
+  if constexpr (CL) {
+    me = cl_rank();
+    EVR_ASSERT(me == (unsigned)(cx + cy * CX));
+    if (threadIdx.x == 0) {
+      cl_bar_init(&x_bar[0]);
+      cl_bar_init(&x_bar[1]);
+      cl_fence_init();
+    }
+    cl_arrive();  // released; waited for after the loads, before the first send
+    if (cx < CX - 1) to_r = cl_map(smem_addr(x_qx), me + 1);
+    if (cy < CY - 1) to_b = cl_map(smem_addr(x_qy), me + CX);
+    if (cx > 0) to_l = cl_map(smem_addr(x_vr), me - 1);
+    if (cy > 0) to_a = cl_map(smem_addr(x_vb), me - CX);
+  }
   const int jc = min(max(gj, 0), W - 1);
   T p1[RPT], p2[RPT], p3[RPT], u[RPT];
   Coef<T> cf[RPT];
@@ -257,8 +292,15 @@ k_pd_tile(const MarchRows<Q4<T>> in, M m, Q4<T>* __restrict__ out, int H, int W,
     m.finish(craw[r], cf[r], sg[r], beta[r], fb[r]);
     if constexpr (sizeof(T) == 8) ysg[r] = fdp_recip(sg[r]);
   }
-  const int ry0 = gi0 - g * RPT, rx0 = (int)blockIdx.x * TIW - K;
+  const int ry0 = gi0 - g * RPT, rx0 = (int)blockIdx.x / CX * TIW - K + cx * 32;
   const bool interior = ry0 >= 1 && ry0 + RH <= H - 1 && rx0 >= 1 && rx0 + 32 <= W - 1;
+  if constexpr (CL) cl_sync_wait();  // every CTA's barriers initialised
+  // the kept pixels: the cluster region's interior
+  auto keep_col = [&] { return cx * 32 + l >= K && cx * 32 + l < CW - K && gj < W; };
+  auto keep_row = [&](int r) {
+    const int R = cy * RH + g * RPT + r;
+    return R >= K && R < CH - K;
+  };
   auto iterate = [&](auto interior_c) {
     constexpr bool IN = decltype(interior_c)::value;
     const bool XR = IN || gj < W - 1;
@@ -270,11 +312,11 @@ k_pd_tile(const MarchRows<Q4<T>> in, M m, Q4<T>* __restrict__ out, int H, int W,
 #pragma unroll 1
     for (int it = 0; it < K; ++it) {
       if (PREV && it == K - 1) {  // the final launch: u before the last iteration
-        if (l >= K && l < 32 - K && gj < W) {  // (k_unpack_rel's rel_change)
+        if (keep_col()) {  // (k_unpack_rel's rel_change)
   #pragma unroll
           for (int r = 0; r < RPT; ++r) {
-            const int R = g * RPT + r, gi = gi0 + r;
-            if (R >= K && R < RH - K && gi < y1)
+            const int gi = gi0 + r;
+            if (keep_row(r) && gi < y1)
               prev[(int64_t)(gi - y0 + (BANDED ? in.olo : 0)) * W + gj] = u[r];
           }
         }
@@ -283,15 +325,32 @@ k_pd_tile(const MarchRows<Q4<T>> in, M m, Q4<T>* __restrict__ out, int H, int W,
   #pragma unroll
       for (int r = 0; r < RPT; ++r) q_of(cf[r], p1[r], p2[r], p3[r], qx[r], qy[r]);
       qy_bot[g][l] = qy[RPT - 1];
+      if constexpr (CL) {
+        if (to_r && l == 31) {
+          const unsigned bar = cl_map(smem_addr(&x_bar[0]), me + 1);
+  #pragma unroll
+          for (int r = 0; r < RPT; ++r) cl_send(to_r + (g * RPT + r) * sizeof(T), qx[r], bar);
+        }
+        if (to_b && g == G - 1)
+          cl_send(to_b + l * sizeof(T), qy[RPT - 1], cl_map(smem_addr(&x_bar[0]), me + CX));
+      }
       __syncthreads();
-      const T qy_above = qy_bot[g > 0 ? g - 1 : g][l];
+      T qy_above = qy_bot[g > 0 ? g - 1 : g][l];
+      if constexpr (CL) {
+        if (in_p) {
+          if (threadIdx.x == 0) cl_expect(&x_bar[0], in_p);
+          cl_wait(&x_bar[0], it & 1);
+        }
+        if (g == 0 && cy > 0) qy_above = x_qy[l];
+      }
       {
         T d[RPT], nu[RPT];
         bool slow = false;
   #pragma unroll
         for (int r = 0; r < RPT; ++r) {  // primal (solve.py:233-245)
           const int gi = gi0 + r;
-          const T qxl = __shfl_up_sync(0xffffffffu, qx[r], 1);
+          T qxl = __shfl_up_sync(0xffffffffu, qx[r], 1);
+          if (CL && l == 0 && cx > 0) qxl = x_qx[g * RPT + r];
           const T qyu = r > 0 ? qy[r - 1] : qy_above;
           d[r] = DIV(qx[r], qxl, qy[r], qyu, gi);
           if constexpr (DT == DT_ROF) {
@@ -316,15 +375,32 @@ k_pd_tile(const MarchRows<Q4<T>> in, M m, Q4<T>* __restrict__ out, int H, int W,
         }
       }
       v_top[g][l] = v[0];
+      if constexpr (CL) {
+        if (to_l && l == 0) {
+          const unsigned bar = cl_map(smem_addr(&x_bar[1]), me - 1);
+  #pragma unroll
+          for (int r = 0; r < RPT; ++r) cl_send(to_l + (g * RPT + r) * sizeof(T), v[r], bar);
+        }
+        if (to_a && g == 0)
+          cl_send(to_a + l * sizeof(T), v[0], cl_map(smem_addr(&x_bar[1]), me - CX));
+      }
       __syncthreads();
-      const T v_below = v_top[g < G - 1 ? g + 1 : g][l];
+      T v_below = v_top[g < G - 1 ? g + 1 : g][l];
+      if constexpr (CL) {
+        if (in_d) {
+          if (threadIdx.x == 0) cl_expect(&x_bar[1], in_d);
+          cl_wait(&x_bar[1], it & 1);
+        }
+        if (g == G - 1 && cy < CY - 1) v_below = x_vb[l];
+      }
       if constexpr (sizeof(T) == 8) {
         T gx[RPT], gy[RPT], n1[RPT], n2[RPT], n3[RPT], nn[RPT];
         bool slow = false, proj = false;
   #pragma unroll
         for (int r = 0; r < RPT; ++r) {  // dual (solve.py:246-252)
           const int gi = gi0 + r;
-          const T vr = __shfl_down_sync(0xffffffffu, v[r], 1);
+          T vr = __shfl_down_sync(0xffffffffu, v[r], 1);
+          if (CL && l == 31 && cx < CX - 1) vr = x_vr[g * RPT + r];
           const T vd = r < RPT - 1 ? v[r + 1] : v_below;
           gx[r] = XR ? vr - v[r] : T(0);
           gy[r] = YD(gi) ? vd - v[r] : T(0);
@@ -358,7 +434,8 @@ k_pd_tile(const MarchRows<Q4<T>> in, M m, Q4<T>* __restrict__ out, int H, int W,
   #pragma unroll
         for (int r = 0; r < RPT; ++r) {  // dual (solve.py:246-252)
           const int gi = gi0 + r;
-          const T vr = __shfl_down_sync(0xffffffffu, v[r], 1);
+          T vr = __shfl_down_sync(0xffffffffu, v[r], 1);
+          if (CL && l == 31 && cx < CX - 1) vr = x_vr[g * RPT + r];
           const T vd = r < RPT - 1 ? v[r + 1] : v_below;
           const T gx = XR ? vr - v[r] : T(0);
           const T gy = YD(gi) ? vd - v[r] : T(0);
@@ -373,11 +450,11 @@ k_pd_tile(const MarchRows<Q4<T>> in, M m, Q4<T>* __restrict__ out, int H, int W,
     iterate(std::true_type{});
   else
     iterate(std::false_type{});
-  if (l < K || l >= 32 - K || gj >= W) return;
+  if (!keep_col()) return;
 #pragma unroll
   for (int r = 0; r < RPT; ++r) {
-    const int R = g * RPT + r, gi = gi0 + r;
-    if (R >= K && R < RH - K && gi < y1)
+    const int gi = gi0 + r;
+    if (keep_row(r) && gi < y1)
       out[(int64_t)(gi - y0 + (BANDED ? in.olo : 0)) * W + gj] = Q4<T>{p1[r], p2[r], p3[r], u[r]};
   }
 }
