@@ -20,6 +20,7 @@ for v in rof l1 tgv; do
 done
 python bench.py --config C5 --bands 2 --steps 20 --warmup 3 > $O/bench_C5_bands2_1gpu.json 2>&1
 for fz in 0 3; do EVR_FUSE=$fz python bench.py --steps 200 --warmup 10 --no-cpu-baseline > $O/bench_C3_f64_fuse$fz.json 2>&1; done
+for cl in 2x2 4x2; do EVR_TILE_CLUSTER=$cl python bench.py --steps 100 --warmup 5 --no-cpu-baseline > $O/bench_C3_f64_cluster$cl.json 2>&1; done
 ncu --metrics gpu__time_duration.sum --clock-control none --csv -c 300 --log-file $O/launches_C3_f64.csv \
     python bench.py --steps 2 --warmup 3 --no-cpu-baseline > /dev/null 2>&1
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches_C2_f64.csv \
