@@ -513,6 +513,15 @@ def run_gpu(args):
     assert got == args.steps
     e2e = world * epp * args.steps / e2e_s
 
+    # the north-star's real-time target is stated "within tolerance" (log u
+    # within 1e-4 of the reference after the same iterations): the float32
+    # engine on the same packets, device-resident and end to end, reported
+    # beside the float64 line (not the line's value)
+    alt = None
+    if args.precision == "f64" and not args.no_f32_leg:
+        alt = float32_leg(args, evr, _lib, torch, world, local, packets, wins, pinned, n_total,
+                          flush, H, W, epp, pd, mc, sc, th, engine)
+
     cpu = numpy_ref = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         os.environ["OMP_NUM_THREADS"] = str(len(os.sched_getaffinity(0)))
@@ -550,12 +559,77 @@ def run_gpu(args):
             "clocks": clocks.summary(),
             "cpu_baseline": cpu,
         }
+        if alt is not None:
+            line["float32_within_tolerance"] = alt
         print(json.dumps(line), flush=True)
     if world > 1:
         import torch.distributed as dist
 
         dist.destroy_process_group()
     return 0
+
+
+def float32_leg(args, evr, _lib, torch, world, local, packets, wins, pinned, n_total, flush, H,
+                W, epp, pd, mc, sc, th, engine):
+    """The float32 engine on the float64 line's packets: the device-resident
+    leg (CUDA events per step, L2 flushed before each) and the streaming e2e
+    leg, max over ranks like the line itself."""
+    L = _lib.lib()
+    st = evr.init_state(evr.SensorGeometry(W, H), sc, precision=1, engine=engine)
+    ctx = st.context()
+    evr.pipeline._prepare(st, mc, sc, th)
+    h = ctx.handle
+    stream = torch.cuda.ExternalStream(L.evr_stream(h), device=local)
+    allev = np.concatenate(packets[:n_total])
+    dev_ev = torch.from_numpy(allev.view(np.uint8)).to("cuda")
+    base = dev_ev.data_ptr()
+
+    def dev_packet(k):
+        _lib.check(h, L.evr_process_packet_device(h, ctypes.c_void_p(base + 16 * epp * k), epp,
+                                                  wins[k]), "packet")
+
+    for k in range(args.warmup):
+        dev_packet(k)
+    torch.cuda.synchronize()
+    L.evr_synchronize(h, None)
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    barrier(world)
+    torch.cuda.synchronize()
+    for i in range(args.steps):
+        with torch.cuda.stream(stream):
+            flush.zero_()
+            starts[i].record(stream)
+        dev_packet(args.warmup + i)
+        with torch.cuda.stream(stream):
+            ends[i].record(stream)
+    torch.cuda.synchronize()
+    L.evr_synchronize(h, None)
+    barrier(world)
+    dev_s = allmax(sum(s.elapsed_time(e) for s, e in zip(starts, ends)) / 1e3, world)
+    st3 = evr.init_state(evr.SensorGeometry(W, H), sc, precision=1, engine=engine)
+    for _ in evr.stream_packets(st3, pinned[:args.warmup], mc, sc, th):
+        pass
+    torch.cuda.synchronize()
+    barrier(world)
+    t0 = time.perf_counter()
+    got = 0
+    for frame, res in evr.stream_packets(st3, pinned[args.warmup:n_total], mc, sc, th):
+        got += int(frame is not None and res.iterations == pd)
+    e2e_s = allmax(time.perf_counter() - t0, world)
+    assert got == args.steps
+    return {
+        "dtype": "f32", "value": round(world * epp * args.steps / dev_s, 1), "unit": "events/s",
+        "ms_per_step": round(dev_s * 1e3 / args.steps, 5),
+        "frames_per_s": round(world * args.steps / dev_s, 2),
+        "e2e": {"value": round(world * epp * args.steps / e2e_s, 1), "unit": "events/s",
+                "api": "stream_packets (as the line's e2e)"},
+        "engine": f"{st.engine()}: {ctx.engine_detail()}",
+        "tolerance": "log u within 1e-4 max-abs of the float64 engine (bit-exact with the "
+                     "reference) after the same iterations: the north-star's criterion; "
+                     "enforced over 300 chained DVS128 packets and 50 / 30 chained 1280x720 "
+                     "packets by tests/test_gpu_long_chains.py (worst 2.8e-5)",
+    }
 
 
 def run_bands(args):
@@ -699,6 +773,8 @@ def main():
     ap.add_argument("--ref-budget", type=float, default=240.0,
                     help="--impl reference: stop after this many seconds of packets")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-f32-leg", action="store_true",
+                    help="skip the float32-within-tolerance leg of a float64 line")
     args = ap.parse_args()
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")
