@@ -584,6 +584,79 @@ void launch_cluster(void (*k)(KArgs...), dim3 grid, unsigned block, int cx, int 
   lc.numAttrs = pdl_enabled() ? 2 : 1;
   cudaLaunchKernelEx(&lc, k, std::forward<Args>(args)...);
 }
+// TMA region loads (k_pd_tile with MetricPackF64Tma): EVR_TILE_TMA=1
+bool env_tile_tma() {
+  static const bool env = [] {
+    const char* e = getenv("EVR_TILE_TMA");
+    return e && atoi(e) != 0;
+  }();
+  return env;
+}
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no libcuda link)
+using TmaEncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                 const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                 const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                 CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+TmaEncodeFn tma_encode_fn() {
+  static TmaEncodeFn fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) !=
+            cudaSuccess || q != cudaDriverEntryPointSuccess)
+      p = nullptr;
+    return reinterpret_cast<TmaEncodeFn>(p);
+  }();
+  return fn;
+}
+// a whole-sensor plane of `per_px` doubles per pixel as a 2-D tensor, boxes
+// of RH rows x 32 pixels
+bool tma_plane(CUtensorMap* tm, const void* base, int W, int H, int per_px, int RH) {
+  const TmaEncodeFn fn = tma_encode_fn();
+  if (!fn) return false;
+  const cuuint64_t dims[2] = {(cuuint64_t)per_px * W, (cuuint64_t)H};
+  const cuuint64_t strides[1] = {(cuuint64_t)per_px * W * sizeof(double)};
+  const cuuint32_t box[2] = {(cuuint32_t)(32 * per_px), (cuuint32_t)RH};
+  const cuuint32_t estr[2] = {1, 1};
+  return fn(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<void*>(base), dims, strides, box,
+            estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+template <class... KArgs, class... Args>
+void launch_pdl_smem(void (*k)(KArgs...), dim3 grid, unsigned block, size_t smem, cudaStream_t s,
+                     Args&&... args) {
+  cudaLaunchConfig_t lc{};
+  lc.gridDim = grid;
+  lc.blockDim = dim3(block);
+  lc.dynamicSmemBytes = smem;
+  lc.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  lc.attrs = at;
+  lc.numAttrs = pdl_enabled() ? 1 : 0;
+  cudaLaunchKernelEx(&lc, k, std::forward<Args>(args)...);
+}
+template <int K, int RPT>
+bool pd_tile_tma(evr_ctx* ctx, const MarchRows<Q4<double>>& in, const MetricPackF64& m,
+                 Q4<double>* out, double tau, double sigma, double lo, double hi, int early,
+                 double* prev) {
+  constexpr int G = TileShape<double>::G, MB = TileShape<double>::MINB, RH = G * RPT;
+  if (ctx->banded) return false;
+  MetricPackF64Tma mt;
+  static_cast<MetricPackF64&>(mt) = m;
+  if (!tma_plane(&mt.tc, m.c, ctx->W, ctx->Htot, 8, RH) ||
+      !tma_plane(&mt.ts, in.own, ctx->W, ctx->Htot, 4, RH))
+    return false;
+  constexpr size_t smem = (size_t)RH * 32 * 3 * sizeof(Q4<double>);
+  auto k = prev ? k_pd_tile<double, K, RPT, G, MB, MetricPackF64Tma, false, DT_KL, true>
+                : k_pd_tile<double, K, RPT, G, MB, MetricPackF64Tma, false, DT_KL, false>;
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout,
+                       cudaSharedmemCarveoutMaxShared);  // two CTAs' boxes per SM
+  launch_pdl_smem(k, tile_grid<double, K, RPT>(ctx), 32 * G, smem, ctx->stream, in, mt, out,
+                  ctx->Htot, ctx->W, tau, sigma, lo, hi, early, prev);
+  return true;
+}
 template <class T, int K, int RPT, int CX, int CY, class M>
 void pd_tile_cl(evr_ctx* ctx, const MarchRows<Q4<T>>& in, const M& m, Q4<T>* out, T tau,
                 T sigma, T lo, T hi, int early, T* prev) {
@@ -615,6 +688,12 @@ void pd_tile_rpt(evr_ctx* ctx, int K, const MarchRows<Q4<T>>& in, const M& m, Q4
   cudaStream_t s = ctx->stream;
   const T tau = (T)(step < 0 ? g.tau : step), sigma = (T)(step < 0 ? g.sigma : step);
   const T lo = (T)g.u_min, hi = (T)g.u_max;
+  if constexpr (!B && DT == DT_KL && std::is_same<M, MetricPackF64>::value) {
+    if (env_tile_tma() && !env_tile_cluster()) {
+      if (K == 3 && pd_tile_tma<3, RPT>(ctx, in, m, out, tau, sigma, lo, hi, early, prev)) return;
+      if (K == 4 && pd_tile_tma<4, RPT>(ctx, in, m, out, tau, sigma, lo, hi, early, prev)) return;
+    }
+  }
   if constexpr (!B && DT == DT_KL && std::is_same<T, double>::value) {
     const int cl = env_tile_cluster();
     if (cl && K == 3 && pd_tile_cluster<T, 3, RPT>(ctx, cl, in, m, out, tau, sigma, lo, hi, early, prev))

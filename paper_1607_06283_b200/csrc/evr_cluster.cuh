@@ -60,6 +60,16 @@ __device__ __forceinline__ void cl_send(unsigned ra, float v, unsigned rb) {
                "r"(__float_as_uint(v)), "r"(rb)
                : "memory");
 }
+// the TMA engine: a 2-D box of a tensor (descriptor in param / global
+// space) into this CTA's shared memory, completing on bar
+__device__ __forceinline__ void tma_load_2d(void* dst, const void* tmap, int x, int y,
+                                            uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];" ::"r"(smem_addr(dst)),
+      "l"(reinterpret_cast<uint64_t>(tmap)), "r"(x), "r"(y), "r"(smem_addr(bar))
+      : "memory");
+}
 __device__ __forceinline__ void cl_arrive() {
   asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
 }

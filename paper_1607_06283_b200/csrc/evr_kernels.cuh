@@ -9,6 +9,8 @@
 // the ABI boundary only.
 #pragma once
 
+#include <cuda.h>  // CUtensorMap
+
 #include <cstdint>
 
 #include "evr_ingest.cuh"
@@ -570,6 +572,7 @@ k_tv_march(const Q4<T>* __restrict__ own, const MarchRows<Q4<T>> in, const T* __
 
 // metric inputs of the primal-dual iteration, from the packed constants
 struct MetricPackF32 {
+  static constexpr bool kTma = false;
   const Q4<float>* __restrict__ c;  // {tx, ty, fb, 0}, the context's own rows
   MarchRows<Q4<float>> rows;        // a band's neighbour rows
   float tl;                         // tau * lam (solve.py:227)
@@ -596,6 +599,7 @@ struct MetricPackF32 {
   }
 };
 struct MetricPackF64 {
+  static constexpr bool kTma = false;
   const Q4<double>* __restrict__ c;  // {a11, a12, a22, a31}, {a32, sqrtG, beta, fb}
   MarchRows<Q4<double>> rows;        // a band's neighbour rows (E = 2)
   struct Raw {
@@ -624,6 +628,14 @@ struct MetricPackF64 {
     beta = r.b.z;
     fb = r.b.w;
   }
+};
+// MetricPackF64 plus TMA descriptors of the packed constants (tc: 8 doubles
+// per pixel) and of the launch's input state (ts: 4 doubles per pixel), whole
+// sensor; a tile kernel taking it loads its region with two 2-D tensor copies
+// into shared memory (k_pd_tile's TMA form)
+struct MetricPackF64Tma : MetricPackF64 {
+  static constexpr bool kTma = true;
+  CUtensorMap tc, ts;
 };
 template <class T> struct MetricPack;
 template <> struct MetricPack<float> { using type = MetricPackF32; };

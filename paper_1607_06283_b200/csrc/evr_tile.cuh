@@ -211,7 +211,7 @@ enum : int { DT_KL = 0, DT_ROF = 1, DT_L1 = 2 };
 template <class T, int K, int RPT, int G, int MINB, class M, bool BANDED, int DT = DT_KL,
           bool PREV = false, int CX = 1, int CY = 1>
 __global__ void __launch_bounds__(32 * G, MINB)
-k_pd_tile(const MarchRows<Q4<T>> in, M m, Q4<T>* __restrict__ out, int H, int W, T tau,
+k_pd_tile(const MarchRows<Q4<T>> in, const __grid_constant__ M m, Q4<T>* __restrict__ out, int H, int W, T tau,
           T sigma, T umin, T umax, int early, T* __restrict__ prev) {
   constexpr bool CL = CX * CY > 1;
   constexpr int RH = G * RPT, CW = 32 * CX, CH = RH * CY, TIW = CW - 2 * K, TIH = CH - 2 * K;
@@ -278,14 +278,53 @@ k_pd_tile(const MarchRows<Q4<T>> in, M m, Q4<T>* __restrict__ out, int H, int W,
   // next), so their loads go out before this launch's dependency wait and
   // overlap the previous launch's tail; the state waits for it
   const bool pre = !BANDED && sizeof(T) == 8 && early;  // float32: measured no gain
-  if (pre) load_c(std::false_type{});
-  pdl_wait_and_release();
-  if (inner) {  // warp-uniform: a band's warps away from its edges skip the selects
-    if (!pre) load_c(std::false_type{});
-    load_s(std::false_type{});
-  } else if constexpr (BANDED) {
-    load_c(std::true_type{});
-    load_s(std::true_type{});
+  if constexpr (M::kTma) {
+    // TMA form (whole sensor, float64): the region's constants and state come
+    // in as two 2-D boxes (RH rows x 32 pixels; the box's part off the sensor
+    // is zero-filled and never read) issued by one thread, the constants
+    // before the dependency wait when early
+    static_assert(!BANDED && !CL && sizeof(T) == 8, "TMA tiles: whole-sensor float64");
+    extern __shared__ __align__(128) unsigned char tma_dyn[];
+    Q4<T>* const s_st = reinterpret_cast<Q4<T>*>(tma_dyn);  // RH x 32 quads
+    Q4<T>* const s_c = s_st + RH * 32;                     // RH x 32 x 2 quads
+    __shared__ uint64_t t_bar;
+    const int x0 = gj - l, yr0 = gi0 - g * RPT;
+    if (threadIdx.x == 0) {
+      cl_bar_init(&t_bar);
+      cl_fence_init();
+      cl_expect(&t_bar, RH * 32 * 3 * sizeof(Q4<T>));
+      if (pre) tma_load_2d(s_c, &m.tc, 8 * x0, yr0, &t_bar);
+    }
+    pdl_wait_and_release();
+    if (threadIdx.x == 0) {
+      if (!pre) tma_load_2d(s_c, &m.tc, 8 * x0, yr0, &t_bar);
+      tma_load_2d(s_st, &m.ts, 4 * x0, yr0, &t_bar);
+    }
+    __syncthreads();  // the barrier's init before anyone waits on it
+    cl_wait(&t_bar, 0);
+    // a region pixel off the sensor takes its clamped pixel (inside the box),
+    // as the global-load form does: its halo values stay finite, so no warp
+    // drops to the IEEE slow paths
+#pragma unroll
+    for (int r = 0; r < RPT; ++r) {
+      const int k = (min(max(gi0 + r, 0), H - 1) - yr0) * 32 + (jc - x0);
+      const Q4<T> q = s_st[k];
+      p1[r] = q.x;
+      p2[r] = q.y;
+      p3[r] = q.z;
+      u[r] = q.w;
+      craw[r] = typename M::Raw{s_c[2 * k], s_c[2 * k + 1]};
+    }
+  } else {
+    if (pre) load_c(std::false_type{});
+    pdl_wait_and_release();
+    if (inner) {  // warp-uniform: a band's warps away from its edges skip the selects
+      if (!pre) load_c(std::false_type{});
+      load_s(std::false_type{});
+    } else if constexpr (BANDED) {
+      load_c(std::true_type{});
+      load_s(std::true_type{});
+    }
   }
 #pragma unroll
   for (int r = 0; r < RPT; ++r) {

@@ -1,9 +1,10 @@
-"""Clustered primal-dual tiles (k_pd_tile<..., CX, CY>, EVR_TILE_CLUSTER):
-the region of a thread-block cluster, neighbour values crossing between its
-CTAs through DSMEM each half-step, must give the oracle's bits exactly --
-chained packets at the headline shape and at 640x480, K = 3 and 4, every
-cluster shape.  The switch is read once per process, so each case runs in a
-subprocess."""
+"""The opt-in forms of the primal-dual tile must give the oracle's bits
+exactly -- chained packets at the headline shape and at 640x480, K = 3 and 4:
+clustered tiles (k_pd_tile<..., CX, CY>, EVR_TILE_CLUSTER; the region of a
+thread-block cluster, neighbour values crossing between its CTAs through
+DSMEM each half-step) for every cluster shape, and TMA tiles (EVR_TILE_TMA;
+the region loaded as two 2-D tensor boxes, off-sensor pixels zero-filled).
+The switches are read once per process, so each case runs in a subprocess."""
 
 import os
 import subprocess
@@ -40,11 +41,15 @@ SCRIPT = textwrap.dedent("""
 """)
 
 
-@pytest.mark.parametrize("shape", ["2x2", "4x2", "2x4"])
+@pytest.mark.parametrize("variant", ["cluster2x2", "cluster4x2", "cluster2x4", "tma"])
 @pytest.mark.parametrize("K", [3, 4])
 @pytest.mark.parametrize("H,W,n", [(720, 1280, 2), (480, 640, 3)])
-def test_clustered_tiles_bit_exact(shape, K, H, W, n):
-    env = dict(os.environ, EVR_TILE_CLUSTER=shape, EVR_TILE_K=str(K))
+def test_tile_variants_bit_exact(variant, K, H, W, n):
+    env = dict(os.environ, EVR_TILE_K=str(K))
+    if variant == "tma":
+        env["EVR_TILE_TMA"] = "1"
+    else:
+        env["EVR_TILE_CLUSTER"] = variant[len("cluster"):]
     r = subprocess.run([sys.executable, "-c", SCRIPT, str(H), str(W), str(n)], cwd=ROOT, env=env,
                        capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-4000:]
