@@ -45,3 +45,19 @@ def test_bench_line_contract(config):
     from bench import workload_config
 
     assert d["config"] == workload_config(config, "f64")
+
+
+def test_bench_bands_line():
+    """`--bands N` (the C5 row-band split) prints one strong-scaling line."""
+    d = _line("--config", "C5", "--bands", "2", "--steps", "3", "--warmup", "3")
+    assert d["scaling"] == "strong" and d["value"] > 0 and d["ms_per_step"] > 0
+    assert d["config"]["sensor"] == "2048x2048"
+
+
+@pytest.mark.parametrize("variant", ["rof", "l1", "tgv"])
+def test_bench_variant_line(variant):
+    """`--variant` (the operator-level solves of configs[1]) prints one line
+    with its C-port baseline."""
+    d = _line("--config", "C2", "--variant", variant, "--steps", "3", "--warmup", "3")
+    assert d["value"] > 0 and d["ms_per_step"] > 0
+    assert d["cpu_baseline"]["value"] > 0
