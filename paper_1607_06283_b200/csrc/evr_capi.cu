@@ -1051,7 +1051,6 @@ template <class T> int resident_alloc(evr_ctx* ctx) {
   cudaFree(ctx->d_xchg);
   cudaFree(ctx->d_ticket);
   cudaFree(ctx->d_rx);
-  cudaFree(ctx->d_rx);
   ctx->d_rx = nullptr;
   ctx->d_flags = nullptr;
   ctx->d_xchg = nullptr;
