@@ -166,12 +166,15 @@ def uniform_packets(H, W, n_packets, epp, seed, t_step):
 @pytest.mark.parametrize("engine", ENGINES)
 @pytest.mark.parametrize("H,W,epp,iters", [(260, 346, 500, 50), (128, 128, 500, 50),
                                            (33, 70, 1500, 17), (500, 200, 700, 20),
-                                           (140, 600, 500, 12)])
+                                           (140, 600, 500, 12), (296, 512, 500, 20),
+                                           (148, 512, 500, 20)])
 def test_full_size_chained_vs_oracle(H, W, epp, iters, engine):
     """DAVIS346 / DVS128 generator-U streams, plus a packet
     larger than one ingest chunk: bit-exact with the C oracle, chained.  The
     resident engine runs its column kernel (bands <= 2 rows, W <= 512) on
-    the first three shapes and its plane-frame kernel on the last two."""
+    the first three shapes and the last two (its largest shapes: 148 CTAs of
+    512 threads, bands of 2 and 1 rows) and its plane-frame kernel on the
+    other two."""
     sc = evr.SolverConfig(max_iterations=iters)
     st = evr.init_state(evr.SensorGeometry(W, H), sc, precision=0, engine=engine_id(engine))
     ref = O.OracleStream(H, W, O.make_config(max_iterations=iters))
